@@ -1,0 +1,150 @@
+/*
+ * askv.h — C ABI of the B200 (sm_100a) AttentionStore KV-reuse prefill path.
+ *
+ * The reference (kvsim 0.1.0, /root/reference/pkg/src/kvsim) is pure Python
+ * with no FFI; each entry point below names the reference interface whose
+ * behaviour it implements for the hot path.  The Python host
+ * package paper_2403_19708_b200 binds these with ctypes.
+ *
+ * Conventions
+ *   - plain pointers and sizes; bf16 tensors are passed as void* (2-byte
+ *     elements), device or pinned-host as documented per argument;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream);
+ *   - no allocation and no device synchronisation inside any call;
+ *   - return 0 on success, ASKV_EINVAL for argument errors (ValueError in the
+ *     Python shim), ASKV_ECUDA for CUDA launch/runtime errors (RuntimeError),
+ *     ASKV_EUNSUPPORTED for shapes the kernels are not built for;
+ *     askv_last_error() returns the message of the calling thread's last error;
+ *   - deterministic: no atomics in reductions, fixed split-KV combine order.
+ *
+ * KV row layout (device and host): one token = [2][Hkv][head_dim] bf16,
+ * K then V, "pre-RoPE" (keys stored before positional encoding).
+ * Host arena: block b of a session holds `block_tokens` rows per layer;
+ * the (block, layer) chunk is contiguous at host_base + block_id*block_bytes
+ * + layer*chunk_bytes, chunk_bytes = block_tokens * row_bytes.
+ */
+#ifndef ASKV_H_
+#define ASKV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ASKV_OK 0
+#define ASKV_EINVAL (-1)
+#define ASKV_ECUDA (-2)
+#define ASKV_EUNSUPPORTED (-3)
+
+/* ABI version (major*100 + minor). */
+int askv_version(void);
+
+/* Message for the last non-zero return on this thread ("" if none). */
+const char* askv_last_error(void);
+
+/*
+ * RoPE cos/sin table, computed in float64 and stored as float32 pairs:
+ * table[p*(head_dim/2) + i] = (cos(p*theta^(-2i/d)), sin(...)), p in [0, max_pos).
+ * Replaces: rope.py:55-60 (_pair_angles) + the cos/sin of rope.py:67-68.
+ * table: device float[2*max_pos*(head_dim/2)].
+ */
+int askv_rope_table(float* table, int max_pos, int head_dim, double theta_base, void* stream);
+
+/*
+ * K2 — fused gather + truncate + re-embed of one layer of a session's cached
+ * pre-RoPE K/V.  Row i (0 <= i < kept) is session token (first_token + i);
+ * its source row lives in block (first_token+i)/block_tokens of `src_block_off`
+ * (element offsets from src_base, device int64 array), or, when src_block_off
+ * is NULL, at src_base + (first_token+i)*src_row_stride.  K is rotated at
+ * position positions[i] (device int32; NULL = the compacted positions pos0 + i
+ * used after truncation, rope.py:263-266) and written with V to
+ * dst + i*dst_row_stride.  Truncation = the caller starts at first_token
+ * (multiple of block_tokens after whole-block drops) and passes `kept`.
+ * Replaces: rope.py:63-74 (rotate_matrix) at rope.py:138, KvRecord.truncated
+ * rope.py:48-52, and the kept range of sim.py:468-483.
+ * src/dst: device bf16.  Strides in elements.
+ */
+int askv_reembed(const void* src_base, const int64_t* src_block_off, int block_tokens,
+                 int64_t src_row_stride, int64_t first_token, int kept, int n_kv_heads,
+                 int head_dim, const float* rope_table, int table_positions,
+                 const int32_t* positions, int pos0, void* dst, int64_t dst_row_stride,
+                 void* stream);
+
+/*
+ * Rotate every head of n_rows rows x[i] = [heads][hd] at positions[i]
+ * (device int32, or pos0 + i when NULL) into out[i].
+ * Replaces: rope.py:63-74 (rotate_matrix) / rope.py:77-85 (rope_rotate).
+ */
+int askv_rotate_rows(const void* x, int64_t x_row_stride, int n_rows, int n_heads,
+                     int head_dim, const float* rope_table, int table_positions,
+                     const int32_t* positions, int pos0, void* out, int64_t out_row_stride,
+                     void* stream);
+
+/*
+ * New-token epilogue of the QKV projection: for token i < n_new of
+ * qkv[i] = [q (Hq*hd) | k (Hkv*hd) | v (Hkv*hd)] (row stride qkv_row_stride):
+ *   q_out[i]  = rope(q, pos0+i)            layout [n_new][Hq][hd]
+ *   kv_out[i] = [rope(k, pos0+i) | v]      row i of a [rows][2][Hkv][hd] buffer
+ *   save_out[i] = [k | v] pre-RoPE         (may be NULL)
+ * Replaces: rope.py:139-140 (rotation of new k and q) and the paper's
+ * "cache k, v before apply_pos_emb" order.
+ */
+int askv_rope_new(const void* qkv, int64_t qkv_row_stride, int n_new, int n_heads,
+                  int n_kv_heads, int head_dim, const float* rope_table, int table_positions,
+                  int pos0, void* q_out, void* kv_out, int64_t kv_row_stride, void* save_out,
+                  void* stream);
+
+/*
+ * K3 — prefill attention over [reused prefix | new tokens] on tcgen05/TMEM,
+ * TMA-fed, split-KV + deterministic combine when the grid is short.
+ *   q   : [n_new][Hq][hd] bf16 (already rotated)
+ *   kv  : [n_cached+n_new][2][Hkv][hd] bf16 rows (K rotated), row stride kv_row_stride
+ *   out : [n_new][Hq][hd] bf16
+ * Query i sees keys j <= n_cached + i; q-head h uses kv-head h/(Hq/Hkv).
+ * scale = 1/sqrt(hd) reproduces rope.py:98.  num_splits = 0 picks a split count
+ * for the SM count; workspace must hold askv_attn_workspace_bytes(...).
+ * Replaces: rope.py:94-105 (_causal_attention) inside rope.py:118-144.
+ */
+int askv_prefill_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cached,
+                      int n_new, int n_heads, int n_kv_heads, int head_dim, float scale,
+                      void* out, void* workspace, size_t workspace_bytes, int num_splits,
+                      void* stream);
+size_t askv_attn_workspace_bytes(int n_cached, int n_new, int n_heads, int head_dim,
+                                 int num_splits);
+/* Split count the auto policy would use (for reporting / tests). */
+int askv_attn_num_splits(int n_cached, int n_new, int n_heads, int sm_count);
+
+/*
+ * K1 — layer-wise pre-loader: H2D of one layer's kept blocks of one session
+ * from the pinned host arena into a contiguous HBM read-buffer slot:
+ *   dst + i*chunk_bytes <- host_base + block_ids[i]*block_bytes + layer_off
+ * for i < nblocks (the last copy carries tail_bytes, 0 = full chunk), issued
+ * as one batch on `stream`; records `done_event` (cudaEvent_t, may be NULL).
+ * block_ids is a host array.
+ * Replaces: the load stream of overlap.py:69-123 (plan_preload) as called from
+ * sim.py:436-442.
+ */
+int askv_preload_layer(void* dst, const void* host_base, const int64_t* block_ids,
+                       int nblocks, int64_t block_bytes, int64_t layer_off,
+                       int64_t chunk_bytes, int64_t tail_bytes, void* stream,
+                       void* done_event);
+
+/*
+ * K4 — layer-wise asynchronous saver: D2H of n_tokens new rows (contiguous
+ * [n][row_bytes] at src, device) into the session's host blocks, starting at
+ * session token `first_token` (block block_ids[t/block_tokens], row
+ * t%block_tokens, layer offset layer_off).  One batch on `stream`; records
+ * `done_event` if non-NULL.  block_ids is a host array covering the tail.
+ * Replaces: overlap.py:126-200 (plan_async_save) and the save of sim.py:532-555.
+ */
+int askv_save_layer(void* host_base, const int64_t* block_ids, int nblocks,
+                    int64_t block_bytes, int64_t layer_off, int block_tokens,
+                    int64_t row_bytes, int64_t first_token, int n_tokens, const void* src,
+                    void* stream, void* done_event);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ASKV_H_ */

@@ -1,0 +1,277 @@
+// RoPE-side kernels of the KV-reuse prefill path (sm_100a).
+//
+//   askv_rope_table : fp64-derived cos/sin table           (rope.py:55-60, 67-68)
+//   askv_reembed    : K2 gather + truncate + re-embed       (rope.py:48-52, 63-74, 138;
+//                                                            sim.py:468-483)
+//   askv_rope_new   : new-token q/k rotation + pre-RoPE save copy (rope.py:139-140;
+//                                                            PAPER.md:416-420)
+//
+// All three are HBM-bound elementwise kernels: each thread moves one 16-byte
+// vector (8 bf16 = 4 interleaved rotation pairs), loads are read-only
+// non-allocating, and the grid is a multiple of the SM count with a
+// grid-stride loop.  The cos/sin table (<= a few MB) stays L2-resident.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "askv_internal.h"
+
+namespace askv {
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ int4 ld_nc16(const void* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st16(void* p, int4 v) {
+  asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// Rotate the 4 interleaved pairs of a 16-byte bf16 vector by table entries
+// cs[0..7] = (cos0, sin0, cos1, sin1, ...).
+__device__ __forceinline__ int4 rotate8(int4 x, const float* cs) {
+  const float4 a = *reinterpret_cast<const float4*>(cs);
+  const float4 b = *reinterpret_cast<const float4*>(cs + 4);
+  const float c[4] = {a.x, a.z, b.x, b.z};
+  const float s[4] = {a.y, a.w, b.y, b.w};
+  uint32_t w[4] = {(uint32_t)x.x, (uint32_t)x.y, (uint32_t)x.z, (uint32_t)x.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    __nv_bfloat162 p = *reinterpret_cast<__nv_bfloat162*>(&w[k]);
+    const float e = __bfloat162float(p.x), o = __bfloat162float(p.y);
+    const float r0 = fmaf(e, c[k], -(o * s[k]));
+    const float r1 = fmaf(e, s[k], o * c[k]);
+    __nv_bfloat162 q = __floats2bfloat162_rn(r0, r1);
+    w[k] = *reinterpret_cast<uint32_t*>(&q);
+  }
+  return make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
+}
+
+__global__ void rope_table_kernel(float* __restrict__ table, int max_pos, int half,
+                                  double theta_base, int head_dim) {
+  const int64_t total = (int64_t)max_pos * half;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int p = (int)(g / half);
+    const int i = (int)(g - (int64_t)p * half);
+    const double inv = pow(theta_base, -(2.0 * i) / (double)head_dim);
+    double s, c;
+    sincos((double)p * inv, &s, &c);
+    table[2 * g] = (float)c;
+    table[2 * g + 1] = (float)s;
+  }
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kThreads)
+    reembed_kernel(const __nv_bfloat16* __restrict__ src, const int64_t* __restrict__ blk_off,
+                   int block_tokens, int64_t src_row_stride, int64_t first_token, int kept,
+                   int hkv, const float* __restrict__ table, const int32_t* __restrict__ positions,
+                   int pos0, __nv_bfloat16* __restrict__ dst, int64_t dst_row_stride) {
+  constexpr int kUnitsPerHead = HD / 8;
+  const int k_units = hkv * kUnitsPerHead;
+  const int row_units = 2 * k_units;
+  const int64_t total = (int64_t)kept * row_units;
+  for (int64_t g = blockIdx.x * (int64_t)kThreads + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * kThreads) {
+    const int i = (int)(g / row_units);
+    const int u = (int)(g - (int64_t)i * row_units);
+    const int64_t t = first_token + i;
+    const __nv_bfloat16* srow;
+    if (blk_off != nullptr) {
+      const int64_t b = t / block_tokens;
+      srow = src + blk_off[b] + (t - b * block_tokens) * src_row_stride;
+    } else {
+      srow = src + t * src_row_stride;
+    }
+    int4 v = ld_nc16(srow + u * 8);
+    if (u < k_units) {
+      const int d0 = (u % kUnitsPerHead) * 8;
+      const int pos = positions ? positions[i] : pos0 + i;
+      const float* cs = table + ((int64_t)pos * (HD / 2) + d0 / 2) * 2;
+      v = rotate8(v, cs);
+    }
+    st16(dst + (int64_t)i * dst_row_stride + u * 8, v);
+  }
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kThreads)
+    rope_new_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t qkv_row_stride, int n_new,
+                    int hq, int hkv, const float* __restrict__ table, int pos0,
+                    __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ kv_out,
+                    int64_t kv_row_stride, __nv_bfloat16* __restrict__ save_out) {
+  constexpr int kUnitsPerHead = HD / 8;
+  const int q_units = hq * kUnitsPerHead;
+  const int k_units = hkv * kUnitsPerHead;
+  const int row_units = q_units + 2 * k_units;
+  const int64_t total = (int64_t)n_new * row_units;
+  for (int64_t g = blockIdx.x * (int64_t)kThreads + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * kThreads) {
+    const int i = (int)(g / row_units);
+    const int u = (int)(g - (int64_t)i * row_units);
+    const int4 x = ld_nc16(qkv + (int64_t)i * qkv_row_stride + u * 8);
+    const int d0 = (u % kUnitsPerHead) * 8;
+    const float* cs = table + ((int64_t)(pos0 + i) * (HD / 2) + d0 / 2) * 2;
+    if (u < q_units) {
+      st16(q_out + (int64_t)i * q_units * 8 + u * 8, rotate8(x, cs));
+    } else {
+      const int ku = u - q_units;  // [0, 2*k_units): K then V, same as the row layout
+      if (save_out != nullptr) st16(save_out + (int64_t)i * 2 * k_units * 8 + ku * 8, x);
+      st16(kv_out + (int64_t)i * kv_row_stride + ku * 8, ku < k_units ? rotate8(x, cs) : x);
+    }
+  }
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kThreads)
+    rotate_rows_kernel(const __nv_bfloat16* __restrict__ x, int64_t x_row_stride, int n_rows,
+                       int heads, const float* __restrict__ table,
+                       const int32_t* __restrict__ positions, int pos0,
+                       __nv_bfloat16* __restrict__ out, int64_t out_row_stride) {
+  constexpr int kUnitsPerHead = HD / 8;
+  const int row_units = heads * kUnitsPerHead;
+  const int64_t total = (int64_t)n_rows * row_units;
+  for (int64_t g = blockIdx.x * (int64_t)kThreads + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * kThreads) {
+    const int i = (int)(g / row_units);
+    const int u = (int)(g - (int64_t)i * row_units);
+    const int pos = positions ? positions[i] : pos0 + i;
+    const float* cs = table + ((int64_t)pos * (HD / 2) + (u % kUnitsPerHead) * 4) * 2;
+    st16(out + (int64_t)i * out_row_stride + u * 8,
+         rotate8(ld_nc16(x + (int64_t)i * x_row_stride + u * 8), cs));
+  }
+}
+
+int grid_for(int64_t units) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (units + kThreads - 1) / kThreads;
+  const int64_t cap = (int64_t)sms * 8;  // 8 x 256 threads resident per SM
+  return (int)(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+}  // namespace
+}  // namespace askv
+
+using namespace askv;
+
+extern "C" int askv_rope_table(float* table, int max_pos, int head_dim, double theta_base,
+                               void* stream) {
+  clear_error();
+  ASKV_REQUIRE(table != nullptr, "rope_table: null table");
+  ASKV_REQUIRE(max_pos > 0 && head_dim > 0 && head_dim % 2 == 0,
+               "rope_table: bad max_pos=%d head_dim=%d (head_dim must be even)", max_pos,
+               head_dim);
+  const int half = head_dim / 2;
+  const int64_t total = (int64_t)max_pos * half;
+  int blocks = (int)((total + kThreads - 1) / kThreads);
+  if (blocks > 4096) blocks = 4096;
+  rope_table_kernel<<<blocks, kThreads, 0, (cudaStream_t)stream>>>(table, max_pos, half,
+                                                                   theta_base, head_dim);
+  return launch_status("rope_table launch");
+}
+
+extern "C" int askv_reembed(const void* src_base, const int64_t* src_block_off,
+                            int block_tokens, int64_t src_row_stride, int64_t first_token,
+                            int kept, int n_kv_heads, int head_dim, const float* rope_table,
+                            int table_positions, const int32_t* positions, int pos0, void* dst,
+                            int64_t dst_row_stride, void* stream) {
+  clear_error();
+  ASKV_REQUIRE(kept >= 0 && n_kv_heads > 0 && first_token >= 0 && pos0 >= 0,
+               "reembed: bad kept=%d hkv=%d first_token=%lld pos0=%d", kept, n_kv_heads,
+               (long long)first_token, pos0);
+  ASKV_REQUIRE(head_dim == 64 || head_dim == 128, "reembed: head_dim %d unsupported",
+               head_dim);
+  ASKV_REQUIRE(src_block_off == nullptr || block_tokens > 0, "reembed: block_tokens <= 0");
+  ASKV_REQUIRE(positions != nullptr || pos0 + kept <= table_positions,
+               "reembed: positions up to %d exceed rope table (%d)", pos0 + kept,
+               table_positions);
+  ASKV_REQUIRE(src_row_stride % 8 == 0 && dst_row_stride % 8 == 0,
+               "reembed: row strides must be multiples of 8 elements");
+  if (kept == 0) return ASKV_OK;
+  ASKV_REQUIRE(src_base && dst && rope_table, "reembed: null pointer");
+  const int64_t units = (int64_t)kept * 2 * n_kv_heads * (head_dim / 8);
+  const int grid = grid_for(units);
+  auto* s = static_cast<const __nv_bfloat16*>(src_base);
+  auto* d = static_cast<__nv_bfloat16*>(dst);
+  if (head_dim == 128)
+    reembed_kernel<128><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+        s, src_block_off, block_tokens, src_row_stride, first_token, kept, n_kv_heads,
+        rope_table, positions, pos0, d, dst_row_stride);
+  else
+    reembed_kernel<64><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+        s, src_block_off, block_tokens, src_row_stride, first_token, kept, n_kv_heads,
+        rope_table, positions, pos0, d, dst_row_stride);
+  return launch_status("reembed launch");
+}
+
+extern "C" int askv_rope_new(const void* qkv, int64_t qkv_row_stride, int n_new, int n_heads,
+                             int n_kv_heads, int head_dim, const float* rope_table,
+                             int table_positions, int pos0, void* q_out, void* kv_out,
+                             int64_t kv_row_stride, void* save_out, void* stream) {
+  clear_error();
+  ASKV_REQUIRE(n_new >= 0 && n_heads > 0 && n_kv_heads > 0 && n_heads % n_kv_heads == 0,
+               "rope_new: bad n_new=%d hq=%d hkv=%d", n_new, n_heads, n_kv_heads);
+  ASKV_REQUIRE(head_dim == 64 || head_dim == 128, "rope_new: head_dim %d unsupported",
+               head_dim);
+  ASKV_REQUIRE(pos0 >= 0 && pos0 + n_new <= table_positions,
+               "rope_new: positions up to %d exceed rope table (%d)", pos0 + n_new,
+               table_positions);
+  ASKV_REQUIRE(qkv_row_stride % 8 == 0 && kv_row_stride % 8 == 0,
+               "rope_new: row strides must be multiples of 8 elements");
+  if (n_new == 0) return ASKV_OK;
+  ASKV_REQUIRE(qkv && q_out && kv_out && rope_table, "rope_new: null pointer");
+  const int64_t units = (int64_t)n_new * (n_heads + 2 * n_kv_heads) * (head_dim / 8);
+  const int grid = grid_for(units);
+  auto* x = static_cast<const __nv_bfloat16*>(qkv);
+  auto* qo = static_cast<__nv_bfloat16*>(q_out);
+  auto* kvo = static_cast<__nv_bfloat16*>(kv_out);
+  auto* so = static_cast<__nv_bfloat16*>(save_out);
+  if (head_dim == 128)
+    rope_new_kernel<128><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+        x, qkv_row_stride, n_new, n_heads, n_kv_heads, rope_table, pos0, qo, kvo,
+        kv_row_stride, so);
+  else
+    rope_new_kernel<64><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+        x, qkv_row_stride, n_new, n_heads, n_kv_heads, rope_table, pos0, qo, kvo,
+        kv_row_stride, so);
+  return launch_status("rope_new launch");
+}
+
+extern "C" int askv_rotate_rows(const void* x, int64_t x_row_stride, int n_rows, int n_heads,
+                                int head_dim, const float* rope_table, int table_positions,
+                                const int32_t* positions, int pos0, void* out,
+                                int64_t out_row_stride, void* stream) {
+  clear_error();
+  ASKV_REQUIRE(n_rows >= 0 && n_heads > 0, "rotate_rows: bad n_rows=%d heads=%d", n_rows,
+               n_heads);
+  ASKV_REQUIRE(head_dim == 64 || head_dim == 128, "rotate_rows: head_dim %d unsupported",
+               head_dim);
+  ASKV_REQUIRE(positions != nullptr || (pos0 >= 0 && pos0 + n_rows <= table_positions),
+               "rotate_rows: positions up to %d exceed rope table (%d)", pos0 + n_rows,
+               table_positions);
+  ASKV_REQUIRE(x_row_stride % 8 == 0 && out_row_stride % 8 == 0,
+               "rotate_rows: row strides must be multiples of 8 elements");
+  if (n_rows == 0) return ASKV_OK;
+  ASKV_REQUIRE(x && out && rope_table, "rotate_rows: null pointer");
+  const int grid = grid_for((int64_t)n_rows * n_heads * (head_dim / 8));
+  auto* xi = static_cast<const __nv_bfloat16*>(x);
+  auto* o = static_cast<__nv_bfloat16*>(out);
+  if (head_dim == 128)
+    rotate_rows_kernel<128><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+        xi, x_row_stride, n_rows, n_heads, rope_table, positions, pos0, o, out_row_stride);
+  else
+    rotate_rows_kernel<64><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+        xi, x_row_stride, n_rows, n_heads, rope_table, positions, pos0, o, out_row_stride);
+  return launch_status("rotate_rows launch");
+}

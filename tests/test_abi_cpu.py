@@ -1,0 +1,65 @@
+"""The C-ABI library loads without a GPU and exports every symbol include/askv.h
+declares; the ctypes signature table covers exactly those symbols."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def declared():
+    text = (ROOT / "include" / "askv.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(askv_[a-z0-9_]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def built():
+    from paper_2403_19708_b200 import build
+    return build.build()
+
+
+def test_header_declares_hot_path_entry_points():
+    names = declared()
+    for fn in ("askv_reembed", "askv_prefill_attn", "askv_preload_layer", "askv_save_layer",
+               "askv_rope_new", "askv_version"):
+        assert fn in names
+
+
+def test_library_exports_every_declared_symbol(built):
+    lib = ctypes.CDLL(str(built))
+    for name in declared():
+        assert hasattr(lib, name), name
+
+
+def test_ctypes_table_matches_header(built):
+    from paper_2403_19708_b200 import _lib
+    assert sorted(_lib.SIGNATURES) == declared()
+    lib = _lib.lib()
+    assert lib.askv_version() == 100
+    assert lib.askv_last_error() == b""
+
+
+def test_split_policy_without_gpu(built):
+    from paper_2403_19708_b200 import _lib
+    lib = _lib.lib()
+    # 13B p50 turn (kept 2142, new 237, 40 heads): short grid -> split-KV
+    s = lib.askv_attn_num_splits(2142, 237, 40, 148)
+    assert 2 <= s <= 8
+    # full recompute of 2379 tokens fills the machine without splitting
+    assert lib.askv_attn_num_splits(0, 2379, 40, 148) == 1
+    assert lib.askv_attn_workspace_bytes(2142, 237, 40, 128, 4) == 4 * 237 * 40 * 129 * 4
+
+
+def test_argument_errors_without_gpu(built):
+    """Validation happens before any CUDA call, so it is testable on CPU."""
+    from paper_2403_19708_b200 import _lib
+    lib = _lib.lib()
+    rc = lib.askv_prefill_attn(None, None, 256, 0, 4, 3, 2, 128, 1.0, None, None, 0, 0, None)
+    assert rc == _lib.ASKV_EINVAL
+    assert b"multiple" in lib.askv_last_error()
+    rc = lib.askv_save_layer(None, None, 1, 100, 0, 16, 8, 0, 40, None, None, None)
+    assert rc == _lib.ASKV_EINVAL
