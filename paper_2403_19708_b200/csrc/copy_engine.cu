@@ -37,8 +37,11 @@ void clear_error() { g_last_error.clear(); }
 namespace {
 
 // Issue a list of same-direction copies in stream order.
+// Pointers are UVA-classified (cudaMemcpyDefault), so the same entry points
+// serve a pinned-host arena (H2D / D2H over the host link) and an
+// HBM-resident arena (D2D).
 int issue_batch(std::vector<void*>& dsts, std::vector<void*>& srcs, std::vector<size_t>& sizes,
-                cudaStream_t stream, bool h2d) {
+                cudaStream_t stream) {
   if (dsts.empty()) return ASKV_OK;
   cudaMemcpyAttributes attr = {};
   attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
@@ -51,8 +54,7 @@ int issue_batch(std::vector<void*>& dsts, std::vector<void*>& srcs, std::vector<
   // Batch API unavailable (older driver): same segments, one call each.
   (void)cudaGetLastError();
   for (size_t i = 0; i < dsts.size(); ++i) {
-    e = cudaMemcpyAsync(dsts[i], srcs[i], sizes[i],
-                        h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, stream);
+    e = cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDefault, stream);
     if (e != cudaSuccess) return cuda_status(e, "cudaMemcpyAsync");
   }
   return ASKV_OK;
@@ -88,7 +90,7 @@ extern "C" int askv_preload_layer(void* dst, const void* host_base, const int64_
     s[i] = const_cast<char*>(hb + block_ids[i] * block_bytes + layer_off);
     n[i] = (size_t)((i == nblocks - 1 && tail_bytes > 0) ? tail_bytes : chunk_bytes);
   }
-  int rc = issue_batch(d, s, n, (cudaStream_t)stream, true);
+  int rc = issue_batch(d, s, n, (cudaStream_t)stream);
   if (rc) return rc;
   if (done_event)
     return cuda_status(cudaEventRecord((cudaEvent_t)done_event, (cudaStream_t)stream),
@@ -127,7 +129,7 @@ extern "C" int askv_save_layer(void* host_base, const int64_t* block_ids, int nb
     n.push_back((size_t)(cnt * row_bytes));
     t += cnt;
   }
-  int rc = issue_batch(d, s, n, (cudaStream_t)stream, false);
+  int rc = issue_batch(d, s, n, (cudaStream_t)stream);
   if (rc) return rc;
   if (done_event)
     return cuda_status(cudaEventRecord((cudaEvent_t)done_event, (cudaStream_t)stream),

@@ -1,0 +1,150 @@
+"""Multi-turn serving loop: the reference simulator's job start / finish
+semantics driving the real B200 runner.
+
+Reference call sites (sim.py):
+  _start_job   :408-466  overflow truncation -> store lookup -> reuse or recompute
+  _handle_overflow :468-483   drop `cut` tokens from the front until it fits
+  _finish_job  :519-565  save-time truncation -> save (computed tokens)
+  _truncate_tokens :576-581
+
+Differences from the simulator, by design: time is real (CUDA events), the
+KV bytes are real (pinned host arena blocks), and output tokens' KV — produced
+by decode in a real server, which is outside the prefill hot path — is
+produced here by a teacher-forced append prefill of the supplied output ids so
+the next turn finds a complete history (SURVEY.md §7.2 "Output tokens' KV").
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from .model import LlamaShape, TierConfig, profile_for
+from .runner import Job, JobResult, LlamaWeights, Runner
+from .store import HitClass, HostArena, KvStore
+
+
+def overflow_kept(hist: int, new: int, window: int, cut: int) -> int:
+    """Kept history after load-time truncation, closed form of sim.py:471-474:
+    the number of `cut` chunks dropped is ceil((hist + new - W) / cut)."""
+    if hist + new <= window:
+        return hist
+    m = -(-(hist + new - window) // cut)
+    return max(0, hist - m * cut)
+
+
+def save_truncate(tokens: int, window: int, cut: int) -> int:
+    """sim.py:576-581 in closed form."""
+    if tokens <= window:
+        return max(tokens, 0)
+    return tokens - cut * (-(-(tokens - window) // cut))
+
+
+@dataclass
+class TurnOutcome:
+    session_id: str
+    turn: int
+    hit: str
+    kept: int
+    drop: int
+    new: int
+    prompt: int
+    overflowed: bool
+    result: JobResult          # the prefill of the new input tokens (TTFT job)
+    append: JobResult | None   # teacher-forced append of output tokens
+
+
+class Engine:
+    def __init__(self, shape: LlamaShape, *, host_blocks: int, block_tokens: int = 128,
+                 device="cuda", seed: int = 0, weights: LlamaWeights | None = None,
+                 read_buffer_bytes: int = 1 << 30, max_new: int = 1024,
+                 truncation_ratio: float = 0.5, ttl: float = math.inf, pin: bool = True):
+        self.shape = shape
+        self.profile = profile_for(shape, truncation_ratio=truncation_ratio)
+        self.block_tokens = block_tokens
+        block_bytes = block_tokens * shape.kv_bytes_per_token
+        self.arena = HostArena(host_blocks, block_bytes, pin=pin)
+        tiers = TierConfig(dram_capacity=host_blocks * block_bytes, disk_capacity=0)
+        self.store = KvStore(self.profile, tiers, block_bytes=block_bytes, ttl=ttl,
+                             evictor=self._make_room, arena=self.arena,
+                             block_tokens=block_tokens)
+        self.runner = Runner(shape, weights=weights, device=device, seed=seed,
+                             block_tokens=block_tokens, host_arena=self.arena,
+                             read_buffer_bytes=read_buffer_bytes,
+                             max_new=shape.context_window + max_new,
+                             max_ctx=shape.context_window + max_new)
+        self.window = shape.context_window
+        self.cut = self.profile.cut_tokens
+        self.context: dict[str, int] = {}
+        self.tokens: dict[str, torch.Tensor] = {}   # conversation token ids (for misses)
+
+    def _make_room(self, needed: float) -> None:
+        """Evict least-recently-used unpinned sessions (no disk tier here)."""
+        freed = 0.0
+        for it in sorted(self.store.memory_items(), key=lambda i: (i.last_access, i.seq)):
+            if freed >= needed:
+                break
+            if it.session_id in self.store.pinned:
+                continue
+            freed += self.store.charge(it.bytes)
+            self.store.remove(it.session_id)
+
+    def turn(self, sid: str, turn_index: int, new_ids: torch.Tensor,
+             out_ids: torch.Tensor | None = None, now: float = 0.0,
+             want_logits: bool = False) -> TurnOutcome:
+        new_ids = new_ids.reshape(-1).to(torch.int64)
+        hist = self.context.get(sid, 0)
+        new = int(new_ids.numel())
+        overflowed = hist + new > self.window
+        kept = hist
+        if overflowed:
+            kept = overflow_kept(hist, new, self.window, self.cut)
+            if self.store.peek(sid) is not None:
+                if kept == 0:
+                    self.store.remove(sid)
+                else:
+                    self.store.truncate_item(sid, kept, now)
+            self.context[sid] = kept
+            if sid in self.tokens:
+                self.tokens[sid] = self.tokens[sid][hist - kept:]
+        hit = HitClass.MISS
+        if turn_index > 0:
+            hit = self.store.lookup(sid, now)
+            if hit is not HitClass.MISS and self.store.peek(sid).tokens != kept:
+                self.store.remove(sid)
+                hit = HitClass.MISS
+        self.store.pinned.add(sid)
+        hist_ids = self.tokens.get(sid, torch.empty(0, dtype=torch.int64))
+        if hit is HitClass.MISS or kept == 0:
+            hit = HitClass.MISS
+            prompt_ids = torch.cat([hist_ids, new_ids])
+            ids = self.store.reserve_rows(sid, kept + new)
+            job = Job(sid, prompt_ids, kept=0, source="none", block_ids=ids, save=True,
+                      head=self.store.head_row(sid))
+        else:
+            ids = self.store.reserve_rows(sid, kept + new)
+            job = Job(sid, new_ids, kept=kept, source="host", block_ids=ids, save=True,
+                      head=self.store.head_row(sid))
+        res = self.runner.run([job], want_logits=want_logits)[0]
+        self.store.mark_written(sid, kept + new)
+        append = None
+        n_out = 0 if out_ids is None else int(out_ids.numel())
+        if n_out:
+            ids = self.store.reserve_rows(sid, kept + new + n_out)
+            ajob = Job(sid, out_ids.reshape(-1).to(torch.int64), kept=kept + new,
+                       source="host", block_ids=ids, save=True, head=self.store.head_row(sid))
+            append = self.runner.run([ajob])[0]
+            self.store.mark_written(sid, kept + new + n_out)
+        raw = kept + new + n_out
+        ctx = save_truncate(raw, self.window, self.cut)
+        all_ids = torch.cat([hist_ids, new_ids] + ([out_ids.reshape(-1).to(torch.int64)]
+                                                   if n_out else []))
+        self.tokens[sid] = all_ids[raw - ctx:]
+        self.context[sid] = ctx
+        if ctx > 0:
+            self.store.save(sid, ctx, now)
+        self.store.pinned.discard(sid)
+        return TurnOutcome(sid, turn_index, hit.value, kept, hist - kept, new, kept + new,
+                           overflowed, res, append)

@@ -1,0 +1,138 @@
+"""KvStore mirror (paper_2403_19708_b200.store) against the reference's golden
+dump_state sequence, plus block-table invariants of the physical arena, plus
+the closed-form truncation arithmetic against the oracle and golden grid."""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+from hypothesis import given, settings, strategies as st
+
+from oracle import layout_ref
+from paper_2403_19708_b200 import model
+from paper_2403_19708_b200.engine import overflow_kept, save_truncate
+from paper_2403_19708_b200.store import (HitClass, HostArena, ItemNotFoundError, KvStore,
+                                         StoreSizeError, Tier)
+
+G = Path(__file__).resolve().parent / "golden"
+
+
+def _profile(kvb, layers=2):
+    return model.ModelProfile(name="p", kv_bytes_per_token=float(kvb),
+                              prefill_seconds_per_token=1e-4, decode_seconds_per_step=1e-3,
+                              context_window=4096, layers=layers)
+
+
+@pytest.mark.parametrize("physical", [False, True])
+def test_store_matches_reference_dump_sequence(physical):
+    for case in json.loads((G / "store.json").read_text()):
+        prof = _profile(case["kv_bytes_per_token"])
+        tiers = model.TierConfig(dram_capacity=10**15, disk_capacity=10**15)
+        kw = {}
+        if physical:
+            if case["block_tokens"] > 64:   # keep the CPU arena small
+                continue
+            kw = dict(arena=HostArena(1200, case["block_bytes"], pin=False),
+                      block_tokens=case["block_tokens"])
+        stor = KvStore(prof, tiers, block_bytes=case["block_bytes"], **kw)
+        for (op, sid, tok, now), want in zip(case["ops"], case["dumps"]):
+            if op == "save":
+                if physical:
+                    stor.reserve_rows(sid, tok)
+                    stor.mark_written(sid, tok)
+                stor.save(sid, tok, now)
+            elif op == "truncate":
+                stor.truncate_item(sid, tok, now)
+            else:
+                stor.remove(sid)
+            stor.check_invariants()
+            assert json.loads(stor.dump_state()) == want
+
+
+def test_block_table_truncation_drops_front_blocks():
+    tb = 16
+    prof = model.ModelProfile(name="p", kv_bytes_per_token=1024.0, prefill_seconds_per_token=1e-4,
+                              decode_seconds_per_step=1e-3, context_window=64, layers=2)
+    arena = HostArena(64, tb * 1024, pin=False)
+    stor = KvStore(prof, model.TierConfig(dram_capacity=64 * tb * 1024, disk_capacity=0),
+                   block_bytes=tb * 1024, arena=arena, block_tokens=tb)
+    tab = stor.reserve_rows("s", 60)
+    stor.mark_written("s", 60)
+    stor.save("s", 60, 0.0)
+    assert len(tab) == 4
+    # load-time truncation: W=64, cut=32; hist 60 + new 10 -> kept 28 (drops 32 = 2 blocks)
+    kept = overflow_kept(60, 10, 64, 32)
+    assert kept == 28
+    stor.truncate_item("s", kept, 1.0)
+    assert stor.block_table("s") == tab[2:]
+    stor.check_invariants()
+    # the next save appends in place
+    tab2 = stor.reserve_rows("s", kept + 10)
+    assert tab2[:2] == tab[2:]
+    stor.mark_written("s", kept + 10)
+    stor.save("s", kept + 10, 2.0)
+    stor.check_invariants()
+    stor.remove("s")
+    assert arena.free_blocks == 64
+    with pytest.raises(ItemNotFoundError):
+        stor.remove("s")
+
+
+def test_physical_store_rejects_misaligned_blocks():
+    prof = _profile(100)
+    with pytest.raises(ValueError):
+        KvStore(prof, model.TierConfig(), block_bytes=3000 * 100,
+                arena=HostArena(1, 3000 * 100, pin=False), block_tokens=3000)
+
+
+def test_store_errors_and_ttl():
+    prof = _profile(1000)
+    stor = KvStore(prof, model.TierConfig(dram_capacity=10**9, disk_capacity=10**9),
+                   block_bytes=10**6, ttl=10.0)
+    with pytest.raises(ValueError):
+        stor.save("a", 0, 0.0)
+    with pytest.raises(StoreSizeError):
+        stor.save("a", 10**7, 0.0)
+    stor.save("a", 100, 0.0)
+    assert stor.lookup("a", 5.0) is HitClass.MEMORY_HIT
+    assert stor.lookup("a", 16.0) is HitClass.MISS       # expired and removed
+    assert stor.peek("a") is None
+    stor.save("b", 100, 0.0)
+    assert stor.move("b", Tier.DISK) == 100 * 1000
+    assert stor.lookup("b", 1.0) is HitClass.DISK_HIT
+
+
+@settings(max_examples=300, deadline=None)
+@given(hist=st.integers(0, 40000), new=st.integers(1, 9000),
+       w=st.sampled_from([64, 100, 2048, 4096]), ratio=st.sampled_from([0.25, 0.5, 0.75]))
+def test_closed_form_truncation_equals_reference_loops(hist, new, w, ratio):
+    cut = max(1, int(ratio * w))
+    assert overflow_kept(hist, new, w, cut) == layout_ref.overflow_kept(hist, new, w, ratio)
+    assert save_truncate(hist + new, w, cut) == layout_ref.save_truncate(hist + new, w, ratio)
+
+
+def test_closed_form_truncation_golden_grid():
+    for r in json.loads((G / "truncation.json").read_text()):
+        cut = max(1, int(r["ratio"] * r["W"]))
+        if "kept" in r:
+            assert overflow_kept(r["hist"], r["new"], r["W"], cut) == r["kept"]
+        else:
+            assert save_truncate(r["save_tokens"], r["W"], cut) == r["saved"]
+
+
+def test_block_counts_equal_reference_charge():
+    """charge(tokens * kvb) / block_bytes == ceil(tokens / T_b) for the LLaMA shapes."""
+    for name, tb in (("llama2-13b", 128), ("llama2-7b", 256), ("llama2-70b", 128)):
+        s = model.shape(name)
+        bb = tb * s.kv_bytes_per_token
+        for tok in (1, tb - 1, tb, tb + 1, 2142, 4096):
+            ch = layout_ref.charge(layout_ref.kv_size(tok, s.kv_bytes_per_token), bb)
+            assert ch // bb == -(-tok // tb)
+
+
+def test_shapes_kv_bytes():
+    assert model.shape("13b").kv_bytes_per_token == 819200
+    assert model.shape("7b").kv_bytes_per_token == 524288
+    assert model.shape("70b").kv_bytes_per_token == 327680
+    assert model.shape("70b").tp_shard(8).kv_bytes_per_token == 40960
