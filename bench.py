@@ -1,0 +1,464 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 AttentionStore KV-reuse prefill path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c3] [--turns B]
+
+Workload (BASELINE.json configs[2], the north-star target "LLaMA-2-13B-shaped
+multi-turn synthetic sessions"): the reference generator's 512 ShareGPT-shaped
+sessions (trace.generate_poisson(512, 1.0, seed=7), committed as
+tests/golden/workload_c3.json) replayed through the reference truncation rules
+(W = 4096, ratio 0.5).  Sessions are sharded across ranks by a stable hash of
+the session id (no collective on the path); each rank takes B hit turns of its
+shard (seeded sample), random-init LLaMA-2-13B weights and random bf16
+pre-RoPE KV history of the right size per turn.  One step = prefill of those B
+turns back to back.
+
+Modes (same turns, same kernels):
+  e2e   "host": each turn's kept KV streamed from the pinned host arena by the
+        layer-wise pre-loader (K1), re-embedded (K2), attended (K3, tcgen05),
+        new-token KV saved back to host (K4); token ids H2D and the first token
+        D2H every step.                       -> the JSON "e2e" (headline)
+  value "hbm": the same with the session KV resident in an HBM arena (inputs
+        already in HBM: SURVEY.md §8f item 1).  -> the JSON "value"
+  recompute: full prompt prefill, no reuse, no save (sim.py:432-435 baseline).
+Metric = prefill tokens/s = sum(kept + new) / seconds (metrics.py:118-119, 142).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+import zlib
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+METRIC = "multi-turn prefill tokens/s and p50 TTFT vs recompute; H2D GB/s per GPU"
+CONFIGS = {
+    "c2": ("llama2-7b", "workload_c2.json"),
+    "c3": ("llama2-13b", "workload_c3.json"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--turns", type=int, default=16, help="hit turns per GPU per step")
+    ap.add_argument("--block-tokens", type=int, default=128)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-attn", action="store_true",
+                    help="run only a few hbm steps (for ncu captures)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+
+def select_turns(cfg: str, rank: int, world: int, n: int):
+    """Hit turns of this rank's session shard (stable crc32 hash), seeded sample."""
+    from paper_2403_19708_b200.engine import overflow_kept, save_truncate
+
+    wl = json.loads((ROOT / "tests" / "golden" / CONFIGS[cfg][1]).read_text())
+    w, ratio = wl["window"], wl["truncation_ratio"]
+    cut = max(1, int(ratio * w))
+    hits = []
+    for s in wl["sessions"]:
+        if zlib.crc32(s["id"].encode()) % world != rank:
+            continue
+        ctx = 0
+        for k, (new, out) in enumerate(s["turns"]):
+            kept = overflow_kept(ctx, new, w, cut)
+            if k > 0 and kept > 0:
+                hits.append((s["id"], k, kept, new))
+            ctx = save_truncate(kept + new + out, w, cut)
+    rng = np.random.default_rng(1234 + rank)
+    pick = sorted(rng.choice(len(hits), size=min(n, len(hits)), replace=False))
+    return [hits[i] for i in pick], len(hits)
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                    rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows]
+        mx = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4)
+                          if r[5 + i].lower().startswith("active")})
+        loaded = [x for x in sm if x > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference numeric path (oracle port of rope.py:118-144)
+# ---------------------------------------------------------------------------
+
+def _cpu_task(args):
+    kept, new, hd, seed = args
+    from oracle import rope_ref
+    rng = np.random.default_rng(seed)
+    keys, values = rng.standard_normal((kept, hd)), rng.standard_normal((kept, hd))
+    q, k, v = (rng.standard_normal((new, hd)) for _ in range(3))
+    t = time.perf_counter()
+    rope_ref.decoupled_attention(keys, values, q, k, v, np.arange(kept))
+    return time.perf_counter() - t
+
+
+def cpu_reference(turns, shape, pairs_per_turn: int, seed: int = 0):
+    """Time attention_with_decoupled_cache (float64 numpy, one (layer, head) per
+    task) on all host cores; extrapolate to whole turns (L x Hq pairs each)."""
+    import multiprocessing as mp
+
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["OMP_NUM_THREADS"] = "1"
+    cores = len(os.sched_getaffinity(0))
+    tasks = [(kept, new, shape.head_dim, seed + 97 * i + j)
+             for i, (_, _, kept, new) in enumerate(turns) for j in range(pairs_per_turn)]
+    ctx = mp.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        times = pool.map(_cpu_task, tasks, chunksize=1)
+    wall = time.perf_counter() - t0
+    per_turn = []
+    for i in range(len(turns)):
+        mean_pair = statistics.fmean(times[i * pairs_per_turn:(i + 1) * pairs_per_turn])
+        per_turn.append(mean_pair * shape.layers * shape.n_heads / cores)
+    tokens = sum(kept + new for _, _, kept, new in turns)
+    return {"value": tokens / sum(per_turn), "cores": cores, "cpu_seconds": sum(times),
+            "wall_seconds": wall, "tasks": len(tasks)}
+
+
+def run_reference(args, shape, turns):
+    """--impl reference: the reference's CPU implementation of the path (oracle
+    port of kvsim.rope.attention_with_decoupled_cache), all host cores."""
+    pairs = 4
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference(turns, shape, pairs, seed=i)
+        if i >= args.warmup:
+            vals.append(r)
+    value = statistics.median(v["value"] for v in vals)
+    ms = statistics.fmean(v["wall_seconds"] for v in vals) * 1e3
+    sample = (f"attention_with_decoupled_cache (float64 numpy, rope.py:118-144) on {pairs} "
+              f"(layer, head) pairs of each of {len(turns)} hit turns per step, extrapolated "
+              f"to {shape.layers}x{shape.n_heads} pairs per turn; projections excluded "
+              f"(the reference has none)")
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {shape.name}-shaped hit turns "
+                                   f"(reference CPU path)", "turns_per_gpu": len(turns)},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": vals[0]["cores"],
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    sys.path.insert(0, str(ROOT))
+    from paper_2403_19708_b200 import model
+
+    shape = model.shape(CONFIGS[args.config][0])
+    turns, n_hits = select_turns(args.config, rank, world, args.turns)
+
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args, shape, turns)), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2403_19708_b200 import build as _build
+    from paper_2403_19708_b200.metrics import percentile
+    from paper_2403_19708_b200.runner import Job, Runner, attention_flops
+    from paper_2403_19708_b200.store import HostArena
+
+    _build.build()
+    tb = args.block_tokens
+    block_bytes = tb * shape.kv_bytes_per_token
+    nbs = [-(-(kept + new) // tb) for _, _, kept, new in turns]
+    n_blocks = sum(nbs)
+    max_new = max(new for *_, new in turns)
+    max_kept = max(kept for *_, kept, _ in turns)
+    # arenas: the same block ids in the pinned host arena and the HBM arena
+    arena = HostArena(n_blocks, block_bytes, pin=True)
+    hbm = torch.empty(n_blocks * block_bytes // 2, dtype=torch.bfloat16, device=dev)
+    g = torch.Generator(device=dev).manual_seed(7 + rank)
+    chunk = 1 << 28
+    host_bf = arena.buffer.view(torch.bfloat16)
+    for off in range(0, hbm.numel(), chunk):
+        m = min(chunk, hbm.numel() - off)
+        hbm[off:off + m].normal_(generator=g)
+        host_bf[off:off + m].copy_(hbm[off:off + m])
+    torch.cuda.synchronize()
+    runner = Runner(shape, device=dev, seed=0, block_tokens=tb, host_arena=arena,
+                    hbm_arena=hbm, read_buffer_bytes=4 << 30, write_buffer_bytes=1 << 30,
+                    max_new=max(max_new, 1), max_ctx=max(shape.context_window, max_kept + 1))
+    ids_perm = np.random.default_rng(99 + rank).permutation(n_blocks)
+    jobs = {"host": [], "hbm": [], "recompute": []}
+    pos = 0
+    trng = np.random.default_rng(5 + rank)
+    elems_per_block = block_bytes // 2
+    for (sid0, k, kept, new), nb in zip(turns, nbs):
+        sid = f"{sid0}#{k}"  # each sampled turn owns its own synthetic blocks
+        bids = [int(b) for b in ids_perm[pos:pos + nb]]
+        pos += nb
+        new_ids = torch.as_tensor(trng.integers(0, shape.vocab, new)).pin_memory()
+        prompt_ids = torch.as_tensor(trng.integers(0, shape.vocab, kept + new)).pin_memory()
+        off = torch.as_tensor([b * elems_per_block for b in bids], dtype=torch.int64,
+                              device=dev)
+        jobs["host"].append(Job(sid, new_ids, kept=kept, source="host", block_ids=bids,
+                                save=True))
+        jobs["hbm"].append(Job(sid, new_ids.to(dev), kept=kept, source="hbm", block_ids=bids,
+                               save=True, dev_block_off=off))
+        jobs["recompute"].append(Job(sid, prompt_ids.to(dev)))
+    prompt_tokens = sum(kept + new for *_, kept, new in turns)
+    new_tokens = sum(new for *_, new in turns)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def timed(mode: str, steps: int, warmup: int, probe: bool = False, clocks=None):
+        js = jobs[mode]
+        for _ in range(warmup):
+            runner.run(js)
+            runner.join()
+        torch.cuda.synchronize()
+        barrier()
+        runner.probe = [] if probe else None
+        launches0 = runner.launches
+        cs = runner.s_compute
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        sampler = ClockSampler(local) if clocks is not None else None
+        if sampler:
+            sampler.__enter__()
+        e0.record(cs)
+        res = None
+        for _ in range(steps):
+            res = runner.run(js)
+            runner.join()
+        e1.record(cs)
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.__exit__(None, None, None)
+            clocks.update(sampler.summary())
+        barrier()
+        ms = e0.elapsed_time(e1)
+        launches = runner.launches - launches0
+        Runner.finalize(res)
+        probe_rec = runner.probe
+        runner.probe = None
+        return ms, res, launches, probe_rec
+
+    clocks: dict = {}
+    if args.profile_attn:
+        timed("hbm", 2, 1)
+        return
+
+    # e2e (headline) — KV from the pinned host arena, clocks sampled here
+    ms_host, res_host, launches, _ = timed("host", args.steps, args.warmup, clocks=clocks)
+    # value — KV resident in HBM; probe the attention / re-embed launches
+    ms_hbm, res_hbm, _, probe = timed("hbm", args.steps, args.warmup, probe=True)
+    # recompute baseline
+    ms_re, res_re, _, _ = timed("recompute", max(2, args.steps // 2), 1)
+    # prestaged TTFT: each turn starts once its whole KV sits in the read buffer
+    for j in jobs["host"]:
+        j.prestage = True
+    _, res_pre, _, _ = timed("host", 1, 1)
+    for j in jobs["host"]:
+        j.prestage = False
+
+    steps_re = max(2, args.steps // 2)
+    t_host = max_over_ranks(ms_host) * 1e-3
+    t_hbm = max_over_ranks(ms_hbm) * 1e-3
+    t_re = max_over_ranks(ms_re) * 1e-3
+    tok_all = sum_over_ranks(prompt_tokens)
+    value = tok_all * args.steps / t_hbm
+    e2e = tok_all * args.steps / t_host
+    recompute = tok_all * steps_re / t_re
+
+    # roofline of the dominant kernel (K3 attention), live CUDA-event durations
+    att = [(e0.elapsed_time(e1) * 1e-3, w) for kind, e0, e1, w in probe if kind == "attention"]
+    emb = [(e0.elapsed_time(e1) * 1e-3, w) for kind, e0, e1, w in probe if kind == "reembed"]
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    tflops_peak = peaks.get("bf16_tflops_sustained", 1400.0)
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    att_tflops = sum(w for _, w in att) / sum(t for t, _ in att) / 1e12
+    emb_gbs = sum(w for _, w in emb) / sum(t for t, _ in emb) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_attn_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+
+    # TTFT / exposed transfer / link GB/s from the measured timelines
+    def ttfts(res):
+        return [r.timeline.makespan for r in res]
+
+    ttft_host = percentile(ttfts(res_host), 0.5)
+    ttft_hbm = percentile(ttfts(res_hbm), 0.5)
+    ttft_re = percentile(ttfts(res_re), 0.5)
+    ttft_pre = percentile(ttfts(res_pre), 0.5)
+    stall_host = sum(r.timeline.stall_total for r in res_host)
+    span_host = sum(r.timeline.makespan for r in res_host)
+    stall_pre = sum(r.timeline.stall_total for r in res_pre)
+    span_pre = sum(r.timeline.makespan for r in res_pre)
+    load_busy = sum(r.timeline.load_total for r in res_host)
+    save_busy = sum(r.timeline.save_total for r in res_host)
+    h2d_bytes = sum(r.bytes_loaded for r in res_host)
+    d2h_bytes = sum(r.bytes_saved for r in res_host)
+    h2d_step = h2d_bytes + sum(j.n_new * 8 for j in jobs["host"])
+    d2h_step = d2h_bytes + 8 * len(jobs["host"])
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cb = cpu_reference(turns, shape, pairs_per_turn=24)
+        cpu = {"value": cb["value"], "unit": "tokens/s", "cores": cb["cores"], "kind": "port",
+               "sample": (f"oracle port of attention_with_decoupled_cache (rope.py:118-144, "
+                          f"float64 numpy, 1 thread/process) on 24 (layer, head) pairs of each "
+                          f"of the {len(turns)} rank-0 turns ({cb['cpu_seconds']:.1f} CPU-s), "
+                          f"extrapolated to {shape.layers}x{shape.n_heads} pairs per turn; "
+                          f"projections excluded")}
+
+    kept_l = [kept for *_, kept, _ in turns]
+    new_l = [new for *_, new in turns]
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_hbm / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (reference ShareGPT-shaped session generator; random-init weights "
+                "and KV)",
+        "config": {
+            "workload": f"{args.config}: {shape.name}-shaped, generate_poisson(512, seed=7) "
+                        f"sessions sharded by crc32(session) over {world} GPU(s); "
+                        f"{len(turns)} hit turns/GPU/step (of {n_hits} in shard)",
+            "turns_per_gpu": len(turns), "kept_p50": percentile(kept_l, 0.5),
+            "new_p50": percentile(new_l, 0.5), "block_tokens": tb,
+            "value_mode": "KV resident in an HBM arena (no host link)",
+            "e2e_mode": "KV streamed from pinned host DRAM by the layer-wise pre-loader; "
+                        "new-token KV saved back asynchronously",
+            "l2": "inputs larger than L2 (per-step KV " f"{h2d_bytes / 1e9:.1f} GB)",
+            "parallelism": f"sessions sharded, no collective ({world} independent ranks)"},
+        "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d_step,
+                "d2h_bytes_per_step": d2h_step, "ms_per_step": ms_host / args.steps},
+        "recompute": {"value": recompute, "unit": "tokens/s",
+                      "ms_per_step": ms_re / steps_re},
+        "speedup_vs_recompute": {"value_mode": value / recompute, "e2e_mode": e2e / recompute},
+        "ttft_p50_s": {"reuse_host_saturated": ttft_host, "reuse_host_prestaged": ttft_pre,
+                       "reuse_hbm": ttft_hbm, "recompute": ttft_re,
+                       "speedup_prestaged": ttft_re / ttft_pre if ttft_pre else None,
+                       "speedup_saturated": ttft_re / ttft_host if ttft_host else None},
+        "exposed_transfer_frac": {"host_saturated": stall_host / span_host,
+                                  "host_prestaged": stall_pre / span_pre},
+        "link_gbs_per_gpu": {"h2d": h2d_bytes / load_busy / 1e9 if load_busy else None,
+                             "d2h": d2h_bytes / save_busy / 1e9 if save_busy else None,
+                             "h2d_bytes_per_step": h2d_bytes},
+        "roofline": {"kernel": "askv_prefill_attn (K3, tcgen05)", "bound": "tensor",
+                     "achieved": att_tflops, "peak": tflops_peak, "unit": "TFLOP/s",
+                     "frac": att_tflops / tflops_peak, "traffic": traffic,
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
+                     "flops_per_launch": statistics.fmean(w for _, w in att),
+                     "launches": len(att)},
+        "roofline_reembed": {"kernel": "askv_reembed (K2)", "bound": "hbm",
+                             "achieved": emb_gbs, "peak": hbm_peak, "unit": "GB/s",
+                             "frac": emb_gbs / hbm_peak},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -275,10 +275,10 @@ class Runner:
         n, kept = job.n_new, job.kept
         if n < 1:
             raise ValueError("a job needs at least one new token")
-        if n > self.max_new:
-            raise ValueError(f"{n} new tokens exceed max_new={self.max_new}")
-        if kept + n > self.max_ctx + self.max_new:
-            raise ValueError("context exceeds the runner's buffers")
+        if job.save and n > self.max_new:
+            raise ValueError(f"{n} saved rows exceed the write-buffer slot ({self.max_new})")
+        if kept + n > self.table.max_pos:
+            raise ValueError("context exceeds the runner's RoPE table")
         if job.save and len(job.block_ids) * self.block_tokens < job.head + kept + n:
             raise ValueError("save needs block_ids covering kept + new rows")
         arena = None

@@ -6,7 +6,8 @@ Tolerances (stated here and in DESIGN.md §Parity):
   the same bf16 inputs)): every element within 1 bf16 ulp, >= 99.9 % identical.
 * V rows, pre-RoPE save copies, preload/save DMA: bit-exact.
 * Attention output vs f64 oracle on the same bf16 q/k/v:
-  relative Frobenius error <= 1e-2 and max-abs error <= 2e-2.
+  relative Frobenius error <= 5e-3 and max-abs error <= 1.5e-2 (measured on
+  B200: rel 1.8e-3 .. 2.3e-3, i.e. the bf16 rounding of the output itself).
 """
 
 import math
@@ -177,7 +178,7 @@ def test_prefill_attention_vs_oracle(n_cached, n_new, hq, hkv, d, splits):
     mx = np.abs(got - want).max()
     _log_err("attn", dict(n_cached=n_cached, n_new=n_new, hq=hq, hkv=hkv, d=d, splits=s,
                           rel=rel, max_abs=float(mx)))
-    assert rel <= 1e-2 and mx <= 2e-2, (rel, mx)
+    assert rel <= 5e-3 and mx <= 1.5e-2, (rel, mx)
 
 
 def test_attention_splits_agree():
