@@ -35,7 +35,6 @@ import subprocess
 import sys
 import tempfile
 import time
-import zlib
 from pathlib import Path
 
 import numpy as np
@@ -74,9 +73,11 @@ def select_turns(cfg: str, rank: int, world: int, n: int):
     wl = json.loads((ROOT / "tests" / "golden" / CONFIGS[cfg][1]).read_text())
     w, ratio = wl["window"], wl["truncation_ratio"]
     cut = max(1, int(ratio * w))
+    from paper_2403_19708_b200.dist import shard_of
+
     hits = []
     for s in wl["sessions"]:
-        if zlib.crc32(s["id"].encode()) % world != rank:
+        if shard_of(s["id"], world) != rank:
             continue
         ctx = 0
         for k, (new, out) in enumerate(s["turns"]):
@@ -237,8 +238,9 @@ def main():
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    from paper_2403_19708_b200 import dist as pdist
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        pdist.init("nccl", dev)
 
     from paper_2403_19708_b200 import build as _build
     from paper_2403_19708_b200.metrics import percentile
@@ -292,18 +294,10 @@ def main():
             dist.barrier()
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return pdist.max_over_ranks(x, dev)
 
     def sum_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+        return pdist.sum_over_ranks(x, dev)
 
     def timed(mode: str, steps: int, warmup: int, probe: bool = False, clocks=None):
         js = jobs[mode]
