@@ -144,6 +144,16 @@ int askv_save_layer(void* host_base, const int64_t* block_ids, int nblocks,
                     int64_t row_bytes, int64_t first_token, int n_tokens, const void* src,
                     void* stream, void* done_event);
 
+/*
+ * Fused elementwise ops of the LLaMA block the runner executes around the path
+ * (no reference counterpart; the reference has no model):
+ *   askv_rmsnorm : y[r] = x[r] * rsqrt(mean(x[r]^2) + eps) * w   (bf16 io, fp32 math)
+ *   askv_silu_mul: out[r] = silu(gu[r][0:ffn]) * gu[r][ffn:2ffn]
+ */
+int askv_rmsnorm(const void* x, const void* w, void* y, int rows, int cols, float eps,
+                 void* stream);
+int askv_silu_mul(const void* gu, void* out, int rows, int ffn, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

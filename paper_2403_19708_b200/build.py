@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libaskv.so"
-SOURCES = ["rope.cu", "attention.cu", "copy_engine.cu"]
+SOURCES = ["rope.cu", "attention.cu", "copy_engine.cu", "elementwise.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

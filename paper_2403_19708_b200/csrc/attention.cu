@@ -4,18 +4,10 @@
 // where query i (0-based among the n_new new tokens) sees key rows
 // j <= n_cached + i.  q and k arrive already rotated (K2 / rope_new).
 //
-// One CTA = one 128-row query tile x one q-head x one KV split.  Warp roles:
-//   warp 0      TMA producer: Q once, then K/V 128-row tiles into a STAGES ring
-//   warp 1      MMA issuer (one thread): S = Q K^T into a double-buffered TMEM
-//               tile, then O_j = P_j V_j into a TMEM tile (tcgen05.mma kind::f16)
-//   warp 2      TMEM allocator (512 columns: S0 | S1 | O)
-//   warps 4-7   softmax: thread r owns query row r (= TMEM lane r); reads S with
-//               tcgen05.ld, online softmax in fp32 (exp2), writes P (bf16) into a
-//               SWIZZLE_128B K-major smem tile for the PV MMA, folds each
-//               finished O_j into a register accumulator with the running-max
-//               correction, and writes the normalised row (or a split partial).
-// The MMA warp issues S_{j+1} before PV_j, so QK^T of the next tile runs on the
-// tensor core while the softmax warps work on the current one.
+// Design (kernel comment below): per CTA one 128-row query tile x one q-head x
+// one KV split; two softmax warpgroups take alternate KV tiles and ping-pong
+// on the tensor core; S, P and O live in TMEM; K/V stream through 3-deep TMA
+// rings; split-KV partials merge in a deterministic combine kernel.
 //
 // Layouts: Q [n_new][Hq][d]; K/V rows [T][2][Hkv][d] (token-major, K then V,
 // exactly the host-block row layout so preloaded blocks are used in place);
@@ -28,6 +20,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "askv_internal.h"
@@ -38,28 +31,7 @@ namespace {
 
 constexpr int kBM = 128;  // query rows per tile (UMMA M)
 constexpr int kBN = 128;  // key rows per tile (UMMA N of S, K of PV)
-constexpr int kThreads = 256;
 constexpr int kMaxSplits = 32;
-
-template <int HD>
-struct Cfg {
-  static constexpr int kStages = HD == 128 ? 2 : 4;
-  static constexpr int kChunks = HD / 64;                  // 64-col swizzle chunks
-  static constexpr int kTileBytes = kBM * HD * 2;          // Q / K / V tile
-  static constexpr int kPBytes = kBM * kBN * 2;            // P tile
-  static constexpr int kQOff = 0;
-  static constexpr int kKOff = kQOff + kTileBytes;
-  static constexpr int kVOff = kKOff + kStages * kTileBytes;
-  static constexpr int kPOff = kVOff + kStages * kTileBytes;
-  static constexpr int kBarOff = kPOff + kPBytes;
-  // barriers: q_full, k_full[S], v_full[S], kv_empty[S], s_full[2], s_empty[2],
-  //           p_full, o_full, o_empty
-  static constexpr int kNumBars = 1 + 3 * kStages + 4 + 3;
-  static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
-  static constexpr int kSmemBytes = kTmemSlotOff + 16 + 1024;  // +1024 manual alignment
-  static constexpr uint32_t kTmemCols = 512;
-  static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO = 256;
-};
 
 struct AttnParams {
   int n_new;
@@ -74,52 +46,90 @@ struct AttnParams {
   float* part_lse;     // [splits][n_new][hq]   (log2 units)
 };
 
+// ============================================================================
+// Kernel: two softmax warpgroups ping-pong on the tensor core (FA4-style).
+//
+// One CTA = one 128-row query tile x one q-head x one KV split, as in v1, but
+// the KV tiles of the split alternate between two softmax warpgroups (WG0:
+// even tiles, WG1: odd tiles), each with its own S and O in TMEM
+// (S0 | S1 | O0 | O1 = 512 columns).  The MMA thread issues
+//   S_0, S_1, PV_0, S_2, PV_1, S_3, ...
+// so QK^T / PV of one group run while the other group does its softmax.
+// O accumulates in TMEM across tiles (no per-tile register fold); it is
+// rescaled in place only when a row max grows by more than 2^8 (lazy
+// rescaling: P <= 2^8 is exact in fp32 accumulation and harmless in bf16).
+// P is written back into the S columns as packed bf16 (tcgen05.st) and read by
+// the PV MMA straight from TMEM (A operand in tensor memory), so neither P nor
+// O touches shared memory.  K and V have separate 3-deep TMA rings so K of
+// tile j+2 can land while V of tile j is still in use.  At the end the two
+// groups merge their (m, l, O) through TMEM and each writes half the columns.
+// Warps: 0-3 WG0, 4-7 WG1, 8 TMA (+TMEM alloc), 9 MMA.
+// ============================================================================
+
 template <int HD>
-__global__ void __launch_bounds__(kThreads, 1)
-    attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
-                    const __grid_constant__ CUtensorMap tm_k,
-                    const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
-  using C = Cfg<HD>;
+struct Cfg2 {
+  static constexpr int kStages = 3;
+  static constexpr int kChunks = HD / 64;
+  static constexpr int kTileBytes = kBM * HD * 2;
+  static constexpr int kQOff = 0;
+  static constexpr int kKOff = kQOff + kTileBytes;
+  static constexpr int kVOff = kKOff + kStages * kTileBytes;
+  static constexpr int kBarOff = kVOff + kStages * kTileBytes;
+  // q_full, k_full[S], k_empty[S], v_full[S], v_empty[S], s_full[2], p_full[2], o_full[2]
+  static constexpr int kNumBars = 1 + 4 * kStages + 6;
+  static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
+  static constexpr int kSmemBytes = kTmemSlotOff + 16 + 1024;
+  static constexpr uint32_t kTmemCols = 512;
+  // TMEM columns: S of group w at 128*w, O of group w at 256 + 128*w
+  __host__ __device__ static constexpr uint32_t col_s(int w) { return 128u * (uint32_t)w; }
+  __host__ __device__ static constexpr uint32_t col_o(int w) { return 256u + 128u * (uint32_t)w; }
+  static constexpr int kThreads = 320;
+  static constexpr float kRescaleLog2 = 8.0f;
+  static_assert(kSmemBytes <= 232448, "smem budget");
+};
+
+template <int HD, int kEmu>
+__global__ void __launch_bounds__(320, 1)
+    attn_fwd_v2_kernel(const __grid_constant__ CUtensorMap tm_q,
+                       const __grid_constant__ CUtensorMap tm_k,
+                       const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
+  using C = Cfg2<HD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem + C::kQOff;
   uint8_t* sK = smem + C::kKOff;
   uint8_t* sV = smem + C::kVOff;
-  uint8_t* sP = smem + C::kPOff;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
   uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;
-  uint64_t* v_full = k_full + C::kStages;
-  uint64_t* kv_empty = v_full + C::kStages;
-  uint64_t* s_full = kv_empty + C::kStages;
-  uint64_t* s_empty = s_full + 2;
-  uint64_t* p_full = s_empty + 2;
-  uint64_t* o_full = p_full + 1;
-  uint64_t* o_empty = o_full + 1;
+  uint64_t* k_full = q_full + 1;
+  uint64_t* k_empty = k_full + C::kStages;
+  uint64_t* v_full = k_empty + C::kStages;
+  uint64_t* v_empty = v_full + C::kStages;
+  uint64_t* s_full = v_empty + C::kStages;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_full = p_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kTmemSlotOff);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m_tile = blockIdx.x;
   const int h = blockIdx.y;
   const int split = blockIdx.z;
   const int kh = h / p.group;
-  const int q0 = m_tile * kBM;
+  const int q0 = blockIdx.x * kBM;
   const int q_rows = min(kBM, p.n_new - q0);
-  const int kv_end = p.n_cached + q0 + q_rows;  // exclusive
+  const int kv_end = p.n_cached + q0 + q_rows;
   const int tiles_total = (kv_end + kBN - 1) / kBN;
   const int t_begin = split * p.tiles_per_split;
   const int t_end = min(tiles_total, t_begin + p.tiles_per_split);
   const int n_tiles = t_end > t_begin ? t_end - t_begin : 0;
   const bool partial = p.num_splits > 1;
 
-  if (n_tiles == 0) {  // empty split: neutral partial (CTA-uniform branch)
-    if (warp >= 4) {
-      const int r = threadIdx.x - 128;
-      const int qi = q0 + r;
+  if (n_tiles == 0) {
+    if (warp < 4) {
+      const int r = threadIdx.x;
       if (r < q_rows) {
-        const int64_t row = ((int64_t)split * p.n_new + qi) * p.hq + h;
+        const int64_t row = ((int64_t)split * p.n_new + q0 + r) * p.hq + h;
         p.part_lse[row] = -INFINITY;
         float4* po = reinterpret_cast<float4*>(p.part_o + row * HD);
 #pragma unroll
@@ -133,25 +143,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(q_full, 1);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
       mbar_init(&v_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+      mbar_init(&v_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&s_full[b], 1);
-      mbar_init(&s_empty[b], 128);
+    for (int w = 0; w < 2; ++w) {
+      mbar_init(&s_full[w], 1);
+      mbar_init(&p_full[w], 128);
+      mbar_init(&o_full[w], 1);
     }
-    mbar_init(p_full, 128);
-    mbar_init(o_full, 1);
-    mbar_init(o_empty, 128);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
+  if (warp == 8) tmem_alloc(tmem_slot, C::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       tma_prefetch_desc(&tm_q);
@@ -163,184 +172,205 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_3d(sQ + c * (kBM * 128), &tm_q, q_full, c * 64, h, q0);
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j % C::kStages;
-        if (j >= C::kStages) mbar_wait(&kv_empty[st], ((j / C::kStages) - 1) & 1);
+        const uint32_t ph = ((j / C::kStages) - 1) & 1;
         const int row0 = (t_begin + j) * kBN;
-        uint8_t* dk = sK + st * C::kTileBytes;
-        uint8_t* dv = sV + st * C::kTileBytes;
+        if (j >= C::kStages) mbar_wait(&k_empty[st], ph);
         mbar_expect_tx(&k_full[st], C::kTileBytes);
 #pragma unroll
         for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d(dk + c * (kBN * 128), &tm_k, &k_full[st], c * 64, kh, row0);
+          tma_load_3d(sK + st * C::kTileBytes + c * (kBN * 128), &tm_k, &k_full[st], c * 64, kh,
+                      row0);
+        if (j >= C::kStages) mbar_wait(&v_empty[st], ph);
         mbar_expect_tx(&v_full[st], C::kTileBytes);
 #pragma unroll
         for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d(dv + c * (kBN * 128), &tm_v, &v_full[st], c * 64, kh, row0);
+          tma_load_3d(sV + st * C::kTileBytes + c * (kBN * 128), &tm_v, &v_full[st], c * 64, kh,
+                      row0);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(kBM, kBN, 0, 0);
       constexpr uint32_t idesc_o = idesc_bf16_f32(kBM, HD, 0, 1);
-      const uint32_t sq = smem_u32(sQ), sk = smem_u32(sK), sv = smem_u32(sV),
-                     sp = smem_u32(sP);
+      const uint32_t sq = smem_u32(sQ), sk = smem_u32(sK), sv = smem_u32(sV);
       mbar_wait(q_full, 0);
       auto issue_s = [&](int j) {
         const int st = j % C::kStages;
-        const int b = j & 1;
+        const int w = j & 1;
         mbar_wait(&k_full[st], (j / C::kStages) & 1);
-        if (j >= 2) mbar_wait(&s_empty[b], ((j >> 1) - 1) & 1);
         tc_fence_after();
-        const uint32_t d = tmem + (b ? C::kColS1 : C::kColS0);
         const uint32_t kb = sk + st * C::kTileBytes;
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
           const uint32_t off = (k >> 2) * (kBM * 128) + (k & 3) * 32;
-          umma_bf16(d, sdesc_sw128(sq + off, 16, 1024), sdesc_sw128(kb + off, 16, 1024),
-                    idesc_s, k > 0);
+          umma_bf16(tmem + C::col_s(w), sdesc_sw128(sq + off, 16, 1024),
+                    sdesc_sw128(kb + off, 16, 1024), idesc_s, k > 0);
         }
-        umma_commit(&s_full[b]);
+        umma_commit(&k_empty[st]);
+        umma_commit(&s_full[w]);
       };
       issue_s(0);
+      if (n_tiles > 1) issue_s(1);
       for (int j = 0; j < n_tiles; ++j) {
-        if (j + 1 < n_tiles) issue_s(j + 1);
+        const int w = j & 1;
         const int st = j % C::kStages;
-        mbar_wait(p_full, j & 1);
+        mbar_wait(&p_full[w], (j >> 1) & 1);
         mbar_wait(&v_full[st], (j / C::kStages) & 1);
-        if (j >= 1) mbar_wait(o_empty, (j - 1) & 1);
         tc_fence_after();
         const uint32_t vb = sv + st * C::kTileBytes;
 #pragma unroll
-        for (int k = 0; k < kBN / 16; ++k) {
-          const uint32_t aoff = (k >> 2) * (kBM * 128) + (k & 3) * 32;
-          umma_bf16(tmem + C::kColO, sdesc_sw128(sp + aoff, 16, 1024),
-                    sdesc_sw128(vb + k * (16 * 128), kBN * 128, 1024), idesc_o, k > 0);
-        }
-        umma_commit(o_full);
-        umma_commit(&kv_empty[st]);
+        for (int k = 0; k < kBN / 16; ++k)
+          umma_bf16_tmem_a(tmem + C::col_o(w), tmem + C::col_s(w) + k * 8,
+                           sdesc_sw128(vb + k * (16 * 128), kBN * 128, 1024), idesc_o,
+                           (j >= 2) || (k > 0));
+        umma_commit(&v_empty[st]);
+        umma_commit(&o_full[w]);
+        if (j + 2 < n_tiles) issue_s(j + 2);
       }
     }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ softmax
-    const int r = threadIdx.x - 128;  // row in tile == TMEM lane
-    const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-    const int qi = q0 + r;
-    const int row_limit = p.n_cached + qi;  // last visible key
+  } else {
+    // ------------------------------------------------------------ softmax WGs
+    const int w = warp >> 2;
+    const int r = (warp & 3) * 32 + lane;  // row in tile == TMEM lane
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t t_s = tmem + lane_off + C::col_s(w);
+    const uint32_t t_o = tmem + lane_off + C::col_o(w);
+    const int row_limit = p.n_cached + q0 + r;
     const float sl2 = p.scale_log2;
-    float o[HD];
-#pragma unroll
-    for (int c = 0; c < HD; ++c) o[c] = 0.f;
-    float m_acc = -INFINITY, l_acc = 0.f;  // accumulator state
-    float m_run = -INFINITY;               // running max (scaled, log2 units)
-    float m_prev = -INFINITY, l_prev = 0.f;  // stats of the in-flight PV tile
-    uint8_t* prow = sP + r * 128;
-    const int sw = r & 7;
-
-    // Fold PV_j (relative to m_prev) into the register accumulator.  The
-    // tcgen05.ld calls are warp-collective, so the per-row "tile fully masked"
-    // case is handled with coefficients, not a branch.
-    auto fold = [&](int j) {
-      mbar_wait(o_full, j & 1);
-      tc_fence_after();
-      float a_o = 1.f, b_pv = 0.f;
-      if (m_prev != -INFINITY) {
-        a_o = (m_acc == -INFINITY) ? 0.f : ex2(m_acc - m_prev);
-        b_pv = 1.f;
-        l_acc = l_acc * a_o + l_prev;
-        m_acc = m_prev;
-      }
-#pragma unroll
-      for (int c = 0; c < HD / 32; ++c) {
-        float pv[32];
-        tmem_ld32(trow + C::kColO + c * 32, pv);
-#pragma unroll
-        for (int e = 0; e < 32; ++e) o[c * 32 + e] = fmaf(pv[e], b_pv, o[c * 32 + e] * a_o);
-      }
-    };
-
-    for (int j = 0; j < n_tiles; ++j) {
-      const int b = j & 1;
-      const uint32_t scol = b ? C::kColS1 : C::kColS0;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
+    float m_acc = -INFINITY, l_acc = 0.f;
+    int t = 0;
+    for (int j = w; j < n_tiles; j += 2, ++t) {
+      mbar_wait(&s_full[w], t & 1);
       tc_fence_after();
       const int kbase = (t_begin + j) * kBN;
-      const int lim = row_limit - kbase;  // columns c <= lim are visible
+      const int lim = row_limit - kbase;
+      // CTA-uniform: does any row of this q-tile see a masked column here?
+      const bool diag = kbase + kBN - 1 > p.n_cached + q0;
       float mx = -INFINITY;
 #pragma unroll
       for (int c = 0; c < kBN / 32; ++c) {
-        float s[32];
-        tmem_ld32(trow + scol + c * 32, s);
+        float sv[32];
+        tmem_ld32(t_s + c * 32, sv);
+        if (diag) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) mx = fmaxf(mx, (c * 32 + e <= lim) ? s[e] : -INFINITY);
+          for (int e = 0; e < 32; ++e) mx = fmaxf(mx, (c * 32 + e <= lim) ? sv[e] : -INFINITY);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) mx = fmaxf(mx, sv[e]);
+        }
       }
-      const float m_new = fmaxf(m_run, mx * sl2);
-      if (j >= 1) {
-        fold(j - 1);
-        tc_fence_before();
-        mbar_arrive(o_empty);
+      const float m_tile = mx * sl2;
+      const bool need = m_tile > m_acc + C::kRescaleLog2;
+      if (t == 0) {
+        if (need) m_acc = m_tile;
+      } else if (__any_sync(0xffffffffu, need)) {
+        // O_w holds tiles < t of this group: wait for the last PV, rescale in place.
+        mbar_wait(&o_full[w], (t - 1) & 1);
+        tc_fence_after();
+        const float f = need ? ex2(m_acc - m_tile) : 1.f;
+#pragma unroll
+        for (int c = 0; c < HD / 32; ++c) {
+          float ov[32];
+          tmem_ld32(t_o + c * 32, ov);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) ov[e] *= f;
+          tmem_st32(t_o + c * 32, ov);
+        }
+        tmem_wait_st();
+        if (need) {
+          l_acc *= f;
+          m_acc = m_tile;
+        }
       }
-      // P_j = exp2(S * scale_log2 - m_new), bf16, into the swizzled K-major tile
+      const float neg_m = (m_acc == -INFINITY) ? 0.f : -m_acc;
       float lsum = 0.f;
-      const float neg_m = (m_new == -INFINITY) ? 0.f : -m_new;
 #pragma unroll
       for (int c = 0; c < kBN / 32; ++c) {
-        float s[32];
-        tmem_ld32(trow + scol + c * 32, s);
+        float sv[32];
+        tmem_ld32(t_s + c * 32, sv);
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          const float p0 = (c * 32 + e <= lim) ? ex2(fmaf(s[e], sl2, neg_m)) : 0.f;
-          const float p1 = (c * 32 + e + 1 <= lim) ? ex2(fmaf(s[e + 1], sl2, neg_m)) : 0.f;
+          const float x0 = fmaf(sv[e], sl2, neg_m);
+          const float x1 = fmaf(sv[e + 1], sl2, neg_m);
+          // kEmu of every 8 columns go to the FMA pipe, the rest to MUFU
+          float p0 = (e & 7) < kEmu ? ex2_poly(x0) : ex2(x0);
+          float p1 = ((e + 1) & 7) < kEmu ? ex2_poly(x1) : ex2(x1);
+          if (diag) {
+            p0 = (c * 32 + e <= lim) ? p0 : 0.f;
+            p1 = (c * 32 + e + 1 <= lim) ? p1 : 0.f;
+          }
           lsum += p0 + p1;
           pk[e >> 1] = pack_bf16x2(p0, p1);
         }
-        uint8_t* half = prow + (c >> 1) * (kBM * 128);
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const int u = (c & 1) * 4 + w;
-          *reinterpret_cast<uint4*>(half + ((u ^ sw) << 4)) =
-              make_uint4(pk[4 * w], pk[4 * w + 1], pk[4 * w + 2], pk[4 * w + 3]);
-        }
+        tmem_st16(t_s + c * 16, pk);  // P over the already-read S columns
       }
+      l_acc += lsum;
+      tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&s_empty[b]);
-      fence_proxy_async_smem();
-      mbar_arrive(p_full);
-      m_prev = m_new;
-      l_prev = lsum;
-      m_run = m_new;
+      mbar_arrive(&p_full[w]);
     }
-    fold(n_tiles - 1);
+    // ---- epilogue: wait for this group's last PV, merge the two groups
+    if (t > 0) {
+      mbar_wait(&o_full[w], (t - 1) & 1);
+      tc_fence_after();
+    }
+    tmem_st2(t_s + 64, m_acc, l_acc);  // S columns are free once the last PV is done
+    tmem_wait_st();
     tc_fence_before();
-
-    if (r < q_rows) {
-      const float inv_l = l_acc > 0.f ? 1.f / l_acc : 0.f;
-      if (!partial) {
-        __nv_bfloat16* dst = p.out + ((int64_t)qi * p.hq + h) * HD;
+    named_bar_sync(1, 256);
+    tc_fence_after();
+    float m0, l0, m1, l1;
+    tmem_ld2(tmem + lane_off + C::col_s(0) + 64, m0, l0);
+    tmem_ld2(tmem + lane_off + C::col_s(1) + 64, m1, l1);
+    const float m = fmaxf(m0, m1);
+    const float f0 = l0 > 0.f ? ex2(m0 - m) : 0.f;
+    const float f1 = l1 > 0.f ? ex2(m1 - m) : 0.f;
+    const float l = l0 * f0 + l1 * f1;
+    const float inv_l = l > 0.f ? 1.f / l : 0.f;
+    const int qi = q0 + r;
+    constexpr int kHalf = HD / 2;
 #pragma unroll
-        for (int c = 0; c < HD / 8; ++c) {
-          uint4 v;
-          v.x = pack_bf16x2(o[8 * c + 0] * inv_l, o[8 * c + 1] * inv_l);
-          v.y = pack_bf16x2(o[8 * c + 2] * inv_l, o[8 * c + 3] * inv_l);
-          v.z = pack_bf16x2(o[8 * c + 4] * inv_l, o[8 * c + 5] * inv_l);
-          v.w = pack_bf16x2(o[8 * c + 6] * inv_l, o[8 * c + 7] * inv_l);
-          reinterpret_cast<uint4*>(dst)[c] = v;
+    for (int c = 0; c < kHalf / 32; ++c) {
+      const int col = w * kHalf + c * 32;
+      float a[32], b[32];
+      tmem_ld32(tmem + lane_off + C::col_o(0) + col, a);
+      tmem_ld32(tmem + lane_off + C::col_o(1) + col, b);
+      float o[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const float x = f0 > 0.f ? a[e] * f0 : 0.f;
+        const float y = f1 > 0.f ? b[e] * f1 : 0.f;
+        o[e] = (x + y) * inv_l;
+      }
+      if (r < q_rows) {
+        if (!partial) {
+          __nv_bfloat16* dst = p.out + ((int64_t)qi * p.hq + h) * HD + col;
+#pragma unroll
+          for (int e = 0; e < 32; e += 8) {
+            uint4 v;
+            v.x = pack_bf16x2(o[e + 0], o[e + 1]);
+            v.y = pack_bf16x2(o[e + 2], o[e + 3]);
+            v.z = pack_bf16x2(o[e + 4], o[e + 5]);
+            v.w = pack_bf16x2(o[e + 6], o[e + 7]);
+            *reinterpret_cast<uint4*>(dst + e) = v;
+          }
+        } else {
+          const int64_t row = ((int64_t)split * p.n_new + qi) * p.hq + h;
+          float4* po = reinterpret_cast<float4*>(p.part_o + row * HD + col);
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            po[e / 4] = make_float4(o[e], o[e + 1], o[e + 2], o[e + 3]);
+          if (w == 0 && c == 0) p.part_lse[row] = l > 0.f ? m + __log2f(l) : -INFINITY;
         }
-      } else {
-        const int64_t row = ((int64_t)split * p.n_new + qi) * p.hq + h;
-        p.part_lse[row] = l_acc > 0.f ? m_acc + __log2f(l_acc) : -INFINITY;
-        float4* po = reinterpret_cast<float4*>(p.part_o + row * HD);
-#pragma unroll
-        for (int c = 0; c < HD / 4; ++c)
-          po[c] = make_float4(o[4 * c] * inv_l, o[4 * c + 1] * inv_l, o[4 * c + 2] * inv_l,
-                              o[4 * c + 3] * inv_l);
       }
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 8) {
     tc_fence_after();
     tmem_dealloc(tmem, C::kTmemCols);
   }
@@ -420,6 +450,11 @@ int make_map(CUtensorMap* m, const void* base, int head_dim, int heads, int64_t 
   return ASKV_OK;
 }
 
+// Columns of every 8 whose exp2 runs on the FMA pipe (ex2_poly) instead of
+// MUFU.  Measured on B200 at the path's shapes: 0 is fastest (the softmax is
+// not MUFU-bound; profiles/r01_attn_experiments.md).
+constexpr int kExp2OnFma = 0;
+
 int sm_count() {
   static int n = 0;
   if (n == 0) {
@@ -456,15 +491,6 @@ template <int HD>
 int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cached, int n_new,
                 int hq, int hkv, float scale, void* out, void* ws, size_t ws_bytes,
                 int splits, cudaStream_t stream) {
-  using C = Cfg<HD>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<HD>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::kSmemBytes);
-    if (e != cudaSuccess) return cuda_status(e, "attn smem attribute");
-    attr_set = true;
-  }
   const int rows = n_cached + n_new;
   CUtensorMap mq, mk, mv;
   int rc = make_map(&mq, q, HD, hq, HD, n_new, (int64_t)hq * HD);
@@ -499,7 +525,16 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
     prm.part_lse = prm.part_o + (size_t)splits * rows_qh * HD;
   }
   dim3 grid(q_tiles, hq, splits);
-  attn_fwd_kernel<HD><<<grid, kThreads, C::kSmemBytes, stream>>>(mq, mk, mv, prm);
+  using C2 = Cfg2<HD>;
+  auto kern = attn_fwd_v2_kernel<HD, kExp2OnFma>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C2::kSmemBytes);
+    if (e != cudaSuccess) return cuda_status(e, "attn smem attribute");
+    attr = true;
+  }
+  kern<<<grid, C2::kThreads, C2::kSmemBytes, stream>>>(mq, mk, mv, prm);
   rc = launch_status("attn_fwd launch");
   if (rc || splits == 1) return rc;
   const int rows_qh = n_new * hq;

@@ -91,6 +91,23 @@ class Engine:
             freed += self.store.charge(it.bytes)
             self.store.remove(it.session_id)
 
+    def install_history(self, sid: str, ids: torch.Tensor, now: float = 0.0) -> JobResult:
+        """Prefill and store a session history as-is (no save-time truncation):
+        a pre-stored long document / history larger than the window, the
+        starting point of config C4 (32K history served at W = 4096)."""
+        ids = ids.reshape(-1).to(torch.int64)
+        n = int(ids.numel())
+        if self.store.peek(sid) is not None:
+            self.store.remove(sid)
+        tab = self.store.reserve_rows(sid, n)
+        res = self.runner.run([Job(sid, ids, kept=0, source="none", block_ids=tab, save=True,
+                                   head=self.store.head_row(sid))])[0]
+        self.store.mark_written(sid, n)
+        self.store.save(sid, n, now)
+        self.context[sid] = n
+        self.tokens[sid] = ids
+        return res
+
     def turn(self, sid: str, turn_index: int, new_ids: torch.Tensor,
              out_ids: torch.Tensor | None = None, now: float = 0.0,
              want_logits: bool = False) -> TurnOutcome:

@@ -145,3 +145,25 @@ def save_layer(host_base: torch.Tensor, block_ids, block_bytes: int, layer_off: 
                                 int(layer_off), int(block_tokens), int(row_bytes),
                                 int(first_token), int(n_tokens), src.data_ptr(),
                                 _stream(stream), None), "save_layer")
+
+
+def rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float = 1e-5, out=None, *, stream=None):
+    """y = x * rsqrt(mean(x^2) + eps) * w over the last dim (bf16)."""
+    _require_cuda(x, w)
+    x = x.contiguous()
+    out = torch.empty_like(x) if out is None else out
+    rows = x.numel() // x.shape[-1]
+    check(lib().askv_rmsnorm(x.data_ptr(), w.data_ptr(), out.data_ptr(), int(rows),
+                             int(x.shape[-1]), float(eps), _stream(stream)), "rmsnorm")
+    return out
+
+
+def silu_mul(gu: torch.Tensor, out=None, *, stream=None):
+    """silu(gu[:, :F]) * gu[:, F:] for gu = [rows, 2F] (bf16)."""
+    _require_cuda(gu)
+    rows, two_f = gu.shape
+    ffn = two_f // 2
+    out = torch.empty((rows, ffn), dtype=gu.dtype, device=gu.device) if out is None else out
+    check(lib().askv_silu_mul(gu.data_ptr(), out.data_ptr(), int(rows), int(ffn),
+                              _stream(stream)), "silu_mul")
+    return out

@@ -317,7 +317,7 @@ class Runner:
                 l0 = ev() if ev else None
                 if l0:
                     l0.record(cs)
-                h = F.rms_norm(x, (s.d_model,), lw["w_in"], 1e-5)
+                h = ops.rmsnorm(x, lw["w_in"], 1e-5, stream=cs)
                 qkv = F.linear(h, lw["wqkv"])
                 wslot = None
                 if job.save:
@@ -380,15 +380,16 @@ class Runner:
                 self._probe_end(p0, "attention", attention_flops(kept, n, hq, hd))
                 self.launches += 2 if splits > 1 else 1
                 x = torch.addmm(x, ao, lw["wo"].t())
-                h = F.rms_norm(x, (s.d_model,), lw["w_post"], 1e-5)
+                h = ops.rmsnorm(x, lw["w_post"], 1e-5, stream=cs)
                 gu = F.linear(h, lw["wgu"])
-                a = F.silu(gu[:, : s.ffn]) * gu[:, s.ffn:]
+                a = ops.silu_mul(gu, stream=cs)
                 x = torch.addmm(x, a, lw["wd"].t())
+                self.launches += 3
                 l1 = ev() if ev else None
                 if l1:
                     l1.record(cs)
                 rec["layers"].append((l0, l1))
-            hl = F.rms_norm(x[-1:], (s.d_model,), self.w.w_final, 1e-5)
+            hl = ops.rmsnorm(x[-1:], self.w.w_final, 1e-5, stream=cs)
             logits = F.linear(hl, self.w.lm_head).float()
             first.copy_(logits.argmax(dim=-1), non_blocking=True)
             if want_logits:

@@ -165,3 +165,37 @@ def test_reuse_equals_gpu_recompute_13b_layer_shapes():
     tl = o.result.timeline
     assert tl is not None and len(tl.load_intervals) == shape.layers
     assert tl.makespan > 0 and tl.stall_total <= tl.makespan
+
+
+def test_c4_long_context_32k_history_truncated_reuse():
+    """Config C4: LLaMA-2-7B-shaped (2 layers here), W = 4096, a stored 32K-token
+    history.  The next turn (256 in) truncates the front 30720 tokens as a
+    block-table edit and reuses the last 2048 rows re-embedded at 0..2047;
+    the result matches the decoupled f64 oracle over those stored rows."""
+    engine, model, runner = _mods()
+    from dataclasses import replace
+    shape = replace(model.shape("7b"), layers=2, vocab=1024)
+    eng = engine.Engine(shape, host_blocks=264, block_tokens=128, seed=4, max_new=32768,
+                        read_buffer_bytes=1 << 30)
+    rng = np.random.default_rng(4)
+    hist = torch.as_tensor(rng.integers(0, shape.vocab, 32768))
+    eng.install_history("doc", hist)
+    torch.cuda.synchronize()
+    assert eng.store.peek("doc").tokens == 32768
+    nb_before = len(eng.store.block_table("doc"))
+    before = session_cache(eng, "doc", 32768)
+    new_ids = torch.as_tensor(rng.integers(0, shape.vocab, 256))
+    o = eng.turn("doc", 1, new_ids, torch.as_tensor(rng.integers(0, shape.vocab, 64)),
+                 want_logits=True)
+    torch.cuda.synchronize()
+    assert (o.kept, o.drop, o.hit) == (2048, 30720, "memory_hit")       # SURVEY.md §8d C4
+    assert nb_before == 256
+    cache = [(K[o.drop:], V[o.drop:]) for K, V in before]
+    want, _ = llama_ref.forward(eng.runner.w.to_numpy(), new_ids.numpy(), cache, np.arange(2048),
+                                n_heads=shape.n_heads, n_kv_heads=shape.n_kv_heads,
+                                head_dim=shape.head_dim)
+    got = o.result.logits.cpu().numpy().astype(np.float64)
+    assert rope_ref.rel_err(got, want[-1]) <= LOGIT_TOL
+    # only the kept rows crossed the host link
+    assert o.result.bytes_loaded == 2048 * shape.kv_bytes_per_token
+    eng.store.check_invariants()
