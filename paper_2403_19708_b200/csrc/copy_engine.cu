@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -36,6 +37,17 @@ void clear_error() { g_last_error.clear(); }
 
 namespace {
 
+// cudaMemcpyFlagPreferOverlapWithCompute is a tuning knob (ASKV_COPY_OVERLAP=1);
+// default 0 keeps the DMAs on the copy engines.
+unsigned copy_flags() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ASKV_COPY_OVERLAP");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v ? (unsigned)cudaMemcpyFlagPreferOverlapWithCompute : 0u;
+}
+
 // Issue a list of same-direction copies in stream order.
 // Pointers are UVA-classified (cudaMemcpyDefault), so the same entry points
 // serve a pinned-host arena (H2D / D2H over the host link) and an
@@ -45,7 +57,7 @@ int issue_batch(std::vector<void*>& dsts, std::vector<void*>& srcs, std::vector<
   if (dsts.empty()) return ASKV_OK;
   cudaMemcpyAttributes attr = {};
   attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+  attr.flags = copy_flags();
   size_t attr_idx = 0;
   size_t fail_idx = 0;
   cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(),

@@ -70,36 +70,65 @@ __global__ void rope_table_kernel(float* __restrict__ table, int max_pos, int ha
   }
 }
 
+// K2: one CTA per kReRows consecutive rows.  The rows' cos/sin (kReRows x
+// HD/2 float2) are staged in shared memory once, then every thread streams
+// 16-byte vectors of the rows (4 in flight per thread), rotating K vectors
+// and copying V vectors.  Source rows come through the session block table.
+constexpr int kReRows = 2;
+
 template <int HD>
 __global__ void __launch_bounds__(kThreads)
     reembed_kernel(const __nv_bfloat16* __restrict__ src, const int64_t* __restrict__ blk_off,
                    int block_tokens, int64_t src_row_stride, int64_t first_token, int kept,
                    int hkv, const float* __restrict__ table, const int32_t* __restrict__ positions,
                    int pos0, __nv_bfloat16* __restrict__ dst, int64_t dst_row_stride) {
+  constexpr int kHalf = HD / 2;
   constexpr int kUnitsPerHead = HD / 8;
-  const int k_units = hkv * kUnitsPerHead;
-  const int row_units = 2 * k_units;
-  const int64_t total = (int64_t)kept * row_units;
-  for (int64_t g = blockIdx.x * (int64_t)kThreads + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * kThreads) {
-    const int i = (int)(g / row_units);
-    const int u = (int)(g - (int64_t)i * row_units);
-    const int64_t t = first_token + i;
-    const __nv_bfloat16* srow;
+  __shared__ __align__(16) float cs_s[kReRows * kHalf * 2];
+  __shared__ const __nv_bfloat16* srow_s[kReRows];
+  const int row0 = blockIdx.x * kReRows;
+  const int nrows = min(kReRows, kept - row0);
+  for (int i = threadIdx.x; i < nrows * kHalf; i += kThreads) {
+    const int rr = i / kHalf, pi = i - rr * kHalf;
+    const int pos = positions ? positions[row0 + rr] : pos0 + row0 + rr;
+    const float2 v = reinterpret_cast<const float2*>(table)[(int64_t)pos * kHalf + pi];
+    reinterpret_cast<float2*>(cs_s)[i] = v;
+  }
+  if (threadIdx.x < nrows) {
+    const int64_t t = first_token + row0 + threadIdx.x;
     if (blk_off != nullptr) {
       const int64_t b = t / block_tokens;
-      srow = src + blk_off[b] + (t - b * block_tokens) * src_row_stride;
+      srow_s[threadIdx.x] = src + blk_off[b] + (t - b * block_tokens) * src_row_stride;
     } else {
-      srow = src + t * src_row_stride;
+      srow_s[threadIdx.x] = src + t * src_row_stride;
     }
-    int4 v = ld_nc16(srow + u * 8);
-    if (u < k_units) {
-      const int d0 = (u % kUnitsPerHead) * 8;
-      const int pos = positions ? positions[i] : pos0 + i;
-      const float* cs = table + ((int64_t)pos * (HD / 2) + d0 / 2) * 2;
-      v = rotate8(v, cs);
+  }
+  __syncthreads();
+  const int k_units = hkv * kUnitsPerHead;
+  const int row_units = 2 * k_units;
+  const int total = nrows * row_units;
+  constexpr int kIlp = 4;
+  for (int base = threadIdx.x; base < total; base += kThreads * kIlp) {
+    int4 v[kIlp];
+#pragma unroll
+    for (int k = 0; k < kIlp; ++k) {
+      const int g = base + k * kThreads;
+      if (g < total) {
+        const int rr = g / row_units;
+        v[k] = ld_nc16(srow_s[rr] + (g - rr * row_units) * 8);
+      }
     }
-    st16(dst + (int64_t)i * dst_row_stride + u * 8, v);
+#pragma unroll
+    for (int k = 0; k < kIlp; ++k) {
+      const int g = base + k * kThreads;
+      if (g < total) {
+        const int rr = g / row_units;
+        const int u = g - rr * row_units;
+        int4 x = v[k];
+        if (u < k_units) x = rotate8(x, cs_s + (rr * kHalf + (u % kUnitsPerHead) * 4) * 2);
+        st16(dst + (int64_t)(row0 + rr) * dst_row_stride + u * 8, x);
+      }
+    }
   }
 }
 
@@ -200,8 +229,7 @@ extern "C" int askv_reembed(const void* src_base, const int64_t* src_block_off,
                "reembed: row strides must be multiples of 8 elements");
   if (kept == 0) return ASKV_OK;
   ASKV_REQUIRE(src_base && dst && rope_table, "reembed: null pointer");
-  const int64_t units = (int64_t)kept * 2 * n_kv_heads * (head_dim / 8);
-  const int grid = grid_for(units);
+  const int grid = (kept + kReRows - 1) / kReRows;
   auto* s = static_cast<const __nv_bfloat16*>(src_base);
   auto* d = static_cast<__nv_bfloat16*>(dst);
   if (head_dim == 128)

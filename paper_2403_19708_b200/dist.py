@@ -53,3 +53,57 @@ def max_over_ranks(x: float, device=None) -> float:
 
 def sum_over_ranks(x: float, device=None) -> float:
     return _reduce(x, dist.ReduceOp.SUM, device or "cpu")
+
+
+class NcclAllReduce:
+    """tp_reduce hook for a real TP group: in-place sum over the default group
+    (NCCL over NVLink / NVSwitch), ordered on the runner's compute stream."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    def __call__(self, t: torch.Tensor, stream) -> None:
+        with torch.cuda.stream(stream):
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+
+class ThreadAllReduce:
+    """tp_reduce hook for a 1-GPU emulation of a TP group: one Python thread per
+    rank, each driving its own Runner/streams; partials are summed on the GPU
+    in a fixed rank order (deterministic) and copied back in place."""
+
+    def __init__(self, world: int):
+        import threading
+
+        self.world = world
+        self._bar = threading.Barrier(world)
+        self._slots: list = [None] * world
+        self._done = None
+
+    def bind(self, rank: int):
+        return lambda t, stream: self._reduce(rank, t, stream)
+
+    def _reduce(self, rank: int, t: torch.Tensor, stream) -> None:
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self._slots[rank] = (t, ev, stream)
+        self._bar.wait()
+        if rank == 0:
+            with torch.cuda.stream(stream):
+                for _, e, _ in self._slots:
+                    stream.wait_event(e)
+                acc = self._slots[0][0].float()
+                for r in range(1, self.world):
+                    acc += self._slots[r][0].float()
+                total = acc.to(t.dtype)
+                done = torch.cuda.Event()
+                done.record(stream)
+            for _, _, s in self._slots[1:]:
+                total.record_stream(s)   # other ranks read it on their streams
+            self._done = (total, done)
+        self._bar.wait()
+        total, done = self._done
+        stream.wait_event(done)
+        with torch.cuda.stream(stream):
+            t.copy_(total)
+        self._bar.wait()

@@ -60,7 +60,8 @@ class Engine:
     def __init__(self, shape: LlamaShape, *, host_blocks: int, block_tokens: int = 128,
                  device="cuda", seed: int = 0, weights: LlamaWeights | None = None,
                  read_buffer_bytes: int = 1 << 30, max_new: int = 1024,
-                 truncation_ratio: float = 0.5, ttl: float = math.inf, pin: bool = True):
+                 truncation_ratio: float = 0.5, ttl: float = math.inf, pin: bool = True,
+                 tp_reduce=None):
         self.shape = shape
         self.profile = profile_for(shape, truncation_ratio=truncation_ratio)
         self.block_tokens = block_tokens
@@ -74,7 +75,7 @@ class Engine:
                              block_tokens=block_tokens, host_arena=self.arena,
                              read_buffer_bytes=read_buffer_bytes,
                              max_new=shape.context_window + max_new,
-                             max_ctx=shape.context_window + max_new)
+                             max_ctx=shape.context_window + max_new, tp_reduce=tp_reduce)
         self.window = shape.context_window
         self.cut = self.profile.cut_tokens
         self.context: dict[str, int] = {}

@@ -66,6 +66,33 @@ class LlamaWeights:
         self.w_final = torch.ones(s.d_model, dtype=BF16, device=device)
         self.lm_head = rnd(s.vocab, s.d_model)
 
+    def shard(self, rank: int, tp: int) -> "LlamaWeights":
+        """Head-parallel tensor-parallel shard (Megatron layout):
+        q-heads [r*Hq/tp, (r+1)*Hq/tp), kv-heads [r*Hkv/tp, ...), the matching
+        rows of W_qkv / columns of W_o, rows r of the gate/up split and columns of
+        W_down.  Norms, embedding and lm_head are replicated."""
+        s = self.shape
+        sh = s.tp_shard(tp)
+        hd = s.head_dim
+        out = LlamaWeights.__new__(LlamaWeights)
+        out.shape = sh
+        out.embed = self.embed
+        out.w_final = self.w_final
+        out.lm_head = self.lm_head
+        qa, qb = rank * sh.n_heads * hd, (rank + 1) * sh.n_heads * hd
+        ka, kb = rank * sh.n_kv_heads * hd, (rank + 1) * sh.n_kv_heads * hd
+        fa, fb = rank * sh.ffn, (rank + 1) * sh.ffn
+        qoff, koff, voff = 0, s.n_heads * hd, (s.n_heads + s.n_kv_heads) * hd
+        out.layers = []
+        for l in self.layers:
+            wqkv = torch.cat([l["wqkv"][qoff + qa: qoff + qb], l["wqkv"][koff + ka: koff + kb],
+                              l["wqkv"][voff + ka: voff + kb]]).contiguous()
+            wgu = torch.cat([l["wgu"][fa:fb], l["wgu"][s.ffn + fa: s.ffn + fb]]).contiguous()
+            out.layers.append({"w_in": l["w_in"], "wqkv": wqkv,
+                               "wo": l["wo"][:, qa:qb].contiguous(), "w_post": l["w_post"],
+                               "wgu": wgu, "wd": l["wd"][:, fa:fb].contiguous()})
+        return out
+
     def to_numpy(self) -> dict:
         """float64 copies in the oracle's [in, out] convention (tests only)."""
         f = lambda t: t.float().cpu().numpy().astype("float64")  # noqa: E731
@@ -142,7 +169,8 @@ class Runner:
                  device="cuda", seed: int = 0, theta_base: float = 10000.0,
                  block_tokens: int = 128, host_arena=None, hbm_arena: torch.Tensor | None = None,
                  read_buffer_bytes: int = 4 << 30, write_buffer_bytes: int = 2 << 30,
-                 max_new: int = 1024, max_ctx: int | None = None, timeline: bool = True):
+                 max_new: int = 1024, max_ctx: int | None = None, timeline: bool = True,
+                 tp_reduce=None):
         self.shape = s = shape
         self.device = torch.device(device)
         self.w = weights or LlamaWeights(shape, seed=seed, device=device)
@@ -181,6 +209,10 @@ class Runner:
         self._last_save: dict = {}
         self._bufs = {}
         self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
+        # tensor parallelism (config C5): tp_reduce(t, stream) sums the row-parallel
+        # partials of W_o and W_down over the TP group in place (NCCL all-reduce
+        # over NVLink in a multi-GPU run; dist.ThreadAllReduce in the 1-GPU emulation)
+        self.tp_reduce = tp_reduce
         self.launches = 0          # libaskv kernel launches issued (all streams)
         self.probe = None          # list -> (kind, ev0, ev1, work) per probed launch
 
@@ -379,11 +411,21 @@ class Runner:
                                  num_splits=splits, stream=cs)
                 self._probe_end(p0, "attention", attention_flops(kept, n, hq, hd))
                 self.launches += 2 if splits > 1 else 1
-                x = torch.addmm(x, ao, lw["wo"].t())
+                if self.tp_reduce is None:
+                    x = torch.addmm(x, ao, lw["wo"].t())
+                else:
+                    y = torch.mm(ao, lw["wo"].t())
+                    self.tp_reduce(y, cs)
+                    x = x + y
                 h = ops.rmsnorm(x, lw["w_post"], 1e-5, stream=cs)
                 gu = F.linear(h, lw["wgu"])
                 a = ops.silu_mul(gu, stream=cs)
-                x = torch.addmm(x, a, lw["wd"].t())
+                if self.tp_reduce is None:
+                    x = torch.addmm(x, a, lw["wd"].t())
+                else:
+                    y = torch.mm(a, lw["wd"].t())
+                    self.tp_reduce(y, cs)
+                    x = x + y
                 self.launches += 3
                 l1 = ev() if ev else None
                 if l1:

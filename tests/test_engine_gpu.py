@@ -199,3 +199,54 @@ def test_c4_long_context_32k_history_truncated_reuse():
     # only the kept rows crossed the host link
     assert o.result.bytes_loaded == 2048 * shape.kv_bytes_per_token
     eng.store.check_invariants()
+
+
+def test_tensor_parallel_emulation_matches_unsharded():
+    """Config C5's decomposition (head-parallel QKV / attention / KV store per
+    rank, row-parallel W_o and W_down + all-reduce), emulated with 4 ranks on
+    one GPU (one thread + Runner + host arena per rank, ThreadAllReduce in
+    place of NCCL): the multi-turn reuse path equals the unsharded model."""
+    import threading
+    from dataclasses import replace
+    engine, model, runner = _mods()
+    from paper_2403_19708_b200.dist import ThreadAllReduce
+    shape = replace(model.shape("tiny"), n_heads=8, n_kv_heads=4, d_model=512)
+    tp = 4
+    full = runner.LlamaWeights(shape, seed=5)
+    rng = np.random.default_rng(5)
+    turns = [(torch.as_tensor(rng.integers(0, shape.vocab, 40)),
+              torch.as_tensor(rng.integers(0, shape.vocab, 10))) for _ in range(3)]
+
+    ref = engine.Engine(shape, host_blocks=32, block_tokens=16, weights=full, max_new=64,
+                        read_buffer_bytes=16 << 20)
+    want = []
+    for k, (n, o) in enumerate(turns):
+        want.append(ref.turn("s", k, n, o, want_logits=True).result.logits.cpu().double())
+
+    red = ThreadAllReduce(tp)
+    got = [[None] * len(turns) for _ in range(tp)]
+    errs = []
+
+    def rank(r):
+        try:
+            torch.cuda.set_device(0)
+            eng = engine.Engine(shape.tp_shard(tp), host_blocks=32, block_tokens=16,
+                                weights=full.shard(r, tp), max_new=64,
+                                read_buffer_bytes=16 << 20, tp_reduce=red.bind(r))
+            for k, (n, o) in enumerate(turns):
+                res = eng.turn("s", k, n, o, want_logits=True).result
+                torch.cuda.synchronize()
+                got[r][k] = res.logits.cpu().double()
+            assert eng.store.peek("s").tokens == ref.store.peek("s").tokens
+        except Exception as exc:  # pragma: no cover - surfaced below
+            errs.append(exc)
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(tp)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for k in range(len(turns)):
+        for r in range(tp):
+            assert rope_ref.rel_err(got[r][k].numpy(), want[k].numpy()) <= LOGIT_TOL, (k, r)

@@ -70,6 +70,32 @@ def reembed(args):
         print(json.dumps(dict(kept=kept, hkv=hkv, us=t * 1e6, gbs=by / t / 1e9)))
 
 
+def sweep(args):
+    """Time every split count for a few shapes (tunes choose_splits)."""
+    from paper_2403_19708_b200 import ops
+    from paper_2403_19708_b200.runner import attention_flops
+    shapes = [(2142, 237, 40, 40), (2869, 301, 40, 40), (1000, 100, 40, 40), (3600, 700, 40, 40),
+              (2048, 256, 8, 1), (500, 60, 40, 40), (3800, 120, 40, 40), (2000, 400, 32, 32)]
+    for kept, n, hq, hkv in shapes:
+        d = 128
+        q = torch.randn(n, hq, d, device="cuda").to(torch.bfloat16)
+        kv = torch.randn(kept + n, 2, hkv, d, device="cuda").to(torch.bfloat16)
+        o = torch.empty(n, hq, d, device="cuda", dtype=torch.bfloat16)
+        auto = ops.attn_num_splits(kept, n, hq)
+        res = {}
+        for s in (1, 2, 3, 4, 5, 6, 8, 10, 12, 16):
+            if s > (kept + n + 127) // 128:
+                continue
+            ws = torch.empty(max(1, ops.attn_workspace_bytes(kept, n, hq, d, s)),
+                             dtype=torch.uint8, device="cuda")
+            t = timeit(lambda: ops.prefill_attn(q, kv, kept, n, hq, hkv, d, o, ws, num_splits=s),
+                       reps=10)
+            res[s] = round(t * 1e6, 1)
+        best = min(res, key=res.get)
+        print(json.dumps(dict(kept=kept, n=n, hq=hq, hkv=hkv, auto=auto, best=best, us=res,
+                              best_tflops=attention_flops(kept, n, hq, d) / res[best] / 1e6)))
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("what")
@@ -79,4 +105,4 @@ if __name__ == "__main__":
     ap.add_argument("--reps", type=int, default=20)
     a = ap.parse_args()
     os.environ["ASKV_ATTN_KERNEL"] = a.kernel
-    {"attn": attn, "reembed": reembed}[a.what](a)
+    {"attn": attn, "reembed": reembed, "sweep": sweep}[a.what](a)

@@ -1,0 +1,81 @@
+// Micro-probe: cost of one attention softmax tile step (pass 1 row max over
+// 128 TMEM columns, pass 2 exp2 + bf16 pack + tcgen05.st of P) for one warpgroup,
+// with variants that remove pieces.  clock64 per iteration, 1 CTA per SM.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../paper_2403_19708_b200/csrc/askv_ptx.cuh"
+using namespace askv;
+
+template <int MODE>  // 0 full, 1 ex2->fmul, 2 no pass1, 3 ex2 poly
+__global__ void probe(long long* out, float* sink, int iters) {
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0) tmem_alloc(&slot, 256);
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  const uint32_t tmem = slot + ((uint32_t)(warp * 32) << 16);
+  float init[32];
+  for (int e = 0; e < 32; ++e) init[e] = 0.01f * (lane + e);
+  for (int c = 0; c < 4; ++c) tmem_st32(tmem + c * 32, init);
+  tmem_wait_st();
+  float acc = 0.f, m_acc = 1.f;
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    float mx = -INFINITY;
+    if (MODE != 2) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float sv[32];
+        tmem_ld32(tmem + c * 32, sv);
+        float m4[4] = {sv[0], sv[1], sv[2], sv[3]};
+#pragma unroll
+        for (int e = 4; e < 32; ++e) m4[e & 3] = fmaxf(m4[e & 3], sv[e]);
+        mx = fmaxf(mx, fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])));
+      }
+    }
+    const float neg_m = -(mx > m_acc ? mx : m_acc);
+    float ls[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float sv[32];
+      tmem_ld32(tmem + c * 32, sv);
+      uint32_t pk[16];
+#pragma unroll
+      for (int e = 0; e < 32; e += 2) {
+        float x0 = fmaf(sv[e], 1.44f, neg_m), x1 = fmaf(sv[e + 1], 1.44f, neg_m);
+        float p0, p1;
+        if (MODE == 1) { p0 = x0 * 0.5f; p1 = x1 * 0.5f; }
+        else if (MODE == 3) { p0 = ex2_poly(x0); p1 = ex2_poly(x1); }
+        else { p0 = ex2(x0); p1 = ex2(x1); }
+        ls[(e >> 1) & 3] += p0 + p1;
+        pk[e >> 1] = pack_bf16x2(p0, p1);
+      }
+      tmem_st16(tmem + 128 + c * 16, pk);
+    }
+    tmem_wait_st();
+    acc += ls[0] + ls[1] + ls[2] + ls[3];
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+  tc_fence_before(); __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc(slot, 256); }
+}
+
+int main() {
+  long long* d; float* sink;
+  cudaMalloc(&d, 1024 * 8); cudaMalloc(&sink, 1 << 22);
+  const char* names[4] = {"full", "ex2->fmul", "no pass1", "ex2 poly"};
+  for (int mode = 0; mode < 4; ++mode)
+    for (int wgs : {1, 2}) {
+      auto k = mode == 0 ? probe<0> : mode == 1 ? probe<1> : mode == 2 ? probe<2> : probe<3>;
+      const int iters = 200;
+      // wgs warpgroups per SM: run 2 CTAs of 128 threads per SM when wgs == 2
+      k<<<148 * wgs, 128>>>(d, sink, iters);
+      cudaDeviceSynchronize();
+      long long h[296]; cudaMemcpy(h, d, 148 * wgs * 8, cudaMemcpyDeviceToHost);
+      double mx = 0; for (int i = 0; i < 148 * wgs; ++i) mx = h[i] > mx ? h[i] : mx;
+      printf("%-10s WG/SM=%d: %.0f cycles per tile step\n", names[mode], wgs, mx / iters);
+    }
+  return 0;
+}

@@ -1,0 +1,105 @@
+"""Per-kernel breakdown + GPU idle fraction of a bench step (torch.profiler /
+CUPTI; nsys is not in the image).  Diagnostics only, never a bench number.
+
+    python tools/step_profile.py [--mode hbm|host|recompute] [--turns 4]
+"""
+import argparse
+import collections
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--mode", default="hbm")
+    ap.add_argument("--turns", type=int, default=4)
+    ap.add_argument("--config", default="c3")
+    a = ap.parse_args()
+    import bench
+    from paper_2403_19708_b200 import model
+    from paper_2403_19708_b200.runner import Job, Runner
+    from paper_2403_19708_b200.store import HostArena
+
+    shape = model.shape(bench.CONFIGS[a.config][0])
+    turns, _ = bench.select_turns(a.config, 0, 1, a.turns)
+    tb = 128
+    bb = tb * shape.kv_bytes_per_token
+    nbs = [-(-(k + n) // tb) for _, _, k, n in turns]
+    arena = HostArena(sum(nbs), bb, pin=True)
+    hbm = torch.zeros(sum(nbs) * bb // 2, dtype=torch.bfloat16, device="cuda")
+    runner = Runner(shape, host_arena=arena, hbm_arena=hbm, read_buffer_bytes=4 << 30,
+                    write_buffer_bytes=1 << 30, max_new=max(n for *_, n in turns),
+                    max_ctx=4096, timeline=False)
+    jobs, pos = [], 0
+    rng = np.random.default_rng(0)
+    for (sid, k, kept, new), nb in zip(turns, nbs):
+        ids = list(range(pos, pos + nb))
+        pos += nb
+        toks = torch.as_tensor(rng.integers(0, shape.vocab, new))
+        if a.mode == "hbm":
+            off = torch.as_tensor([b * bb // 2 for b in ids], dtype=torch.int64, device="cuda")
+            jobs.append(Job(f"{sid}#{k}", toks.cuda(), kept=kept, source="hbm", block_ids=ids,
+                            save=True, dev_block_off=off))
+        elif a.mode == "host":
+            jobs.append(Job(f"{sid}#{k}", toks.pin_memory(), kept=kept, source="host",
+                            block_ids=ids, save=True))
+        else:
+            jobs.append(Job(f"{sid}#{k}",
+                            torch.as_tensor(rng.integers(0, shape.vocab, kept + new)).cuda()))
+    for _ in range(2):
+        runner.run(jobs)
+        runner.join()
+    torch.cuda.synchronize()
+    from torch.profiler import ProfilerActivity, profile
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+        e0.record(runner.s_compute)
+        runner.run(jobs)
+        runner.join()
+        e1.record(runner.s_compute)
+        torch.cuda.synchronize()
+    wall_us = e0.elapsed_time(e1) * 1e3
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    busy = []
+    for ev in prof.events():
+        if ev.device_type == torch.autograd.DeviceType.CUDA and ev.time_range.elapsed_us() > 0:
+            name = ev.name
+            for key in ("attn_fwd", "attn_combine", "reembed", "rope_new", "rmsnorm", "silu_mul",
+                        "nvjet", "gemm", "Memcpy", "elementwise", "embedding", "argmax",
+                        "reduce"):
+                if key.lower() in name.lower():
+                    name = key
+                    break
+            agg[name][0] += 1
+            agg[name][1] += ev.time_range.elapsed_us()
+            busy.append((ev.time_range.start, ev.time_range.end, name))
+    # compute-stream kernels only (exclude memcpy) for the idle estimate
+    ker = sorted((s, e) for s, e, n in busy if n != "Memcpy")
+    merged = 0.0
+    cs, ce = None, None
+    for s, e in ker:
+        if cs is None or s > ce:
+            if cs is not None:
+                merged += ce - cs
+            cs, ce = s, e
+        else:
+            ce = max(ce, e)
+    if cs is not None:
+        merged += ce - cs
+    cpu_total = sum(ev.cpu_time_total for ev in prof.events()
+                    if ev.device_type == torch.autograd.DeviceType.CPU and ev.name == "aten::linear")
+    out = {"mode": a.mode, "turns": len(jobs), "wall_us": wall_us,
+           "kernel_busy_us": merged, "gpu_idle_frac": 1 - merged / wall_us,
+           "kernels": {k: {"n": v[0], "us": round(v[1], 1), "avg_us": round(v[1] / v[0], 2)}
+                       for k, v in sorted(agg.items(), key=lambda x: -x[1][1])}}
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
