@@ -44,6 +44,7 @@ METRIC = "multi-turn prefill tokens/s and p50 TTFT vs recompute; H2D GB/s per GP
 CONFIGS = {
     "c2": ("llama2-7b", "workload_c2.json"),
     "c3": ("llama2-13b", "workload_c3.json"),
+    "c4": ("llama2-7b", None),   # long-context overflow: 32K history at W = 4096
 }
 
 
@@ -66,9 +67,35 @@ def parse():
 # workload
 # ---------------------------------------------------------------------------
 
+def long_context_turns(rank: int, n: int, history: int = 32768, new: int = 256,
+                       output: int = 64, window: int = 4096):
+    """Config C4: sessions with a stored 32K-token history, then
+    turns of 256 in / 64 out at W = 4096.  Turn k reuses kept_k rows after the
+    reference truncation rules (sim.py:468-483, 576-581): 2048, 2368, ... 3648."""
+    from paper_2403_19708_b200.engine import overflow_kept, save_truncate
+
+    cut = window // 2
+    shapes = []
+    ctx = history
+    for k in range(6):
+        kept = overflow_kept(ctx, new, window, cut)
+        shapes.append((k, kept))
+        ctx = save_truncate(kept + new + output, window, cut)
+    out = []
+    i = 0
+    while len(out) < n:
+        k, kept = shapes[i % len(shapes)]
+        out.append((f"long{rank}_{i // len(shapes)}", k, kept, new))
+        i += 1
+    return out, len(out)
+
+
 def select_turns(cfg: str, rank: int, world: int, n: int):
     """Hit turns of this rank's session shard (stable crc32 hash), seeded sample."""
     from paper_2403_19708_b200.engine import overflow_kept, save_truncate
+
+    if cfg == "c4":
+        return long_context_turns(rank, n)
 
     wl = json.loads((ROOT / "tests" / "golden" / CONFIGS[cfg][1]).read_text())
     w, ratio = wl["window"], wl["truncation_ratio"]
@@ -411,9 +438,14 @@ def main():
         "data": "synthetic (reference ShareGPT-shaped session generator; random-init weights "
                 "and KV)",
         "config": {
-            "workload": f"{args.config}: {shape.name}-shaped, generate_poisson(512, seed=7) "
-                        f"sessions sharded by crc32(session) over {world} GPU(s); "
-                        f"{len(turns)} hit turns/GPU/step (of {n_hits} in shard)",
+            "workload": (f"{args.config}: {shape.name}-shaped, reference generate_poisson "
+                         f"sessions sharded by crc32(session) over {world} GPU(s); "
+                         f"{len(turns)} hit turns/GPU/step (of {n_hits} in shard)"
+                         if args.config != "c4" else
+                         f"c4: {shape.name}-shaped, W=4096, 32768-token stored histories "
+                         f"truncated by the reference rules to kept 2048..3648 (block-table "
+                         f"edit; only the kept blocks are materialised and loaded), 256 new "
+                         f"tokens per turn, {len(turns)} turns/GPU/step"),
             "turns_per_gpu": len(turns), "kept_p50": percentile(kept_l, 0.5),
             "new_p50": percentile(new_l, 0.5), "block_tokens": tb,
             "value_mode": "KV resident in an HBM arena (no host link)",

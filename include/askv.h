@@ -145,6 +145,13 @@ int askv_save_layer(void* host_base, const int64_t* block_ids, int nblocks,
                     void* stream, void* done_event);
 
 /*
+ * Small copy executed by SMs through unified addressing (pinned host <-> device):
+ * keeps the few-KB per-job transfers (token ids in, first token out) off the
+ * copy engines that are busy with the pre-loader / saver DMAs.  bytes <= 16 MiB.
+ */
+int askv_copy_sm(void* dst, const void* src, size_t bytes, void* stream);
+
+/*
  * Fused elementwise ops of the LLaMA block the runner executes around the path
  * (no reference counterpart; the reference has no model):
  *   askv_rmsnorm : y[r] = x[r] * rsqrt(mean(x[r]^2) + eps) * w   (bf16 io, fp32 math)

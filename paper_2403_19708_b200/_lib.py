@@ -39,6 +39,7 @@ SIGNATURES = {
     "askv_save_layer": (_i32, [_vp, _pi64, _i32, _i64, _i64, _i32, _i64, _i64, _i32, _vp, _vp,
                                _vp]),
     "askv_rmsnorm": (_i32, [_vp, _vp, _vp, _i32, _i32, _f32, _vp]),
+    "askv_copy_sm": (_i32, [_vp, _vp, _sz, _vp]),
     "askv_silu_mul": (_i32, [_vp, _vp, _i32, _i32, _vp]),
 }
 

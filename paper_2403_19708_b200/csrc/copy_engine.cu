@@ -72,10 +72,32 @@ int issue_batch(std::vector<void*>& dsts, std::vector<void*>& srcs, std::vector<
   return ASKV_OK;
 }
 
+// Small transfers done by SMs through UVA (pinned host memory is device
+// addressable): token ids in, first token out.  They must not queue behind
+// the multi-GB pre-load / save DMAs on the copy engines (which would put the
+// whole pre-load of the next job in front of this job's 2 KB of token ids).
+__global__ void copy_sm_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                               size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
 }  // namespace
 }  // namespace askv
 
 using namespace askv;
+
+extern "C" int askv_copy_sm(void* dst, const void* src, size_t bytes, void* stream) {
+  clear_error();
+  ASKV_REQUIRE(bytes <= (size_t)1 << 24, "copy_sm: %zu bytes is not a small transfer", bytes);
+  if (bytes == 0) return ASKV_OK;
+  ASKV_REQUIRE(dst && src, "copy_sm: null pointer");
+  const int blocks = (int)((bytes + 255) / 256) < 64 ? (int)((bytes + 255) / 256) : 64;
+  copy_sm_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<uint8_t*>(dst),
+                                                           static_cast<const uint8_t*>(src), bytes);
+  return launch_status("copy_sm launch");
+}
 
 extern "C" int askv_version(void) { return 100; }
 

@@ -167,3 +167,14 @@ def silu_mul(gu: torch.Tensor, out=None, *, stream=None):
     check(lib().askv_silu_mul(gu.data_ptr(), out.data_ptr(), int(rows), int(ffn),
                               _stream(stream)), "silu_mul")
     return out
+
+
+def copy_sm(dst: torch.Tensor, src: torch.Tensor, *, stream=None) -> torch.Tensor:
+    """dst <- src by SMs (pinned host <-> device via UVA), for few-KB transfers."""
+    n = src.numel() * src.element_size()
+    if dst.numel() * dst.element_size() < n:
+        raise ValueError("copy_sm: destination too small")
+    if not src.is_cuda and not src.is_pinned():
+        raise ValueError("copy_sm: host source must be pinned")
+    check(lib().askv_copy_sm(dst.data_ptr(), src.data_ptr(), int(n), _stream(stream)), "copy_sm")
+    return dst

@@ -27,7 +27,8 @@ preload_layer, save_layer).
 from __future__ import annotations
 
 import math
-from collections import deque
+import queue
+import threading
 from dataclasses import dataclass, field
 
 import torch
@@ -158,7 +159,43 @@ def attention_flops(kept: int, n: int, hq: int, hd: int) -> int:
 
 
 class _Unit:
-    __slots__ = ("seq", "slot", "job", "layer", "start", "end")
+    """One (job, layer) pre-load: a read-buffer slot, its DMA events and a host
+    flag set once the IO thread has submitted the DMA."""
+    __slots__ = ("seq", "slot", "start", "end", "issued")
+
+
+class _IOThread(threading.Thread):
+    """Submits copy-engine work (pre-load / save DMA batches) from its own host
+    thread, FIFO.  A multi-GB pre-load queue can block cudaMemcpyBatchAsync on
+    stream back-pressure; on the compute thread that would starve kernel
+    issue (the paper's system likewise uses dedicated IO threads)."""
+
+    def __init__(self, device, name):
+        super().__init__(name=name, daemon=True)
+        dev = torch.device(device)
+        self.device_index = dev.index if dev.index is not None else torch.cuda.current_device()
+        self.q: queue.Queue = queue.Queue()
+        self.error = None
+        self.start()
+
+    def run(self):
+        try:
+            torch.cuda.set_device(self.device_index)
+        except BaseException as exc:
+            self.error = exc
+        while True:
+            fn = self.q.get()
+            if fn is None:
+                return
+            try:
+                fn()
+            except BaseException as exc:  # surfaced on the compute thread
+                self.error = exc
+
+    def submit(self, fn):
+        if self.error is not None:
+            raise RuntimeError("IO thread failed") from self.error
+        self.q.put(fn)
 
 
 class Runner:
@@ -195,18 +232,18 @@ class Runner:
         self.n_slots = max(2, int(read_buffer_bytes // slot_bytes))
         self.slots = torch.empty((self.n_slots, self.slot_rows, s.row_elems), dtype=BF16,
                                  device=self.device)
-        self._pending: deque = deque()
-        self._issued: dict = {}
-        self._seq_issued = 0
-        self._seq_released = 0
-        self._freed = [None] * self.n_slots
+        self._units: dict = {}          # (jid, layer) -> _Unit
+        self._seq = 0                    # pre-load units enqueued so far
+        self._freed: dict = {}           # unit seq -> (event on s_compute, host flag)
+        self._io_load = _IOThread(self.device, "askv-preload")
+        self._io_save = _IOThread(self.device, "askv-save")
         # write buffer: ring of per-layer slots of max_new rows
         self.n_wslots = max(2, int(write_buffer_bytes // (max_new * s.row_bytes)))
         self.wbuf = torch.empty((self.n_wslots, max_new, s.row_elems), dtype=BF16,
                                 device=self.device)
         self._wseq = 0
-        self._wdone = [None] * self.n_wslots
-        self._last_save: dict = {}
+        self._wdone = [None] * self.n_wslots   # (event on s_save, host flag) per slot
+        self._last_save: dict = {}             # session -> (event, flag) of its last save
         self._bufs = {}
         self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
         # tensor parallelism (config C5): tp_reduce(t, stream) sums the row-parallel
@@ -231,6 +268,10 @@ class Runner:
 
     # ------------------------------------------------------------------ K1 pre-loader
     def _enqueue_loads(self, jid, job: Job):
+        """Queue the job's L pre-load units for the IO thread.  Unit seq k uses
+        slot k % n_slots and first waits (host flag, then device event) for the
+        release of unit k - n_slots, so the copy stream runs as far ahead as
+        the read buffer allows -- across jobs, i.e. the read-buffer head start."""
         if job.source != "host" or job.kept == 0:
             return
         if self.host_arena is None:
@@ -243,47 +284,82 @@ class Runner:
         ids = list(job.block_ids[:nb])
         dep = self._last_save.get(job.session_id)
         for layer in range(self.shape.layers):
-            self._pending.append((jid, layer, ids, tail, dep))
-
-    def _pump(self):
-        while self._pending and self._seq_issued < self._seq_released + self.n_slots:
-            jid, layer, ids, tail, dep = self._pending.popleft()
             u = _Unit()
-            u.seq = self._seq_issued
+            u.seq = self._seq
             u.slot = u.seq % self.n_slots
-            u.job, u.layer = jid, layer
-            with torch.cuda.stream(self.s_load):
-                if self._freed[u.slot] is not None:
-                    self.s_load.wait_event(self._freed[u.slot])
-                if dep is not None:  # rows saved by this session's previous turn
-                    self.s_load.wait_event(dep)
-                u.start = torch.cuda.Event(enable_timing=self.timeline)
-                u.end = torch.cuda.Event(enable_timing=self.timeline)
-                u.start.record(self.s_load)
-                ops.preload_layer(self.slots[u.slot], self.host_arena.buffer, ids,
-                                  self.block_bytes, layer * self.chunk_bytes, self.chunk_bytes,
-                                  tail, stream=self.s_load)
-                u.end.record(self.s_load)
-            self._issued[(jid, layer)] = u
-            self._seq_issued += 1
+            u.start = torch.cuda.Event(enable_timing=self.timeline)
+            u.end = torch.cuda.Event(enable_timing=self.timeline)
+            u.issued = threading.Event()
+            self._seq += 1
+            self._units[(jid, layer)] = u
+            prev = u.seq - self.n_slots
+            if prev >= 0 and prev not in self._freed:
+                self._freed[prev] = (torch.cuda.Event(), threading.Event())
+            freed = self._freed.get(prev) if prev >= 0 else None
+
+            def submit(u=u, layer=layer, freed=freed, dep=dep):
+                try:
+                    with torch.cuda.stream(self.s_load):
+                        if freed is not None:   # slot reuse: its previous reader is done
+                            freed[1].wait()
+                            self.s_load.wait_event(freed[0])
+                        if dep is not None:     # rows saved by this session's previous turn
+                            dep[1].wait()
+                            self.s_load.wait_event(dep[0])
+                        u.start.record(self.s_load)
+                        ops.preload_layer(self.slots[u.slot], self.host_arena.buffer, ids,
+                                          self.block_bytes, layer * self.chunk_bytes,
+                                          self.chunk_bytes, tail, stream=self.s_load)
+                        u.end.record(self.s_load)
+                finally:
+                    u.issued.set()
+
+            self._io_load.submit(submit)
 
     def _acquire(self, jid, layer) -> _Unit:
-        key = (jid, layer)
-        while key not in self._issued:
-            if not self._pending:
-                raise RuntimeError("pre-load unit was never enqueued")
-            before = self._seq_issued
-            self._pump()
-            if self._seq_issued == before:
-                raise RuntimeError("read-buffer ring deadlock (units acquired out of order)")
-        return self._issued.pop(key)
+        u = self._units.pop((jid, layer), None)
+        if u is None:
+            raise RuntimeError("pre-load unit was never enqueued")
+        if not u.issued.wait(timeout=600):
+            raise RuntimeError("pre-load IO thread stalled")
+        if self._io_load.error is not None:
+            raise RuntimeError("pre-load IO thread failed") from self._io_load.error
+        return u
 
     def _release(self, u: _Unit):
-        ev = torch.cuda.Event()
-        ev.record(self.s_compute)
-        self._freed[u.slot] = ev
-        self._seq_released += 1
-        self._pump()
+        """The slot's reader (K2) is enqueued: record it and wake the IO thread."""
+        ent = self._freed.get(u.seq)
+        if ent is None:
+            ent = self._freed[u.seq] = (torch.cuda.Event(), threading.Event())
+        ent[0].record(self.s_compute)
+        ent[1].set()
+        self._freed.pop(u.seq - 2 * self.n_slots, None)
+
+    def _submit_save(self, produced, arena, job, layer, kept, n, wslot, sv0, sv1, flag):
+        def submit():
+            try:
+                with torch.cuda.stream(self.s_save):
+                    self.s_save.wait_event(produced)
+                    if sv0 is not None:
+                        sv0.record(self.s_save)
+                    ops.save_layer(arena, job.block_ids, self.block_bytes,
+                                   layer * self.chunk_bytes, self.block_tokens, self.row_bytes,
+                                   job.head + kept, n, self.wbuf[wslot], stream=self.s_save)
+                    sv1.record(self.s_save)
+            finally:
+                flag.set()
+
+        self._io_save.submit(submit)
+
+    def close(self) -> None:
+        for t in (self._io_load, self._io_save):
+            t.q.put(None)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     # ------------------------------------------------------------------ main entry
     def run(self, jobs: list[Job], *, want_logits: bool = False) -> list[JobResult]:
@@ -296,11 +372,21 @@ class Runner:
                              "depends on this turn's save)")
         for i, job in enumerate(jobs):
             self._enqueue_loads((base, i), job)
-        self._pump()
         results = []
         for i, job in enumerate(jobs):
             results.append(self._run_job((base, i), job, want_logits))
+        self.drain_io()
         return results
+
+    def drain_io(self) -> None:
+        """Wait until the IO threads have submitted everything queued so far, so
+        a later device synchronise covers this run's loads and saves."""
+        for t in (self._io_load, self._io_save):
+            done = threading.Event()
+            t.submit(done.set)
+            done.wait()
+            if t.error is not None:
+                raise RuntimeError(f"{t.name} failed") from t.error
 
     def _run_job(self, jid, job: Job, want_logits: bool) -> JobResult:
         s = self.shape
@@ -327,17 +413,22 @@ class Runner:
         logits_out = None
         with torch.cuda.stream(cs):
             if job.prestage and job.source == "host" and kept:
-                key = (jid, s.layers - 1)
-                while key not in self._issued:
-                    before = self._seq_issued
-                    self._pump()
-                    if self._seq_issued == before:
-                        raise RuntimeError("read buffer too small to prestage a whole job")
-                cs.wait_event(self._issued[key].end)
+                if s.layers > self.n_slots:
+                    raise RuntimeError("read buffer too small to prestage a whole job")
+                last = self._units[(jid, s.layers - 1)]
+                if not last.issued.wait(timeout=600):
+                    raise RuntimeError("pre-load IO thread stalled")
+                cs.wait_event(last.end)
             t0 = ev() if ev else None
             if t0:
                 t0.record(cs)
-            ids = job.token_ids.to(self.device, non_blocking=True)
+            if job.token_ids.is_cuda:
+                ids = job.token_ids
+            else:  # pinned host ids: SM copy, not behind the pre-load DMAs
+                src = job.token_ids if job.token_ids.is_pinned() else job.token_ids.pin_memory()
+                ids = ops.copy_sm(torch.empty(n, dtype=torch.int64, device=self.device),
+                                  src.to(torch.int64), stream=cs)
+                self.launches += 1
             x = F.embedding(ids, self.w.embed)
             q_rot = self._buf("q", n, hq * hd)
             kvbuf = self._buf("kv", kept + n, self.row_elems)
@@ -355,27 +446,22 @@ class Runner:
                 if job.save:
                     wslot = self._wseq % self.n_wslots
                     self._wseq += 1
-                    if self._wdone[wslot] is not None:
-                        cs.wait_event(self._wdone[wslot])
+                    if self._wdone[wslot] is not None:   # slot's previous D2H finished
+                        self._wdone[wslot][1].wait()
+                        cs.wait_event(self._wdone[wslot][0])
                 ops.rope_new(qkv, n, hq, hkv, hd, self.table, kept, q_rot, kvbuf[kept:],
                              self.wbuf[wslot] if wslot is not None else None, stream=cs)
                 self.launches += 1
                 if job.save:
                     produced = torch.cuda.Event()
                     produced.record(cs)
-                    with torch.cuda.stream(self.s_save):
-                        self.s_save.wait_event(produced)
-                        sv0 = ev() if ev else None
-                        if sv0:
-                            sv0.record(self.s_save)
-                        ops.save_layer(arena, job.block_ids, self.block_bytes,
-                                       layer * self.chunk_bytes, self.block_tokens,
-                                       self.row_bytes, job.head + kept, n, self.wbuf[wslot],
-                                       stream=self.s_save)
-                        sv1 = torch.cuda.Event(enable_timing=self.timeline)
-                        sv1.record(self.s_save)
-                    self._wdone[wslot] = sv1
-                    rec["saves"].append((sv0, sv1))
+                    sv0 = ev() if ev else None
+                    sv1 = torch.cuda.Event(enable_timing=self.timeline)
+                    flag = threading.Event()
+                    self._submit_save(produced, arena, job, layer, kept, n, wslot, sv0, sv1,
+                                      flag)
+                    self._wdone[wslot] = (sv1, flag)
+                    rec["saves"].append((sv0, sv1, flag))
                 if kept:
                     if job.source == "host":
                         u = self._acquire(jid, layer)
@@ -433,14 +519,16 @@ class Runner:
                 rec["layers"].append((l0, l1))
             hl = ops.rmsnorm(x[-1:], self.w.w_final, 1e-5, stream=cs)
             logits = F.linear(hl, self.w.lm_head).float()
-            first.copy_(logits.argmax(dim=-1), non_blocking=True)
+            ops.copy_sm(first, logits.argmax(dim=-1), stream=cs)
+            self.launches += 1
             if want_logits:
                 logits_out = logits[0].clone()
             t1 = ev() if ev else None
             if t1:
                 t1.record(cs)
         if job.save:
-            self._last_save[job.session_id] = rec["saves"][-1][1]
+            _, sv1, flag = rec["saves"][-1]
+            self._last_save[job.session_id] = (sv1, flag)
         res = JobResult(job.session_id, kept, n, None, first, logits_out,
                         bytes_loaded=kept * s.kv_bytes_per_token if job.source == "host" else 0,
                         bytes_saved=n * s.kv_bytes_per_token if job.save else 0)
@@ -462,7 +550,9 @@ class Runner:
         self.probe.append((kind, e0, e1, work))
 
     def join(self) -> None:
-        """Make the compute stream wait for all issued loads and saves."""
+        """Make the compute stream wait for all loads and saves queued so far
+        (waits for the IO threads to submit them first)."""
+        self.drain_io()
         self.s_compute.wait_stream(self.s_load)
         self.s_compute.wait_stream(self.s_save)
 
@@ -481,7 +571,9 @@ class Runner:
             waits = [(f(a), f(b)) for a, b in rec["waits"]]
             stall = sum(b - a for a, b in waits)
             tl.load_intervals = [(f(a), f(b)) for a, b in rec["loads"]]
-            tl.save_intervals = [(f(a), f(b)) for a, b in rec["saves"]]
+            for *_, flag in rec["saves"]:
+                flag.wait()
+            tl.save_intervals = [(f(a), f(b)) for a, b, _ in rec["saves"]]
             comp = []
             wi = iter(waits)
             for li, (a, b) in enumerate(rec["layers"]):

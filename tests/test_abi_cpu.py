@@ -46,9 +46,12 @@ def test_ctypes_table_matches_header(built):
 def test_split_policy_without_gpu(built):
     from paper_2403_19708_b200 import _lib
     lib = _lib.lib()
-    # 13B p50 turn (kept 2142, new 237, 40 heads): short grid -> split-KV
-    s = lib.askv_attn_num_splits(2142, 237, 40, 148)
-    assert 2 <= s <= 8
+    # one query tile x 40 heads = 40 CTAs: split the 18 KV tiles 3 ways (one wave)
+    assert lib.askv_attn_num_splits(2142, 100, 40, 148) == 3
+    # 13B p50 turn (2 query tiles x 40 heads = 80 CTAs) already fills a wave
+    assert lib.askv_attn_num_splits(2142, 237, 40, 148) == 1
+    # 70B TP8 rank (8 q-heads): split up to >= 4 KV tiles per split
+    assert lib.askv_attn_num_splits(2048, 256, 8, 148) == 5
     # full recompute of 2379 tokens fills the machine without splitting
     assert lib.askv_attn_num_splits(0, 2379, 40, 148) == 1
     assert lib.askv_attn_workspace_bytes(2142, 237, 40, 128, 4) == 4 * 237 * 40 * 129 * 4

@@ -7,7 +7,7 @@
 #include "../paper_2403_19708_b200/csrc/askv_ptx.cuh"
 using namespace askv;
 
-template <int MODE>  // 0 full, 1 ex2->fmul, 2 no pass1, 3 ex2 poly
+template <int MODE>  // 0 full, 1 ex2->fmul, 2 no pass1, 3 ex2 poly, 4 packed (kernel's current)
 __global__ void probe(long long* out, float* sink, int iters) {
   __shared__ uint32_t slot;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -22,6 +22,41 @@ __global__ void probe(long long* out, float* sink, int iters) {
   long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
     float mx = -INFINITY;
+    if (MODE == 4) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float sv[32];
+        tmem_ld32(tmem + c * 32, sv);
+        float m0 = fmax3(sv[0], sv[1], sv[2]), m1 = fmax3(sv[3], sv[4], sv[5]);
+#pragma unroll
+        for (int e = 6; e < 30; e += 4) {
+          m0 = fmax3(m0, sv[e], sv[e + 1]);
+          m1 = fmax3(m1, sv[e + 2], sv[e + 3]);
+        }
+        mx = fmax3(mx, fmax3(m0, m1, sv[30]), sv[31]);
+      }
+      const float neg_m = -(mx > m_acc ? mx : m_acc);
+      const float2 sl2v = make_float2(1.44f, 1.44f), negm2 = make_float2(neg_m, neg_m);
+      float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float sv[32];
+        tmem_ld32(tmem + c * 32, sv);
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const float2 x = ffma2(make_float2(sv[e], sv[e + 1]), sl2v, negm2);
+          float2 pp = make_float2(ex2(x.x), ex2(x.y));
+          if ((e >> 1) & 1) ls1 = fadd2(ls1, pp); else ls0 = fadd2(ls0, pp);
+          pk[e >> 1] = pack_bf16x2(pp.x, pp.y);
+        }
+        tmem_st16(tmem + 128 + c * 16, pk);
+      }
+      tmem_wait_st();
+      acc += ls0.x + ls0.y + ls1.x + ls1.y;
+      continue;
+    }
+    mx = -INFINITY;
     if (MODE != 2) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -65,10 +100,11 @@ __global__ void probe(long long* out, float* sink, int iters) {
 int main() {
   long long* d; float* sink;
   cudaMalloc(&d, 1024 * 8); cudaMalloc(&sink, 1 << 22);
-  const char* names[4] = {"full", "ex2->fmul", "no pass1", "ex2 poly"};
-  for (int mode = 0; mode < 4; ++mode)
+  const char* names[5] = {"full", "ex2->fmul", "no pass1", "ex2 poly", "packed"};
+  for (int mode = 0; mode < 5; ++mode)
     for (int wgs : {1, 2}) {
-      auto k = mode == 0 ? probe<0> : mode == 1 ? probe<1> : mode == 2 ? probe<2> : probe<3>;
+      auto k = mode == 0 ? probe<0> : mode == 1 ? probe<1> : mode == 2 ? probe<2>
+               : mode == 3 ? probe<3> : probe<4>;
       const int iters = 200;
       // wgs warpgroups per SM: run 2 CTAs of 128 threads per SM when wgs == 2
       k<<<148 * wgs, 128>>>(d, sink, iters);

@@ -20,6 +20,8 @@ def main():
     ap.add_argument("--mode", default="hbm")
     ap.add_argument("--turns", type=int, default=4)
     ap.add_argument("--config", default="c3")
+    ap.add_argument("--bg-h2d", action="store_true",
+                    help="stream a background pinned H2D copy during the profiled step")
     a = ap.parse_args()
     import bench
     from paper_2403_19708_b200 import model
@@ -35,7 +37,7 @@ def main():
     hbm = torch.zeros(sum(nbs) * bb // 2, dtype=torch.bfloat16, device="cuda")
     runner = Runner(shape, host_arena=arena, hbm_arena=hbm, read_buffer_bytes=4 << 30,
                     write_buffer_bytes=1 << 30, max_new=max(n for *_, n in turns),
-                    max_ctx=4096, timeline=False)
+                    max_ctx=4096, timeline=True)
     jobs, pos = [], 0
     rng = np.random.default_rng(0)
     for (sid, k, kept, new), nb in zip(turns, nbs):
@@ -46,9 +48,9 @@ def main():
             off = torch.as_tensor([b * bb // 2 for b in ids], dtype=torch.int64, device="cuda")
             jobs.append(Job(f"{sid}#{k}", toks.cuda(), kept=kept, source="hbm", block_ids=ids,
                             save=True, dev_block_off=off))
-        elif a.mode == "host":
+        elif a.mode in ("host", "prestage"):
             jobs.append(Job(f"{sid}#{k}", toks.pin_memory(), kept=kept, source="host",
-                            block_ids=ids, save=True))
+                            block_ids=ids, save=True, prestage=a.mode == "prestage"))
         else:
             jobs.append(Job(f"{sid}#{k}",
                             torch.as_tensor(rng.integers(0, shape.vocab, kept + new)).cuda()))
@@ -57,14 +59,50 @@ def main():
         runner.join()
     torch.cuda.synchronize()
     from torch.profiler import ProfilerActivity, profile
+    bg = None
+    if a.bg_h2d:   # isolate copy-engine interference: 1 GB H2D chunks on their own stream
+        import threading
+        src = torch.empty(1 << 30, dtype=torch.uint8).pin_memory()
+        dst = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+        stop = threading.Event()
+        bs = torch.cuda.Stream()
+
+        def loop():
+            while not stop.is_set():
+                with torch.cuda.stream(bs):
+                    dst.copy_(src, non_blocking=True)
+                bs.synchronize()
+        bg = threading.Thread(target=loop, daemon=True)
+        bg.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    import time
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         e0.record(runner.s_compute)
+        h0 = time.perf_counter()
         runner.run(jobs)
         runner.join()
+        host_issue_ms = (time.perf_counter() - h0) * 1e3
         e1.record(runner.s_compute)
         torch.cuda.synchronize()
+    # host issue rate without the profiler attached
+    torch.cuda.synchronize()
+    h0 = time.perf_counter()
+    runner.run(jobs)
+    runner.join()
+    host_issue_ms_noprof = (time.perf_counter() - h0) * 1e3
+    torch.cuda.synchronize()
+    gpu_ms_noprof = (time.perf_counter() - h0) * 1e3
     wall_us = e0.elapsed_time(e1) * 1e3
+    res = runner.run(jobs)
+    runner.join()
+    torch.cuda.synchronize()
+    Runner.finalize(res)
+    if bg is not None:
+        stop.set()
+        bg.join()
+    tls = [{"makespan_ms": r.timeline.makespan * 1e3, "stall_ms": r.timeline.stall_total * 1e3,
+            "layer_ms": [round((b - a) * 1e3, 3) for a, b in r.timeline.compute_intervals[:6]]}
+           for r in res]
     agg = collections.defaultdict(lambda: [0, 0.0])
     busy = []
     for ev in prof.events():
@@ -94,7 +132,9 @@ def main():
         merged += ce - cs
     cpu_total = sum(ev.cpu_time_total for ev in prof.events()
                     if ev.device_type == torch.autograd.DeviceType.CPU and ev.name == "aten::linear")
-    out = {"mode": a.mode, "turns": len(jobs), "wall_us": wall_us,
+    out = {"mode": a.mode, "turns": len(jobs), "wall_us": wall_us, "timelines": tls,
+           "host_issue_ms": host_issue_ms, "host_issue_ms_noprof": host_issue_ms_noprof,
+           "wall_ms_noprof": gpu_ms_noprof,
            "kernel_busy_us": merged, "gpu_idle_frac": 1 - merged / wall_us,
            "kernels": {k: {"n": v[0], "us": round(v[1], 1), "avg_us": round(v[1] / v[0], 2)}
                        for k, v in sorted(agg.items(), key=lambda x: -x[1][1])}}
