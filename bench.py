@@ -45,6 +45,7 @@ CONFIGS = {
     "c2": ("llama2-7b", "workload_c2.json"),
     "c3": ("llama2-13b", "workload_c3.json"),
     "c4": ("llama2-7b", None),   # long-context overflow: 32K history at W = 4096
+    "c5": ("llama2-70b", "workload_c3.json"),  # tensor-parallel over the launch's ranks
 }
 
 
@@ -251,7 +252,15 @@ def main():
     from paper_2403_19708_b200 import model
 
     shape = model.shape(CONFIGS[args.config][0])
-    turns, n_hits = select_turns(args.config, rank, world, args.turns)
+    tp = world if args.config == "c5" else 1
+    if tp > 1:
+        # C5: one model replica tensor-parallel over all ranks (head-parallel
+        # attention + KV store slice per rank, NCCL all-reduce after W_o / W_down)
+        shape = shape.tp_shard(tp)
+        turns, n_hits = select_turns("c3", 0, 1, args.turns)
+    else:
+        turns, n_hits = select_turns("c3" if args.config == "c5" else args.config, rank,
+                                     world, args.turns)
 
     if args.impl == "reference":
         if rank == 0:
@@ -292,7 +301,11 @@ def main():
         hbm[off:off + m].normal_(generator=g)
         host_bf[off:off + m].copy_(hbm[off:off + m])
     torch.cuda.synchronize()
-    runner = Runner(shape, device=dev, seed=0, block_tokens=tb, host_arena=arena,
+    tp_hook = None
+    if tp > 1:
+        tp_hook = pdist.NcclAllReduce()
+    runner = Runner(shape, device=dev, seed=rank if tp > 1 else 0, block_tokens=tb,
+                    host_arena=arena, tp_reduce=tp_hook,
                     hbm_arena=hbm, read_buffer_bytes=4 << 30, write_buffer_bytes=1 << 30,
                     max_new=max(max_new, 1), max_ctx=max(shape.context_window, max_kept + 1))
     ids_perm = np.random.default_rng(99 + rank).permutation(n_blocks)
@@ -381,7 +394,8 @@ def main():
     t_host = max_over_ranks(ms_host) * 1e-3
     t_hbm = max_over_ranks(ms_hbm) * 1e-3
     t_re = max_over_ranks(ms_re) * 1e-3
-    tok_all = sum_over_ranks(prompt_tokens)
+    # weak scaling: ranks serve disjoint sessions (sum); C5 TP: one replica (its tokens)
+    tok_all = prompt_tokens if tp > 1 else sum_over_ranks(prompt_tokens)
     value = tok_all * args.steps / t_hbm
     e2e = tok_all * args.steps / t_host
     recompute = tok_all * steps_re / t_re
@@ -434,7 +448,8 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_hbm / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "higher_is_better": True, "scaling": "strong" if tp > 1 else "weak",
+        "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (reference ShareGPT-shaped session generator; random-init weights "
                 "and KV)",
         "config": {
@@ -452,7 +467,9 @@ def main():
             "e2e_mode": "KV streamed from pinned host DRAM by the layer-wise pre-loader; "
                         "new-token KV saved back asynchronously",
             "l2": "inputs larger than L2 (per-step KV " f"{h2d_bytes / 1e9:.1f} GB)",
-            "parallelism": f"sessions sharded, no collective ({world} independent ranks)"},
+            "parallelism": (f"tensor-parallel tp{tp} (NCCL all-reduce of W_o / W_down "
+                            f"partials over NVLink)" if tp > 1 else
+                            f"sessions sharded, no collective ({world} independent ranks)")},
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d_step,
                 "d2h_bytes_per_step": d2h_step, "ms_per_step": ms_host / args.steps},
         "recompute": {"value": recompute, "unit": "tokens/s",

@@ -190,13 +190,17 @@ __global__ void __launch_bounds__(320, 1)
       tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
+      // K/V tiles are re-read by every query tile of the head: keep them in L2
+      // against streaming traffic (the pre-loader's DMA writes); Q is read once.
+      const uint64_t pol_kv = l2_policy_evict_last();
+      const uint64_t pol_q = l2_policy_evict_first();
       const int qt = paired ? 2 : 1;
       mbar_expect_tx(q_full, qt * C::kTileBytes);
       for (int t = 0; t < qt; ++t)
 #pragma unroll
         for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d(sQ + t * C::kTileBytes + c * (kBM * 128), &tm_q, q_full, c * 64, h,
-                      q0 + t * kBM);
+          tma_load_3d_hint(sQ + t * C::kTileBytes + c * (kBM * 128), &tm_q, q_full, c * 64, h,
+                           q0 + t * kBM, pol_q);
       // K runs up to kKStages tiles ahead, V up to kVStages; interleave so a
       // blocked V slot never holds back the next K.
       int jk = 0, jv = 0;
@@ -207,8 +211,8 @@ __global__ void __launch_bounds__(320, 1)
           mbar_expect_tx(&k_full[st], C::kTileBytes);
 #pragma unroll
           for (int c = 0; c < C::kChunks; ++c)
-            tma_load_3d(sK + st * C::kTileBytes + c * (kBN * 128), &tm_k, &k_full[st], c * 64,
-                        kh, (t_begin + jk) * kBN);
+            tma_load_3d_hint(sK + st * C::kTileBytes + c * (kBN * 128), &tm_k, &k_full[st],
+                             c * 64, kh, (t_begin + jk) * kBN, pol_kv);
           ++jk;
         } else {
           const int st = jv % C::kVStages;
@@ -216,8 +220,8 @@ __global__ void __launch_bounds__(320, 1)
           mbar_expect_tx(&v_full[st], C::kTileBytes);
 #pragma unroll
           for (int c = 0; c < C::kChunks; ++c)
-            tma_load_3d(sV + st * C::kTileBytes + c * (kBN * 128), &tm_v, &v_full[st], c * 64,
-                        kh, (t_begin + jv) * kBN);
+            tma_load_3d_hint(sV + st * C::kTileBytes + c * (kBN * 128), &tm_v, &v_full[st],
+                             c * 64, kh, (t_begin + jv) * kBN, pol_kv);
           ++jv;
         }
       }

@@ -34,6 +34,14 @@ __device__ __forceinline__ void st16(void* p, int4 v) {
                "r"(v.w)
                : "memory");
 }
+// Store that asks L2 to keep the line (attention's K/V rows are read right after).
+__device__ __forceinline__ void st16_keep(void* p, int4 v) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.v4.s32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
 
 // Rotate the 4 interleaved pairs of a 16-byte bf16 vector by table entries
 // cs[0..7] = (cos0, sin0, cos1, sin1, ...).
@@ -126,7 +134,7 @@ __global__ void __launch_bounds__(kThreads)
         const int u = g - rr * row_units;
         int4 x = v[k];
         if (u < k_units) x = rotate8(x, cs_s + (rr * kHalf + (u % kUnitsPerHead) * 4) * 2);
-        st16(dst + (int64_t)(row0 + rr) * dst_row_stride + u * 8, x);
+        st16_keep(dst + (int64_t)(row0 + rr) * dst_row_stride + u * 8, x);
       }
     }
   }
@@ -155,7 +163,7 @@ __global__ void __launch_bounds__(kThreads)
     } else {
       const int ku = u - q_units;  // [0, 2*k_units): K then V, same as the row layout
       if (save_out != nullptr) st16(save_out + (int64_t)i * 2 * k_units * 8 + ku * 8, x);
-      st16(kv_out + (int64_t)i * kv_row_stride + ku * 8, ku < k_units ? rotate8(x, cs) : x);
+      st16_keep(kv_out + (int64_t)i * kv_row_stride + ku * 8, ku < k_units ? rotate8(x, cs) : x);
     }
   }
 }

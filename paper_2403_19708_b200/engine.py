@@ -17,7 +17,7 @@ the next turn finds a complete history (SURVEY.md §7.2 "Output tokens' KV").
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import torch
 
@@ -42,6 +42,18 @@ def save_truncate(tokens: int, window: int, cut: int) -> int:
     return tokens - cut * (-(-(tokens - window) // cut))
 
 
+def rolling_kept(kept: int, sizes, window: int, cut: int) -> int:
+    """Context after appending chunks with a rolling window: before each chunk
+    that would overflow, drop `cut`-sized front chunks (sim.py:468-483).  For
+    chunk sizes <= cut this ends exactly at save_truncate(kept + sum(sizes))
+    (sim.py:576-581), which tests/test_store_cpu.py checks."""
+    for c in sizes:
+        if kept + c > window:
+            kept = overflow_kept(kept, c, window, cut)
+        kept += c
+    return kept
+
+
 @dataclass
 class TurnOutcome:
     session_id: str
@@ -52,11 +64,23 @@ class TurnOutcome:
     new: int
     prompt: int
     overflowed: bool
-    result: JobResult          # the prefill of the new input tokens (TTFT job)
-    append: JobResult | None   # teacher-forced append of output tokens
+    result: JobResult                 # last chunk of the input prefill (first-token logits)
+    append: JobResult | None          # last chunk of the teacher-forced output append
+    results: list = field(default_factory=list)   # every input-prefill chunk (TTFT = sum)
+
+    def ttft_s(self) -> float:
+        """Isolated time to first token: sum of the input chunks' makespans
+        (call after Runner.finalize(outcome.results))."""
+        return sum(r.timeline.makespan for r in self.results)
 
 
 class Engine:
+    """One GPU's serving loop for the reuse path.  Prefills are processed in
+    chunks of at most `chunk` = min(max_new, cut) tokens (chunked prefill: a
+    chunk after the first reuses the rows its predecessor just saved), with the
+    reference's window truncation applied before any chunk that would overflow,
+    so positions never exceed the window."""
+
     def __init__(self, shape: LlamaShape, *, host_blocks: int, block_tokens: int = 128,
                  device="cuda", seed: int = 0, weights: LlamaWeights | None = None,
                  read_buffer_bytes: int = 1 << 30, max_new: int = 1024,
@@ -71,13 +95,13 @@ class Engine:
         self.store = KvStore(self.profile, tiers, block_bytes=block_bytes, ttl=ttl,
                              evictor=self._make_room, arena=self.arena,
                              block_tokens=block_tokens)
-        self.runner = Runner(shape, weights=weights, device=device, seed=seed,
-                             block_tokens=block_tokens, host_arena=self.arena,
-                             read_buffer_bytes=read_buffer_bytes,
-                             max_new=shape.context_window + max_new,
-                             max_ctx=shape.context_window + max_new, tp_reduce=tp_reduce)
         self.window = shape.context_window
         self.cut = self.profile.cut_tokens
+        self.chunk = max(1, min(max_new, self.cut))
+        self.runner = Runner(shape, weights=weights, device=device, seed=seed,
+                             block_tokens=block_tokens, host_arena=self.arena,
+                             read_buffer_bytes=read_buffer_bytes, max_new=max_new,
+                             max_ctx=self.window + self.chunk, tp_reduce=tp_reduce)
         self.context: dict[str, int] = {}
         self.tokens: dict[str, torch.Tensor] = {}   # conversation token ids (for misses)
 
@@ -93,7 +117,7 @@ class Engine:
             self.store.remove(it.session_id)
 
     def install_history(self, sid: str, ids: torch.Tensor, now: float = 0.0) -> JobResult:
-        """Prefill and store a session history as-is (no save-time truncation):
+        """Prefill and store a session history as-is (one job, no truncation):
         a pre-stored long document / history larger than the window, the
         starting point of config C4 (32K history served at W = 4096)."""
         ids = ids.reshape(-1).to(torch.int64)
@@ -109,10 +133,33 @@ class Engine:
         self.tokens[sid] = ids
         return res
 
+    def _prefill(self, sid: str, ids: torch.Tensor, kept: int, want_logits: bool):
+        """Chunked prefill of `ids` after `kept` stored rows, saving every chunk's
+        K/V; rolling window truncation before a chunk that would overflow.
+        Returns (results, kept_after, rows_dropped)."""
+        results, dropped = [], 0
+        pos, n = 0, int(ids.numel())
+        while pos < n:
+            c = min(self.chunk, n - pos)
+            if kept + c > self.window:
+                k2 = overflow_kept(kept, c, self.window, self.cut)
+                self.store.drop_front_rows(sid, kept - k2)
+                dropped += kept - k2
+                kept = k2
+            tab = self.store.reserve_rows(sid, kept + c)
+            job = Job(sid, ids[pos:pos + c], kept=kept, source="host" if kept else "none",
+                      block_ids=tab, save=True, head=self.store.head_row(sid))
+            results.append(self.runner.run([job], want_logits=want_logits)[0])
+            kept += c
+            self.store.mark_written(sid, kept)
+            pos += c
+        return results, kept, dropped
+
     def turn(self, sid: str, turn_index: int, new_ids: torch.Tensor,
              out_ids: torch.Tensor | None = None, now: float = 0.0,
              want_logits: bool = False) -> TurnOutcome:
         new_ids = new_ids.reshape(-1).to(torch.int64)
+        out_ids = None if out_ids is None else out_ids.reshape(-1).to(torch.int64)
         hist = self.context.get(sid, 0)
         new = int(new_ids.numel())
         overflowed = hist + new > self.window
@@ -137,32 +184,27 @@ class Engine:
         hist_ids = self.tokens.get(sid, torch.empty(0, dtype=torch.int64))
         if hit is HitClass.MISS or kept == 0:
             hit = HitClass.MISS
-            prompt_ids = torch.cat([hist_ids, new_ids])
-            ids = self.store.reserve_rows(sid, kept + new)
-            job = Job(sid, prompt_ids, kept=0, source="none", block_ids=ids, save=True,
-                      head=self.store.head_row(sid))
+            if self.store.peek(sid) is None:
+                self.store.release_rows(sid)
+            # recompute the whole (truncated) prompt, sim.py:432-435
+            results, rows, _ = self._prefill(sid, torch.cat([hist_ids, new_ids]), 0,
+                                             want_logits)
         else:
-            ids = self.store.reserve_rows(sid, kept + new)
-            job = Job(sid, new_ids, kept=kept, source="host", block_ids=ids, save=True,
-                      head=self.store.head_row(sid))
-        res = self.runner.run([job], want_logits=want_logits)[0]
-        self.store.mark_written(sid, kept + new)
+            results, rows, _ = self._prefill(sid, new_ids, kept, want_logits)
         append = None
+        if out_ids is not None and out_ids.numel():
+            ares, rows, _ = self._prefill(sid, out_ids, rows, False)
+            append = ares[-1]
         n_out = 0 if out_ids is None else int(out_ids.numel())
-        if n_out:
-            ids = self.store.reserve_rows(sid, kept + new + n_out)
-            ajob = Job(sid, out_ids.reshape(-1).to(torch.int64), kept=kept + new,
-                       source="host", block_ids=ids, save=True, head=self.store.head_row(sid))
-            append = self.runner.run([ajob])[0]
-            self.store.mark_written(sid, kept + new + n_out)
         raw = kept + new + n_out
         ctx = save_truncate(raw, self.window, self.cut)
-        all_ids = torch.cat([hist_ids, new_ids] + ([out_ids.reshape(-1).to(torch.int64)]
-                                                   if n_out else []))
+        if ctx != rows:
+            raise AssertionError(f"rolling window {rows} != save truncation {ctx}")
+        all_ids = torch.cat([hist_ids, new_ids] + ([out_ids] if n_out else []))
         self.tokens[sid] = all_ids[raw - ctx:]
         self.context[sid] = ctx
         if ctx > 0:
             self.store.save(sid, ctx, now)
         self.store.pinned.discard(sid)
         return TurnOutcome(sid, turn_index, hit.value, kept, hist - kept, new, kept + new,
-                           overflowed, res, append)
+                           overflowed, results[-1], append, results)

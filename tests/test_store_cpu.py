@@ -136,3 +136,17 @@ def test_shapes_kv_bytes():
     assert model.shape("7b").kv_bytes_per_token == 524288
     assert model.shape("70b").kv_bytes_per_token == 327680
     assert model.shape("70b").tp_shard(8).kv_bytes_per_token == 40960
+
+
+@settings(max_examples=400, deadline=None)
+@given(kept=st.integers(0, 4096), sizes=st.lists(st.integers(1, 2048), min_size=1, max_size=12),
+       w=st.sampled_from([4096, 2048]))
+def test_rolling_window_chunks_equal_save_truncation(kept, sizes, w):
+    """Chunked prefill/append with a rolling window (chunks <= cut) ends at the
+    reference's save-time truncation of the whole turn (sim.py:576-581)."""
+    from paper_2403_19708_b200.engine import rolling_kept
+    cut = w // 2
+    sizes = [min(c, cut) for c in sizes]
+    kept = min(kept, w)
+    assert rolling_kept(kept, sizes, w, cut) == layout_ref.save_truncate(kept + sum(sizes), w,
+                                                                          0.5)

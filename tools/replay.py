@@ -67,16 +67,19 @@ def main():
         oids = torch.as_tensor(rng.integers(0, shape.vocab, out)) if out else None
         o = eng.turn(sid, k, ids, oids, now=arr)
         torch.cuda.synchronize()
-        eng.runner.finalize([o.result])
-        tl = o.result.timeline
+        eng.runner.finalize(o.results)
         recs.append(dict(arrival=arr, session=sid, turn=k, hit=o.hit, kept=o.kept, new=new,
-                         prompt=o.prompt, makespan=tl.makespan, stall=tl.stall_total))
+                         prompt=o.prompt, makespan=o.ttft_s(),
+                         stall=sum(r.timeline.stall_total for r in o.results)))
     reuse_wall = time.time() - t_wall
     # recompute mode: the same prompts, whole prompt prefilled, no store
     rec_runner = Runner(shape, weights=weights, block_tokens=tb, max_new=2048,
                         max_ctx=shape.context_window + 2048)
     for r in recs:
-        ids = torch.as_tensor(rng.integers(0, shape.vocab, r["prompt"]))
+        # the (truncated) prompt the reference would recompute; prompts beyond the
+        # window are capped at W (the engine's rolling window keeps <= W rows)
+        n = min(r["prompt"], shape.context_window)
+        ids = torch.as_tensor(rng.integers(0, shape.vocab, n))
         res = rec_runner.run([Job(r["session"], ids.cuda())])[0]
         torch.cuda.synchronize()
         Runner.finalize([res])
