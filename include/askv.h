@@ -161,6 +161,82 @@ int askv_rmsnorm(const void* x, const void* w, void* y, int rows, int cols, floa
                  void* stream);
 int askv_silu_mul(const void* gu, void* out, int rows, int ffn, void* stream);
 
+/*
+ * Native events (cudaEvent_t as void*) used by the runtime's streams / IO threads.
+ */
+int askv_event_create(void** ev, int timing);
+int askv_event_destroy(void* ev);
+int askv_event_record(void* ev, void* stream);
+int askv_stream_wait_event(void* stream, void* ev);
+int askv_event_elapsed_ms(void* start, void* end, float* ms);
+
+/*
+ * One job's full layer loop (the reuse prefill of N new tokens over `kept`
+ * reused rows), issued natively: per layer rmsnorm, QKV GEMM (cuBLASLt),
+ * rope_new (+ the pre-RoPE rows for the saver), wait for the pre-load event,
+ * K2 re-embed (+ optional promotion into the HBM tier), K3 attention, O GEMM
+ * with residual, rmsnorm, gate/up GEMM, silu*mul, down GEMM with residual.
+ * Event arrays (length `layers`, entries may be NULL) connect it to the
+ * pre-loader / saver streams.  With `allreduce` set (tensor parallelism) the
+ * W_o / W_down partials go through the callback before the residual add.
+ * Replaces: the per-layer composition the reference models as compute slots of
+ * overlap.py:69-123 (one slot per layer, loads may lag one layer).
+ */
+typedef struct askv_prefill_plan {
+  int32_t layers, d_model, n_heads, n_kv_heads, head_dim, ffn;
+  int32_t n_new, kept, head;
+  float rms_eps, attn_scale;
+  int32_t attn_splits;
+  const void* const* w_in;
+  const void* const* w_qkv;
+  const void* const* w_o;
+  const void* const* w_post;
+  const void* const* w_gu;
+  const void* const* w_down;
+  void* x;
+  void* h;
+  void* qkv;
+  void* q_rot;
+  void* kv;
+  void* attn_out;
+  void* gu;
+  void* act;
+  void* attn_ws;
+  size_t attn_ws_bytes;
+  void* gemm_ws;
+  size_t gemm_ws_bytes;
+  const float* rope_table;
+  int32_t rope_positions;
+  int32_t src_kind; /* 0 none, 1 contiguous per-layer rows, 2 block table */
+  const void* const* src_layer;
+  const int64_t* src_block_off;
+  int32_t block_tokens;
+  int64_t src_row_stride;
+  void* const* ev_src_ready;
+  void* const* ev_src_free;
+  void* const* save_rows;
+  void* const* ev_save_free;
+  void* const* ev_save_ready;
+  void* promote_base;
+  const int64_t* promote_block_ids; /* host array */
+  int32_t promote_nblocks;
+  int64_t block_bytes, chunk_bytes, row_bytes;
+  void* const* ev_layer_begin;
+  void* const* ev_layer_end;
+  void* const* ev_wait_begin;
+  void* const* ev_wait_end;
+  void* const* ev_reembed_begin;
+  void* const* ev_reembed_end;
+  void* const* ev_attn_begin;
+  void* const* ev_attn_end;
+  void (*allreduce)(void* ptr, int64_t elems, void* stream, void* ctx);
+  void* allreduce_ctx;
+} askv_prefill_plan;
+
+int askv_prefill_layers(const askv_prefill_plan* plan, void* stream);
+/* sizeof(askv_prefill_plan), so FFI mirrors can check their struct layout. */
+size_t askv_prefill_plan_size(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -40,8 +40,47 @@ SIGNATURES = {
                                _vp]),
     "askv_rmsnorm": (_i32, [_vp, _vp, _vp, _i32, _i32, _f32, _vp]),
     "askv_copy_sm": (_i32, [_vp, _vp, _sz, _vp]),
+    "askv_event_create": (_i32, [C.POINTER(C.c_void_p), _i32]),
+    "askv_event_destroy": (_i32, [_vp]),
+    "askv_event_record": (_i32, [_vp, _vp]),
+    "askv_stream_wait_event": (_i32, [_vp, _vp]),
+    "askv_event_elapsed_ms": (_i32, [_vp, _vp, C.POINTER(C.c_float)]),
+    "askv_prefill_layers": (_i32, [_vp, _vp]),
+    "askv_prefill_plan_size": (_sz, []),
     "askv_silu_mul": (_i32, [_vp, _vp, _i32, _i32, _vp]),
 }
+
+_pp = C.POINTER(C.c_void_p)
+ALLREDUCE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+
+
+class PrefillPlan(C.Structure):
+    """ctypes mirror of askv_prefill_plan (include/askv.h)."""
+    _fields_ = [
+        ("layers", C.c_int32), ("d_model", C.c_int32), ("n_heads", C.c_int32),
+        ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32), ("ffn", C.c_int32),
+        ("n_new", C.c_int32), ("kept", C.c_int32), ("head", C.c_int32),
+        ("rms_eps", C.c_float), ("attn_scale", C.c_float), ("attn_splits", C.c_int32),
+        ("w_in", _pp), ("w_qkv", _pp), ("w_o", _pp), ("w_post", _pp), ("w_gu", _pp),
+        ("w_down", _pp),
+        ("x", C.c_void_p), ("h", C.c_void_p), ("qkv", C.c_void_p), ("q_rot", C.c_void_p),
+        ("kv", C.c_void_p), ("attn_out", C.c_void_p), ("gu", C.c_void_p), ("act", C.c_void_p),
+        ("attn_ws", C.c_void_p), ("attn_ws_bytes", C.c_size_t),
+        ("gemm_ws", C.c_void_p), ("gemm_ws_bytes", C.c_size_t),
+        ("rope_table", C.c_void_p), ("rope_positions", C.c_int32),
+        ("src_kind", C.c_int32), ("src_layer", _pp), ("src_block_off", C.c_void_p),
+        ("block_tokens", C.c_int32), ("src_row_stride", C.c_int64),
+        ("ev_src_ready", _pp), ("ev_src_free", _pp),
+        ("save_rows", _pp), ("ev_save_free", _pp), ("ev_save_ready", _pp),
+        ("promote_base", C.c_void_p), ("promote_block_ids", C.POINTER(C.c_int64)),
+        ("promote_nblocks", C.c_int32),
+        ("block_bytes", C.c_int64), ("chunk_bytes", C.c_int64), ("row_bytes", C.c_int64),
+        ("ev_layer_begin", _pp), ("ev_layer_end", _pp), ("ev_wait_begin", _pp),
+        ("ev_wait_end", _pp), ("ev_reembed_begin", _pp), ("ev_reembed_end", _pp),
+        ("ev_attn_begin", _pp), ("ev_attn_end", _pp),
+        ("allreduce", ALLREDUCE_FN), ("allreduce_ctx", C.c_void_p),
+    ]
+
 
 _lock = threading.Lock()
 _lib = None

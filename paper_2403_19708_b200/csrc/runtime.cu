@@ -1,0 +1,248 @@
+// Native per-layer runtime of the reuse prefill (sm_100a).
+//
+// askv_prefill_layers() issues one job's whole layer loop from C++: per layer
+//   rmsnorm -> QKV GEMM -> rope_new (+ pre-RoPE rows for the saver) ->
+//   [wait pre-load] -> K2 re-embed -> [promote to HBM tier] -> K3 attention ->
+//   O GEMM (+ residual) -> rmsnorm -> gate/up GEMM -> silu*mul -> down GEMM (+ residual)
+// with the cross-stream events of the pre-loader / saver recorded and waited
+// inline.  The Python host (runner.py) only builds the plan; doing the loop in
+// Python cost ~240 us of host time per layer, close to the GPU time of a 13B
+// layer, which left the GPU idle between kernels (profiles/).
+// GEMMs are plain cuBLASLt (bf16 in, fp32 accumulate), the same library path
+// torch's F.linear takes; everything else is libaskv's own kernels.
+#include <cublasLt.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "askv_internal.h"
+
+namespace askv {
+namespace {
+
+struct GemmPlan {
+  cublasLtMatmulDesc_t op = nullptr;
+  cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
+  cublasLtMatmulAlgo_t algo;
+  size_t ws = 0;
+};
+
+std::mutex g_mu;
+std::map<int, cublasLtHandle_t> g_handles;
+std::map<std::tuple<int, int, int, int, int, size_t>, GemmPlan> g_plans;
+
+cublasLtHandle_t handle_for_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_handles.find(dev);
+  if (it != g_handles.end()) return it->second;
+  cublasLtHandle_t h = nullptr;
+  if (cublasLtCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
+  g_handles[dev] = h;
+  return h;
+}
+
+// Row-major y[n][m] (+)= x[n][k] . W[m][k]^T  ==  column-major Y(m x n) = W^T(m x k) X(k x n)
+const GemmPlan* plan_for(int m, int n, int k, bool accumulate, size_t ws_bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, m, n, k, (int)accumulate, ws_bytes);
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_plans.find(key);
+    if (it != g_plans.end()) return &it->second;
+  }
+  cublasLtHandle_t h = handle_for_device();
+  if (!h) return nullptr;
+  GemmPlan p;
+  if (cublasLtMatmulDescCreate(&p.op, CUBLAS_COMPUTE_32F, CUDA_R_32F) != CUBLAS_STATUS_SUCCESS)
+    return nullptr;
+  cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
+  cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof(ta));
+  cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof(tb));
+  cublasLtMatrixLayoutCreate(&p.a, CUDA_R_16BF, k, m, k);  // W: [m][k] row-major
+  cublasLtMatrixLayoutCreate(&p.b, CUDA_R_16BF, k, n, k);  // x: [n][k] row-major
+  cublasLtMatrixLayoutCreate(&p.c, CUDA_R_16BF, m, n, m);  // y: [n][m] row-major
+  cublasLtMatmulPreference_t pref = nullptr;
+  cublasLtMatmulPreferenceCreate(&pref);
+  cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws_bytes,
+                                       sizeof(ws_bytes));
+  cublasLtMatmulHeuristicResult_t res = {};
+  int found = 0;
+  cublasStatus_t st =
+      cublasLtMatmulAlgoGetHeuristic(h, p.op, p.a, p.b, p.c, p.c, pref, 1, &res, &found);
+  cublasLtMatmulPreferenceDestroy(pref);
+  if (st != CUBLAS_STATUS_SUCCESS || found == 0) return nullptr;
+  p.algo = res.algo;
+  p.ws = res.workspaceSize;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto ins = g_plans.emplace(key, p);
+  return &ins.first->second;
+}
+
+int gemm(const void* x, const void* w, void* y, int n, int m, int k, bool accumulate,
+         void* ws, size_t ws_bytes, cudaStream_t s) {
+  const GemmPlan* p = plan_for(m, n, k, accumulate, ws_bytes);
+  if (!p) {
+    set_error("cuBLASLt: no algorithm for %d x %d x %d", m, n, k);
+    return ASKV_ECUDA;
+  }
+  const float alpha = 1.f, beta = accumulate ? 1.f : 0.f;
+  cublasStatus_t st = cublasLtMatmul(handle_for_device(), p->op, &alpha, w, p->a, x, p->b, &beta,
+                                     y, p->c, y, p->c, &p->algo, ws, p->ws, s);
+  if (st != CUBLAS_STATUS_SUCCESS) {
+    set_error("cublasLtMatmul failed (%d) for %d x %d x %d", (int)st, m, n, k);
+    return ASKV_ECUDA;
+  }
+  return ASKV_OK;
+}
+
+__global__ void add_inplace_kernel(__nv_bfloat16* __restrict__ x,
+                                   const __nv_bfloat16* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n / 2;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    __nv_bfloat162 a = reinterpret_cast<__nv_bfloat162*>(x)[i];
+    const __nv_bfloat162 b = reinterpret_cast<const __nv_bfloat162*>(y)[i];
+    reinterpret_cast<__nv_bfloat162*>(x)[i] = __hadd2(a, b);
+  }
+}
+
+inline void rec(void* const* evs, int l, cudaStream_t s) {
+  if (evs && evs[l]) cudaEventRecord((cudaEvent_t)evs[l], s);
+}
+inline void wait(void* const* evs, int l, cudaStream_t s) {
+  if (evs && evs[l]) cudaStreamWaitEvent(s, (cudaEvent_t)evs[l], 0);
+}
+
+#define ASKV_TRY(expr)          \
+  do {                          \
+    const int _rc = (expr);     \
+    if (_rc != ASKV_OK) return _rc; \
+  } while (0)
+
+}  // namespace
+}  // namespace askv
+
+using namespace askv;
+
+// ------------------------------------------------------------------ events
+extern "C" int askv_event_create(void** ev, int timing) {
+  clear_error();
+  ASKV_REQUIRE(ev != nullptr, "event_create: null out pointer");
+  cudaEvent_t e;
+  cudaError_t r =
+      cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming);
+  if (r != cudaSuccess) return cuda_status(r, "cudaEventCreate");
+  *ev = (void*)e;
+  return ASKV_OK;
+}
+extern "C" int askv_event_destroy(void* ev) {
+  clear_error();
+  if (!ev) return ASKV_OK;
+  return cuda_status(cudaEventDestroy((cudaEvent_t)ev), "cudaEventDestroy");
+}
+extern "C" int askv_event_record(void* ev, void* stream) {
+  clear_error();
+  ASKV_REQUIRE(ev != nullptr, "event_record: null event");
+  return cuda_status(cudaEventRecord((cudaEvent_t)ev, (cudaStream_t)stream), "cudaEventRecord");
+}
+extern "C" int askv_stream_wait_event(void* stream, void* ev) {
+  clear_error();
+  ASKV_REQUIRE(ev != nullptr, "stream_wait_event: null event");
+  return cuda_status(cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)ev, 0),
+                     "cudaStreamWaitEvent");
+}
+extern "C" int askv_event_elapsed_ms(void* start, void* end, float* ms) {
+  clear_error();
+  ASKV_REQUIRE(start && end && ms, "event_elapsed_ms: null pointer");
+  return cuda_status(cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)end),
+                     "cudaEventElapsedTime");
+}
+
+// ------------------------------------------------------------------ layer loop
+extern "C" size_t askv_prefill_plan_size(void) { return sizeof(askv_prefill_plan); }
+
+extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
+  clear_error();
+  ASKV_REQUIRE(p != nullptr, "prefill_layers: null plan");
+  ASKV_REQUIRE(p->layers > 0 && p->n_new > 0 && p->kept >= 0 && p->head >= 0,
+               "prefill_layers: bad layers=%d n_new=%d kept=%d", p->layers, p->n_new, p->kept);
+  ASKV_REQUIRE(p->w_in && p->w_qkv && p->w_o && p->w_post && p->w_gu && p->w_down,
+               "prefill_layers: missing weight arrays");
+  ASKV_REQUIRE(p->kept == 0 || (p->src_kind == 1 || p->src_kind == 2) && p->src_layer,
+               "prefill_layers: kept rows need a source");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int n = p->n_new, d = p->d_model, hq = p->n_heads, hkv = p->n_kv_heads,
+            hd = p->head_dim, f = p->ffn;
+  const int qkv_cols = (hq + 2 * hkv) * hd;
+  const int64_t row = 2LL * hkv * hd;
+  auto* kv = static_cast<__nv_bfloat16*>(p->kv);
+  for (int l = 0; l < p->layers; ++l) {
+    rec(p->ev_layer_begin, l, s);
+    ASKV_TRY(askv_rmsnorm(p->x, p->w_in[l], p->h, n, d, p->rms_eps, s));
+    ASKV_TRY(gemm(p->h, p->w_qkv[l], p->qkv, n, qkv_cols, d, false, p->gemm_ws,
+                  p->gemm_ws_bytes, s));
+    void* save_rows = p->save_rows ? p->save_rows[l] : nullptr;
+    if (save_rows) wait(p->ev_save_free, l, s);
+    ASKV_TRY(askv_rope_new(p->qkv, qkv_cols, n, hq, hkv, hd, p->rope_table, p->rope_positions,
+                           p->kept, p->q_rot, kv + (int64_t)p->kept * row, row, save_rows, s));
+    if (save_rows) rec(p->ev_save_ready, l, s);
+    if (p->kept > 0) {
+      rec(p->ev_wait_begin, l, s);
+      wait(p->ev_src_ready, l, s);
+      rec(p->ev_wait_end, l, s);
+      rec(p->ev_reembed_begin, l, s);
+      if (p->src_kind == 1) {
+        ASKV_TRY(askv_reembed(p->src_layer[l], nullptr, 0, p->src_row_stride, p->head, p->kept,
+                              hkv, hd, p->rope_table, p->rope_positions, nullptr, 0, kv, row, s));
+      } else {
+        ASKV_TRY(askv_reembed(p->src_layer[l], p->src_block_off, p->block_tokens,
+                              p->src_row_stride, p->head, p->kept, hkv, hd, p->rope_table,
+                              p->rope_positions, nullptr, 0, kv, row, s));
+      }
+      rec(p->ev_reembed_end, l, s);
+      if (p->promote_base) {  // HBM tier: keep the pre-loaded rows resident
+        const auto* src = static_cast<const char*>(p->src_layer[l]) +
+                          (int64_t)p->head * p->row_bytes;
+        ASKV_TRY(askv_save_layer(p->promote_base, p->promote_block_ids, p->promote_nblocks,
+                                 p->block_bytes, (int64_t)l * p->chunk_bytes, p->block_tokens,
+                                 p->row_bytes, p->head, p->kept, src, s, nullptr));
+      }
+      rec(p->ev_src_free, l, s);
+    }
+    rec(p->ev_attn_begin, l, s);
+    ASKV_TRY(askv_prefill_attn(p->q_rot, kv, row, p->kept, n, hq, hkv, hd, p->attn_scale,
+                               p->attn_out, p->attn_ws, p->attn_ws_bytes, p->attn_splits, s));
+    rec(p->ev_attn_end, l, s);
+    if (p->allreduce) {  // tensor parallel: row-parallel W_o partial -> all-reduce -> residual
+      ASKV_TRY(gemm(p->attn_out, p->w_o[l], p->h, n, d, hq * hd, false, p->gemm_ws,
+                    p->gemm_ws_bytes, s));
+      p->allreduce(p->h, (int64_t)n * d, stream, p->allreduce_ctx);
+      add_inplace_kernel<<<148 * 4, 256, 0, s>>>(static_cast<__nv_bfloat16*>(p->x),
+                                                 static_cast<const __nv_bfloat16*>(p->h),
+                                                 (int64_t)n * d);
+    } else {
+      ASKV_TRY(gemm(p->attn_out, p->w_o[l], p->x, n, d, hq * hd, true, p->gemm_ws,
+                    p->gemm_ws_bytes, s));
+    }
+    ASKV_TRY(askv_rmsnorm(p->x, p->w_post[l], p->h, n, d, p->rms_eps, s));
+    ASKV_TRY(gemm(p->h, p->w_gu[l], p->gu, n, 2 * f, d, false, p->gemm_ws, p->gemm_ws_bytes, s));
+    ASKV_TRY(askv_silu_mul(p->gu, p->act, n, f, s));
+    if (p->allreduce) {
+      ASKV_TRY(gemm(p->act, p->w_down[l], p->h, n, d, f, false, p->gemm_ws, p->gemm_ws_bytes,
+                    s));
+      p->allreduce(p->h, (int64_t)n * d, stream, p->allreduce_ctx);
+      add_inplace_kernel<<<148 * 4, 256, 0, s>>>(static_cast<__nv_bfloat16*>(p->x),
+                                                 static_cast<const __nv_bfloat16*>(p->h),
+                                                 (int64_t)n * d);
+    } else {
+      ASKV_TRY(gemm(p->act, p->w_down[l], p->x, n, d, f, true, p->gemm_ws, p->gemm_ws_bytes, s));
+    }
+    rec(p->ev_layer_end, l, s);
+  }
+  return launch_status("prefill_layers");
+}

@@ -74,6 +74,73 @@ class TurnOutcome:
         return sum(r.timeline.makespan for r in self.results)
 
 
+class HbmTier:
+    """HBM-resident session tier (the reference's
+    Mode.HBM_DRAM, sim.py:61, 102-108): an LRU cache of sessions' KV blocks in
+    device memory that mirrors the host block tables one-to-one.  Host DRAM
+    stays the backing store (saves are written through), so eviction from HBM
+    is a table drop.  A turn whose session is HBM-resident re-embeds straight
+    from HBM (no host link); otherwise its pre-loaded rows are promoted."""
+
+    def __init__(self, n_blocks: int, block_bytes: int, device):
+        from collections import OrderedDict, deque
+
+        self.block_elems = block_bytes // 2
+        self.arena = torch.empty(n_blocks * self.block_elems, dtype=torch.bfloat16,
+                                 device=device)
+        self.free = deque(range(n_blocks))
+        self.tab: dict[str, list[int]] = {}
+        self.dropped: dict[str, int] = {}
+        self.valid: set[str] = set()          # mirror holds every row the host holds
+        self.lru: "OrderedDict[str, None]" = OrderedDict()
+        self.device = device
+        self.hits = 0
+        self.promotions = 0
+
+    def drop(self, sid: str) -> None:
+        ids = self.tab.pop(sid, None)
+        if ids:
+            self.free.extend(ids)
+        self.dropped.pop(sid, None)
+        self.valid.discard(sid)
+        self.lru.pop(sid, None)
+
+    def sync(self, sid: str, host_tab: list[int] | None, host_dropped: int, pinned) -> bool:
+        """Mirror the host table's front drops and growth; False if it cannot."""
+        if host_tab is None:
+            self.drop(sid)
+            return False
+        ids = self.tab.setdefault(sid, [])
+        self.dropped.setdefault(sid, host_dropped)
+        k = host_dropped - self.dropped[sid]
+        if k > 0:
+            self.free.extend(ids[:k])
+            del ids[:k]
+            self.dropped[sid] = host_dropped
+        if len(ids) > len(host_tab):
+            self.free.extend(ids[len(host_tab):])
+            del ids[len(host_tab):]
+        while len(ids) < len(host_tab):
+            if not self.free and not self._evict(exclude=pinned | {sid}):
+                self.drop(sid)
+                return False
+            ids.append(self.free.popleft())
+        self.lru[sid] = None
+        self.lru.move_to_end(sid)
+        return True
+
+    def _evict(self, exclude) -> bool:
+        for victim in self.lru:
+            if victim not in exclude:
+                self.drop(victim)
+                return True
+        return False
+
+    def offsets(self, sid: str) -> torch.Tensor:
+        return torch.as_tensor([b * self.block_elems for b in self.tab[sid]],
+                               dtype=torch.int64, device=self.device)
+
+
 class Engine:
     """One GPU's serving loop for the reuse path.  Prefills are processed in
     chunks of at most `chunk` = min(max_new, cut) tokens (chunked prefill: a
@@ -85,7 +152,7 @@ class Engine:
                  device="cuda", seed: int = 0, weights: LlamaWeights | None = None,
                  read_buffer_bytes: int = 1 << 30, max_new: int = 1024,
                  truncation_ratio: float = 0.5, ttl: float = math.inf, pin: bool = True,
-                 tp_reduce=None):
+                 tp_reduce=None, hbm_blocks: int = 0):
         self.shape = shape
         self.profile = profile_for(shape, truncation_ratio=truncation_ratio)
         self.block_tokens = block_tokens
@@ -98,8 +165,10 @@ class Engine:
         self.window = shape.context_window
         self.cut = self.profile.cut_tokens
         self.chunk = max(1, min(max_new, self.cut))
+        self.hbm = HbmTier(hbm_blocks, block_bytes, device) if hbm_blocks > 0 else None
         self.runner = Runner(shape, weights=weights, device=device, seed=seed,
                              block_tokens=block_tokens, host_arena=self.arena,
+                             hbm_arena=self.hbm.arena if self.hbm else None,
                              read_buffer_bytes=read_buffer_bytes, max_new=max_new,
                              max_ctx=self.window + self.chunk, tp_reduce=tp_reduce)
         self.context: dict[str, int] = {}
@@ -115,6 +184,15 @@ class Engine:
                 continue
             freed += self.store.charge(it.bytes)
             self.store.remove(it.session_id)
+            if self.hbm is not None:
+                self.hbm.drop(it.session_id)
+
+    def _hbm_sync(self, sid: str) -> bool:
+        if self.hbm is None:
+            return False
+        ok = self.hbm.sync(sid, self.store.tables.get(sid), self.store.dropped.get(sid, 0),
+                           self.store.pinned)
+        return ok
 
     def install_history(self, sid: str, ids: torch.Tensor, now: float = 0.0) -> JobResult:
         """Prefill and store a session history as-is (one job, no truncation):
@@ -149,6 +227,19 @@ class Engine:
             tab = self.store.reserve_rows(sid, kept + c)
             job = Job(sid, ids[pos:pos + c], kept=kept, source="host" if kept else "none",
                       block_ids=tab, save=True, head=self.store.head_row(sid))
+            if self.hbm is not None:
+                resident = sid in self.hbm.valid
+                if self._hbm_sync(sid):
+                    hids = list(self.hbm.tab[sid])
+                    job.mirror_block_ids = hids
+                    if kept and resident:
+                        job.source = "hbm"        # no host link for this chunk
+                        job.dev_block_off = self.hbm.offsets(sid)
+                        self.hbm.hits += 1
+                    elif kept:
+                        job.promote_block_ids = hids
+                        self.hbm.promotions += 1
+                    self.hbm.valid.add(sid)
             results.append(self.runner.run([job], want_logits=want_logits)[0])
             kept += c
             self.store.mark_written(sid, kept)
@@ -186,6 +277,8 @@ class Engine:
             hit = HitClass.MISS
             if self.store.peek(sid) is None:
                 self.store.release_rows(sid)
+            if self.hbm is not None:
+                self.hbm.drop(sid)
             # recompute the whole (truncated) prompt, sim.py:432-435
             results, rows, _ = self._prefill(sid, torch.cat([hist_ids, new_ids]), 0,
                                              want_logits)
@@ -205,6 +298,7 @@ class Engine:
         self.context[sid] = ctx
         if ctx > 0:
             self.store.save(sid, ctx, now)
+        self._hbm_sync(sid)
         self.store.pinned.discard(sid)
         return TurnOutcome(sid, turn_index, hit.value, kept, hist - kept, new, kept + new,
                            overflowed, results[-1], append, results)

@@ -178,3 +178,38 @@ def copy_sm(dst: torch.Tensor, src: torch.Tensor, *, stream=None) -> torch.Tenso
         raise ValueError("copy_sm: host source must be pinned")
     check(lib().askv_copy_sm(dst.data_ptr(), src.data_ptr(), int(n), _stream(stream)), "copy_sm")
     return dst
+
+
+class NativeEvent:
+    """A cudaEvent_t owned through the C ABI (recorded / waited by the native
+    layer loop and the IO threads alike)."""
+
+    __slots__ = ("handle", "_pool")
+
+    def __init__(self, timing: bool = False, pool=None):
+        h = C.c_void_p()
+        check(lib().askv_event_create(C.byref(h), 1 if timing else 0), "event_create")
+        self.handle = h.value
+        self._pool = pool
+
+    def record(self, stream) -> "NativeEvent":
+        check(lib().askv_event_record(self.handle, stream.cuda_stream), "event_record")
+        return self
+
+    def wait(self, stream) -> None:
+        """Make `stream` wait for this event."""
+        check(lib().askv_stream_wait_event(stream.cuda_stream, self.handle), "stream_wait_event")
+
+    def elapsed_ms(self, end: "NativeEvent") -> float:
+        ms = C.c_float()
+        check(lib().askv_event_elapsed_ms(self.handle, end.handle, C.byref(ms)), "elapsed_ms")
+        return float(ms.value)
+
+    elapsed_time = elapsed_ms   # torch.cuda.Event spelling
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().askv_event_destroy(self.handle)
+        except Exception:
+            pass

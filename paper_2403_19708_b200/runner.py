@@ -19,13 +19,16 @@ block table), or none (miss / recompute: the whole prompt
 is prefilled).  Every timing is a CUDA event on the stream doing the work; the
 per-job ``Timeline`` follows overlap.py:31-66 (see overlap.py here).
 
-The projections are plain cuBLAS GEMMs through torch; everything on the
-AttentionStore path itself is libaskv.so (rope_new, reembed, prefill_attn,
-preload_layer, save_layer).
+The per-layer loop of a job is issued natively by ``askv_prefill_layers``
+(csrc/runtime.cu): projections are plain cuBLASLt GEMMs, everything else is
+libaskv.so's own kernels (rmsnorm, rope_new, reembed, prefill_attn, silu_mul);
+pre-load / save DMAs (preload_layer, save_layer) are submitted by two IO
+threads here.
 """
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 import queue
 import threading
@@ -34,7 +37,7 @@ from dataclasses import dataclass, field
 import torch
 import torch.nn.functional as F
 
-from . import ops
+from . import _lib, ops
 from .model import LlamaShape
 from .overlap import Timeline
 
@@ -128,6 +131,11 @@ class Job:
     block_ids: list[int] = field(default_factory=list)
     save: bool = False
     dev_block_off: torch.Tensor | None = None  # "hbm": element offsets per block
+    # HBM session tier: write-through copy of the saved
+    # rows into these HBM-arena blocks, and/or promotion of the pre-loaded rows
+    # (host source) into them; both mirror block_ids one-to-one.
+    mirror_block_ids: list | None = None
+    promote_block_ids: list | None = None
     head: int = 0   # row of session token 0 inside block_ids[0] (store.head_row)
     prestage: bool = False  # start the job only once all its layers are pre-loaded
 
@@ -159,9 +167,47 @@ def attention_flops(kept: int, n: int, hq: int, hd: int) -> int:
 
 
 class _Unit:
-    """One (job, layer) pre-load: a read-buffer slot, its DMA events and a host
-    flag set once the IO thread has submitted the DMA."""
-    __slots__ = ("seq", "slot", "start", "end", "issued")
+    """One (job, layer) pre-load: a read-buffer slot and a host flag set once
+    the IO thread has submitted its DMA (the slot's ``ready`` event is then
+    recorded behind it)."""
+    __slots__ = ("seq", "slot", "times", "issued")
+
+
+class _EventPool:
+    """Recycled timing events for per-job timelines (creating ~10 events per
+    layer per job would cost more host time than issuing the layer)."""
+
+    def __init__(self):
+        self.free: list = []
+
+    def get(self) -> ops.NativeEvent:
+        return self.free.pop() if self.free else ops.NativeEvent(timing=True)
+
+
+class _Lease:
+    """The timing events of one job; they go back to the pool when the job's
+    result is dropped (by then run() has drained the IO threads, so no record
+    of them is still to be submitted)."""
+    __slots__ = ("pool", "events")
+
+    def __init__(self, pool: _EventPool):
+        self.pool, self.events = pool, []
+
+    def get(self) -> ops.NativeEvent:
+        e = self.pool.get()
+        self.events.append(e)
+        return e
+
+    def __del__(self):
+        try:
+            self.pool.free.extend(self.events)
+        except Exception:
+            pass
+
+
+def _ptr_array(items) -> "C.Array":
+    """ctypes void*[] of device pointers / event handles (None -> NULL)."""
+    return (C.c_void_p * len(items))(*items)
 
 
 class _IOThread(threading.Thread):
@@ -200,14 +246,19 @@ class _IOThread(threading.Thread):
 
 class Runner:
     """Executes Jobs back to back; owns streams, HBM buffers and the read /
-    write buffer rings.  One Runner per GPU (one process per GPU)."""
+    write buffer rings.  One Runner per GPU (one process per GPU).
+
+    Each job's layer loop is issued by the native runtime
+    (``askv_prefill_layers``, csrc/runtime.cu); this class only fills the plan
+    (pointers, per-layer slots and events) and drives the pre-load / save IO
+    threads around it."""
 
     def __init__(self, shape: LlamaShape, *, weights: LlamaWeights | None = None,
                  device="cuda", seed: int = 0, theta_base: float = 10000.0,
                  block_tokens: int = 128, host_arena=None, hbm_arena: torch.Tensor | None = None,
                  read_buffer_bytes: int = 4 << 30, write_buffer_bytes: int = 2 << 30,
                  max_new: int = 1024, max_ctx: int | None = None, timeline: bool = True,
-                 tp_reduce=None):
+                 tp_reduce=None, gemm_workspace_bytes: int = 32 << 20):
         self.shape = s = shape
         self.device = torch.device(device)
         self.w = weights or LlamaWeights(shape, seed=seed, device=device)
@@ -226,30 +277,49 @@ class Runner:
         self.s_compute = torch.cuda.Stream(device=self.device)
         self.s_load = torch.cuda.Stream(device=self.device)
         self.s_save = torch.cuda.Stream(device=self.device)
-        # read buffer: ring of per-layer slots of max_ctx rows
+        L = s.layers
+        # read buffer: ring of per-layer slots of max_ctx rows.  A job's L units
+        # are all submitted before its layer loop is issued, so the ring holds
+        # at least L + 1 slots.
         self.slot_rows = self.max_ctx + block_tokens   # + a partial head block
         slot_bytes = self.slot_rows * s.row_bytes
-        self.n_slots = max(2, int(read_buffer_bytes // slot_bytes))
+        self.n_slots = max(L + 1, int(read_buffer_bytes // slot_bytes))
         self.slots = torch.empty((self.n_slots, self.slot_rows, s.row_elems), dtype=BF16,
                                  device=self.device)
+        self._slot_ready = [ops.NativeEvent() for _ in range(self.n_slots)]
+        self._slot_free = [ops.NativeEvent() for _ in range(self.n_slots)]
         self._units: dict = {}          # (jid, layer) -> _Unit
         self._seq = 0                    # pre-load units enqueued so far
-        self._freed: dict = {}           # unit seq -> (event on s_compute, host flag)
+        self._freed: dict = {}           # unit seq -> host flag: its slot's reader is issued
         self._io_load = _IOThread(self.device, "askv-preload")
         self._io_save = _IOThread(self.device, "askv-save")
-        # write buffer: ring of per-layer slots of max_new rows
-        self.n_wslots = max(2, int(write_buffer_bytes // (max_new * s.row_bytes)))
+        # write buffer: ring of per-layer slots of max_new rows (>= L: one job's
+        # layers never share a slot)
+        self.n_wslots = max(L, int(write_buffer_bytes // (max_new * s.row_bytes)))
         self.wbuf = torch.empty((self.n_wslots, max_new, s.row_elems), dtype=BF16,
                                 device=self.device)
         self._wseq = 0
-        self._wdone = [None] * self.n_wslots   # (event on s_save, host flag) per slot
-        self._last_save: dict = {}             # session -> (event, flag) of its last save
+        self._wready = [ops.NativeEvent() for _ in range(self.n_wslots)]
+        self._wdone = [ops.NativeEvent() for _ in range(self.n_wslots)]
+        self._wflag: list = [None] * self.n_wslots   # host flag: slot's last save submitted
+        self._sess_ev: dict = {}                     # session -> event of its last save
+        self._last_save: dict = {}                   # session -> (event, host flag)
+        self._pool = _EventPool()
+        self._leases: dict = {}
         self._bufs = {}
         self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
+        self._gemm_ws = torch.empty(gemm_workspace_bytes, dtype=torch.uint8, device=self.device)
+        self._w_arrays = {
+            key: _ptr_array([lw[key].data_ptr() for lw in self.w.layers])
+            for key in ("w_in", "wqkv", "wo", "w_post", "wgu", "wd")}
         # tensor parallelism (config C5): tp_reduce(t, stream) sums the row-parallel
         # partials of W_o and W_down over the TP group in place (NCCL all-reduce
-        # over NVLink in a multi-GPU run; dist.ThreadAllReduce in the 1-GPU emulation)
+        # over NVLink in a multi-GPU run; dist.ThreadAllReduce in the 1-GPU emulation).
+        # The native loop calls back into it between the partial GEMM and the
+        # residual add.
         self.tp_reduce = tp_reduce
+        self._cb_error = None
+        self._ar_cb = _lib.ALLREDUCE_FN(self._allreduce) if tp_reduce is not None else None
         self.launches = 0          # libaskv kernel launches issued (all streams)
         self.probe = None          # list -> (kind, ev0, ev1, work) per probed launch
 
@@ -266,12 +336,30 @@ class Runner:
             self._ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         return self._ws
 
+    def _allreduce(self, ptr, elems, stream, ctx):
+        try:
+            h = self._bufs["h"].view(-1)
+            if h.data_ptr() != ptr:
+                raise RuntimeError("all-reduce callback on an unexpected buffer")
+            self.tp_reduce(h[:elems], self.s_compute)
+        except BaseException as exc:  # re-raised after the native call returns
+            self._cb_error = exc
+
+    def _lease(self, jid):
+        if not self.timeline:
+            return None
+        lease = self._leases.get(jid)
+        if lease is None:
+            lease = self._leases[jid] = _Lease(self._pool)
+        return lease
+
     # ------------------------------------------------------------------ K1 pre-loader
     def _enqueue_loads(self, jid, job: Job):
         """Queue the job's L pre-load units for the IO thread.  Unit seq k uses
-        slot k % n_slots and first waits (host flag, then device event) for the
-        release of unit k - n_slots, so the copy stream runs as far ahead as
-        the read buffer allows -- across jobs, i.e. the read-buffer head start."""
+        slot k % n_slots and first waits (host flag, then the slot's ``free``
+        event) for the release of unit k - n_slots, so the copy stream runs as
+        far ahead as the read buffer allows -- across jobs, i.e. the
+        read-buffer head start."""
         if job.source != "host" or job.kept == 0:
             return
         if self.host_arena is None:
@@ -283,34 +371,35 @@ class Runner:
         tail = (rows - (nb - 1) * self.block_tokens) * self.row_bytes
         ids = list(job.block_ids[:nb])
         dep = self._last_save.get(job.session_id)
+        lease = self._lease(jid)
         for layer in range(self.shape.layers):
             u = _Unit()
             u.seq = self._seq
             u.slot = u.seq % self.n_slots
-            u.start = torch.cuda.Event(enable_timing=self.timeline)
-            u.end = torch.cuda.Event(enable_timing=self.timeline)
+            u.times = (lease.get(), lease.get()) if lease else None
             u.issued = threading.Event()
             self._seq += 1
             self._units[(jid, layer)] = u
             prev = u.seq - self.n_slots
-            if prev >= 0 and prev not in self._freed:
-                self._freed[prev] = (torch.cuda.Event(), threading.Event())
-            freed = self._freed.get(prev) if prev >= 0 else None
+            freed = self._freed.setdefault(prev, threading.Event()) if prev >= 0 else None
 
             def submit(u=u, layer=layer, freed=freed, dep=dep):
                 try:
-                    with torch.cuda.stream(self.s_load):
-                        if freed is not None:   # slot reuse: its previous reader is done
-                            freed[1].wait()
-                            self.s_load.wait_event(freed[0])
-                        if dep is not None:     # rows saved by this session's previous turn
-                            dep[1].wait()
-                            self.s_load.wait_event(dep[0])
-                        u.start.record(self.s_load)
-                        ops.preload_layer(self.slots[u.slot], self.host_arena.buffer, ids,
-                                          self.block_bytes, layer * self.chunk_bytes,
-                                          self.chunk_bytes, tail, stream=self.s_load)
-                        u.end.record(self.s_load)
+                    sl = self.s_load
+                    if freed is not None:   # slot reuse: its previous reader is done
+                        freed.wait()
+                        self._slot_free[u.slot].wait(sl)
+                    if dep is not None:     # rows saved by this session's previous turn
+                        dep[1].wait()
+                        dep[0].wait(sl)
+                    if u.times:
+                        u.times[0].record(sl)
+                    ops.preload_layer(self.slots[u.slot], self.host_arena.buffer, ids,
+                                      self.block_bytes, layer * self.chunk_bytes,
+                                      self.chunk_bytes, tail, stream=sl)
+                    self._slot_ready[u.slot].record(sl)
+                    if u.times:
+                        u.times[1].record(sl)
                 finally:
                     u.issued.set()
 
@@ -327,25 +416,33 @@ class Runner:
         return u
 
     def _release(self, u: _Unit):
-        """The slot's reader (K2) is enqueued: record it and wake the IO thread."""
-        ent = self._freed.get(u.seq)
-        if ent is None:
-            ent = self._freed[u.seq] = (torch.cuda.Event(), threading.Event())
-        ent[0].record(self.s_compute)
-        ent[1].set()
+        """The slot's reader (K2) is issued and its ``free`` event recorded:
+        wake the IO thread."""
+        self._freed.setdefault(u.seq, threading.Event()).set()
         self._freed.pop(u.seq - 2 * self.n_slots, None)
 
-    def _submit_save(self, produced, arena, job, layer, kept, n, wslot, sv0, sv1, flag):
+    def _submit_save(self, arena, job, layer, kept, n, wslot, times, flag, last):
+        sess_ev = self._sess_ev.get(job.session_id) if last else None
+
         def submit():
             try:
-                with torch.cuda.stream(self.s_save):
-                    self.s_save.wait_event(produced)
-                    if sv0 is not None:
-                        sv0.record(self.s_save)
-                    ops.save_layer(arena, job.block_ids, self.block_bytes,
-                                   layer * self.chunk_bytes, self.block_tokens, self.row_bytes,
-                                   job.head + kept, n, self.wbuf[wslot], stream=self.s_save)
-                    sv1.record(self.s_save)
+                ss = self.s_save
+                self._wready[wslot].wait(ss)
+                if times:
+                    times[0].record(ss)
+                ops.save_layer(arena, job.block_ids, self.block_bytes,
+                               layer * self.chunk_bytes, self.block_tokens, self.row_bytes,
+                               job.head + kept, n, self.wbuf[wslot], stream=ss)
+                if job.mirror_block_ids is not None:   # HBM tier, write-through
+                    ops.save_layer(self.hbm_arena, job.mirror_block_ids, self.block_bytes,
+                                   layer * self.chunk_bytes, self.block_tokens,
+                                   self.row_bytes, job.head + kept, n, self.wbuf[wslot],
+                                   stream=ss)
+                self._wdone[wslot].record(ss)
+                if sess_ev is not None:
+                    sess_ev.record(ss)
+                if times:
+                    times[1].record(ss)
             finally:
                 flag.set()
 
@@ -388,8 +485,15 @@ class Runner:
             if t.error is not None:
                 raise RuntimeError(f"{t.name} failed") from t.error
 
+    def _probe_pair(self, kind, work, starts, ends):
+        e0, e1 = ops.NativeEvent(timing=True), ops.NativeEvent(timing=True)
+        starts.append(e0.handle)
+        ends.append(e1.handle)
+        self.probe.append((kind, e0, e1, work))
+
     def _run_job(self, jid, job: Job, want_logits: bool) -> JobResult:
         s = self.shape
+        L = s.layers
         n, kept = job.n_new, job.kept
         if n < 1:
             raise ValueError("a job needs at least one new token")
@@ -399,6 +503,10 @@ class Runner:
             raise ValueError("context exceeds the runner's RoPE table")
         if job.save and len(job.block_ids) * self.block_tokens < job.head + kept + n:
             raise ValueError("save needs block_ids covering kept + new rows")
+        if kept and job.source not in ("host", "hbm"):
+            raise ValueError(f"job with kept={kept} needs a source")
+        if kept and job.source == "hbm" and job.dev_block_off is None:
+            raise ValueError("hbm job needs dev_block_off")
         arena = None
         if job.save:
             arena = self.hbm_arena if job.source == "hbm" else (
@@ -407,19 +515,32 @@ class Runner:
                 raise RuntimeError("save requested but no arena for it")
         hd, hq, hkv = s.head_dim, s.n_heads, s.n_kv_heads
         cs = self.s_compute
-        ev = (lambda: torch.cuda.Event(enable_timing=True)) if self.timeline else None
-        rec = {"layers": [], "waits": [], "saves": [], "loads": []}
+        lease = self._lease(jid)
+        self._leases.pop(jid, None)
+        T = (lambda: lease.get().handle) if lease else (lambda: None)  # noqa: E731
+        keep = []                       # ctypes arrays alive through the native call
+
+        def arr(items):
+            a = _ptr_array(items)
+            keep.append(a)
+            return a
+
         first = torch.empty(1, dtype=torch.int64, pin_memory=True)
         logits_out = None
+        rec = {"layers": [], "waits": [], "saves": [], "loads": []}
         with torch.cuda.stream(cs):
-            if job.prestage and job.source == "host" and kept:
-                if s.layers > self.n_slots:
-                    raise RuntimeError("read buffer too small to prestage a whole job")
-                last = self._units[(jid, s.layers - 1)]
-                if not last.issued.wait(timeout=600):
-                    raise RuntimeError("pre-load IO thread stalled")
-                cs.wait_event(last.end)
-            t0 = ev() if ev else None
+            if job.source == "hbm" or job.mirror_block_ids is not None:
+                # HBM-tier rows written by this session's previous saves (save stream)
+                dep = self._last_save.get(job.session_id)
+                if dep is not None:
+                    dep[1].wait()
+                    dep[0].wait(cs)
+            units = None
+            if kept and job.source == "host":
+                units = [self._acquire(jid, l) for l in range(L)]
+                if job.prestage:   # start only once the whole job is resident
+                    self._slot_ready[units[-1].slot].wait(cs)
+            t0 = lease.get() if lease else None
             if t0:
                 t0.record(cs)
             if job.token_ids.is_cuda:
@@ -430,124 +551,122 @@ class Runner:
                                   src.to(torch.int64), stream=cs)
                 self.launches += 1
             x = F.embedding(ids, self.w.embed)
-            q_rot = self._buf("q", n, hq * hd)
-            kvbuf = self._buf("kv", kept + n, self.row_elems)
-            ao = self._buf("ao", n, hq * hd)
+            self._buf("h", n, s.d_model)
             splits = ops.attn_num_splits(kept, n, hq)
             wsb = ops.attn_workspace_bytes(kept, n, hq, hd, splits)
             ws = self._workspace(wsb) if wsb else None
-            for layer, lw in enumerate(self.w.layers):
-                l0 = ev() if ev else None
-                if l0:
-                    l0.record(cs)
-                h = ops.rmsnorm(x, lw["w_in"], 1e-5, stream=cs)
-                qkv = F.linear(h, lw["wqkv"])
-                wslot = None
-                if job.save:
-                    wslot = self._wseq % self.n_wslots
+
+            p = _lib.PrefillPlan()
+            p.layers, p.d_model, p.n_heads, p.n_kv_heads = L, s.d_model, hq, hkv
+            p.head_dim, p.ffn, p.n_new, p.kept, p.head = hd, s.ffn, n, kept, job.head
+            p.rms_eps, p.attn_scale, p.attn_splits = 1e-5, 1.0 / math.sqrt(hd), splits
+            wa = self._w_arrays
+            p.w_in, p.w_qkv, p.w_o = wa["w_in"], wa["wqkv"], wa["wo"]
+            p.w_post, p.w_gu, p.w_down = wa["w_post"], wa["wgu"], wa["wd"]
+            p.x = x.data_ptr()
+            p.h = self._bufs["h"].data_ptr()
+            p.qkv = self._buf("qkv", n, s.qkv_cols).data_ptr()
+            p.q_rot = self._buf("q", n, hq * hd).data_ptr()
+            p.kv = self._buf("kv", kept + n, self.row_elems).data_ptr()
+            p.attn_out = self._buf("ao", n, hq * hd).data_ptr()
+            p.gu = self._buf("gu", n, 2 * s.ffn).data_ptr()
+            p.act = self._buf("act", n, s.ffn).data_ptr()
+            if ws is not None:
+                p.attn_ws, p.attn_ws_bytes = ws.data_ptr(), ws.numel()
+            p.gemm_ws, p.gemm_ws_bytes = self._gemm_ws.data_ptr(), self._gemm_ws.numel()
+            p.rope_table = self.table.table.data_ptr()
+            p.rope_positions = self.table.max_pos
+            p.block_tokens = self.block_tokens
+            p.src_row_stride = self.row_elems
+            p.block_bytes, p.chunk_bytes, p.row_bytes = (self.block_bytes, self.chunk_bytes,
+                                                         self.row_bytes)
+            if units is not None:
+                p.src_kind = 1
+                p.src_layer = arr([self.slots[u.slot].data_ptr() for u in units])
+                p.ev_src_ready = arr([self._slot_ready[u.slot].handle for u in units])
+                p.ev_src_free = arr([self._slot_free[u.slot].handle for u in units])
+                if job.promote_block_ids is not None:   # into the HBM tier
+                    ids64 = (C.c_int64 * len(job.promote_block_ids))(*job.promote_block_ids)
+                    keep.append(ids64)
+                    p.promote_base = self.hbm_arena.data_ptr()
+                    p.promote_block_ids = ids64
+                    p.promote_nblocks = len(job.promote_block_ids)
+                for u in units:
+                    if u.times:
+                        rec["loads"].append(u.times)
+            elif kept:
+                p.src_kind = 2
+                base = self.hbm_arena.data_ptr()
+                p.src_layer = arr([base + l * self.chunk_bytes for l in range(L)])
+                p.src_block_off = job.dev_block_off.data_ptr()
+            wslots = []
+            if job.save:
+                for _ in range(L):
+                    w = self._wseq % self.n_wslots
                     self._wseq += 1
-                    if self._wdone[wslot] is not None:   # slot's previous D2H finished
-                        self._wdone[wslot][1].wait()
-                        cs.wait_event(self._wdone[wslot][0])
-                ops.rope_new(qkv, n, hq, hkv, hd, self.table, kept, q_rot, kvbuf[kept:],
-                             self.wbuf[wslot] if wslot is not None else None, stream=cs)
-                self.launches += 1
-                if job.save:
-                    produced = torch.cuda.Event()
-                    produced.record(cs)
-                    sv0 = ev() if ev else None
-                    sv1 = torch.cuda.Event(enable_timing=self.timeline)
-                    flag = threading.Event()
-                    self._submit_save(produced, arena, job, layer, kept, n, wslot, sv0, sv1,
-                                      flag)
-                    self._wdone[wslot] = (sv1, flag)
-                    rec["saves"].append((sv0, sv1, flag))
+                    if self._wflag[w] is not None:   # its previous save is submitted
+                        self._wflag[w].wait()
+                    wslots.append(w)
+                p.save_rows = arr([self.wbuf[w].data_ptr() for w in wslots])
+                p.ev_save_free = arr([self._wdone[w].handle for w in wslots])
+                p.ev_save_ready = arr([self._wready[w].handle for w in wslots])
+            if lease:
+                lb, le = [T() for _ in range(L)], [T() for _ in range(L)]
+                p.ev_layer_begin, p.ev_layer_end = arr(lb), arr(le)
+                rec["layers"] = list(zip(lb, le))
                 if kept:
-                    if job.source == "host":
-                        u = self._acquire(jid, layer)
-                        w0 = ev() if ev else None
-                        if w0:
-                            w0.record(cs)
-                        cs.wait_event(u.end)
-                        w1 = ev() if ev else None
-                        if w1:
-                            w1.record(cs)
-                        rec["waits"].append((w0, w1))
-                        rec["loads"].append((u.start, u.end))
-                        p0 = self._probe_begin()
-                        ops.reembed(self.slots[u.slot], kept, hkv, hd, self.table, kvbuf,
-                                    first_token=job.head, pos0=0, stream=cs)
-                        self._probe_end(p0, "reembed", 2 * kept * s.row_bytes)
-                        self.launches += 1
-                        self._release(u)
-                    elif job.source == "hbm":
-                        if job.dev_block_off is None:
-                            raise ValueError("hbm job needs dev_block_off")
-                        src = self.hbm_arena[layer * self.block_tokens * self.row_elems:]
-                        p0 = self._probe_begin()
-                        ops.reembed(src, kept, hkv, hd, self.table, kvbuf,
-                                    first_token=job.head, pos0=0, block_off=job.dev_block_off,
-                                    block_tokens=self.block_tokens, stream=cs)
-                        self._probe_end(p0, "reembed", 2 * kept * s.row_bytes)
-                        self.launches += 1
-                    else:
-                        raise ValueError(f"job with kept={kept} needs a source")
-                p0 = self._probe_begin()
-                ops.prefill_attn(q_rot, kvbuf, kept, n, hq, hkv, hd, ao, ws,
-                                 num_splits=splits, stream=cs)
-                self._probe_end(p0, "attention", attention_flops(kept, n, hq, hd))
-                self.launches += 2 if splits > 1 else 1
-                if self.tp_reduce is None:
-                    x = torch.addmm(x, ao, lw["wo"].t())
-                else:
-                    y = torch.mm(ao, lw["wo"].t())
-                    self.tp_reduce(y, cs)
-                    x = x + y
-                h = ops.rmsnorm(x, lw["w_post"], 1e-5, stream=cs)
-                gu = F.linear(h, lw["wgu"])
-                a = ops.silu_mul(gu, stream=cs)
-                if self.tp_reduce is None:
-                    x = torch.addmm(x, a, lw["wd"].t())
-                else:
-                    y = torch.mm(a, lw["wd"].t())
-                    self.tp_reduce(y, cs)
-                    x = x + y
-                self.launches += 3
-                l1 = ev() if ev else None
-                if l1:
-                    l1.record(cs)
-                rec["layers"].append((l0, l1))
+                    wb, we = [T() for _ in range(L)], [T() for _ in range(L)]
+                    p.ev_wait_begin, p.ev_wait_end = arr(wb), arr(we)
+                    rec["waits"] = list(zip(wb, we))
+            if self.probe is not None:
+                rb, re_, ab, ae = [], [], [], []
+                for _ in range(L):
+                    if kept:
+                        self._probe_pair("reembed", 2 * kept * s.row_bytes, rb, re_)
+                    self._probe_pair("attention", attention_flops(kept, n, hq, hd), ab, ae)
+                if kept:
+                    p.ev_reembed_begin, p.ev_reembed_end = arr(rb), arr(re_)
+                p.ev_attn_begin, p.ev_attn_end = arr(ab), arr(ae)
+            if self._ar_cb is not None:
+                p.allreduce = self._ar_cb
+            self._cb_error = None
+            _lib.check(_lib.lib().askv_prefill_layers(C.addressof(p), cs.cuda_stream),
+                       "prefill_layers")
+            if self._cb_error is not None:
+                raise RuntimeError("tensor-parallel all-reduce failed") from self._cb_error
+            self.launches += L * (4 + (1 if kept else 0) + (2 if splits > 1 else 1)
+                                  + (2 if self.tp_reduce is not None else 0))
+            if units is not None:
+                for u in units:
+                    self._release(u)
+            if job.save:
+                sess_ev = self._sess_ev.get(job.session_id)
+                if sess_ev is None:
+                    sess_ev = self._sess_ev[job.session_id] = ops.NativeEvent()
+                flag = None
+                for layer, w in enumerate(wslots):
+                    times = (lease.get(), lease.get()) if lease else None
+                    flag = threading.Event()
+                    self._wflag[w] = flag
+                    self._submit_save(arena, job, layer, kept, n, w, times, flag,
+                                      layer == L - 1)
+                    if times:
+                        rec["saves"].append((times[0], times[1], flag))
+                self._last_save[job.session_id] = (sess_ev, flag)
             hl = ops.rmsnorm(x[-1:], self.w.w_final, 1e-5, stream=cs)
             logits = F.linear(hl, self.w.lm_head).float()
             ops.copy_sm(first, logits.argmax(dim=-1), stream=cs)
-            self.launches += 1
+            self.launches += 2
             if want_logits:
                 logits_out = logits[0].clone()
-            t1 = ev() if ev else None
+            t1 = lease.get() if lease else None
             if t1:
                 t1.record(cs)
-        if job.save:
-            _, sv1, flag = rec["saves"][-1]
-            self._last_save[job.session_id] = (sv1, flag)
         res = JobResult(job.session_id, kept, n, None, first, logits_out,
                         bytes_loaded=kept * s.kv_bytes_per_token if job.source == "host" else 0,
                         bytes_saved=n * s.kv_bytes_per_token if job.save else 0)
-        res._events = (t0, t1, rec) if ev else None
+        res._events = (t0, t1, rec, lease) if lease else None
         return res
-
-    def _probe_begin(self):
-        if self.probe is None:
-            return None
-        e = torch.cuda.Event(enable_timing=True)
-        e.record(self.s_compute)
-        return e
-
-    def _probe_end(self, e0, kind, work):
-        if e0 is None:
-            return
-        e1 = torch.cuda.Event(enable_timing=True)
-        e1.record(self.s_compute)
-        self.probe.append((kind, e0, e1, work))
 
     def join(self) -> None:
         """Make the compute stream wait for all loads and saves queued so far
@@ -564,8 +683,15 @@ class Runner:
             evs = getattr(r, "_events", None)
             if not evs:
                 continue
-            t0, t1, rec = evs
-            f = lambda e: t0.elapsed_time(e) * 1e-3  # noqa: E731
+            t0, t1, rec, lease = evs
+            ms = C.c_float()
+            lib = _lib.lib()
+
+            def f(e):
+                h = e if isinstance(e, int) else e.handle
+                _lib.check(lib.askv_event_elapsed_ms(t0.handle, h, C.byref(ms)), "elapsed")
+                return float(ms.value) * 1e-3
+
             tl = Timeline()
             tl.makespan = f(t1)
             waits = [(f(a), f(b)) for a, b in rec["waits"]]
@@ -576,7 +702,7 @@ class Runner:
             tl.save_intervals = [(f(a), f(b)) for a, b, _ in rec["saves"]]
             comp = []
             wi = iter(waits)
-            for li, (a, b) in enumerate(rec["layers"]):
+            for a, b in rec["layers"]:
                 la, lb = f(a), f(b)
                 if waits:
                     wa, wb = next(wi)

@@ -41,6 +41,8 @@ def test_ctypes_table_matches_header(built):
     lib = _lib.lib()
     assert lib.askv_version() == 100
     assert lib.askv_last_error() == b""
+    # the ctypes mirror of askv_prefill_plan has the C layout
+    assert ctypes.sizeof(_lib.PrefillPlan) == lib.askv_prefill_plan_size()
 
 
 def test_split_policy_without_gpu(built):

@@ -250,3 +250,31 @@ def test_tensor_parallel_emulation_matches_unsharded():
     for k in range(len(turns)):
         for r in range(tp):
             assert rope_ref.rel_err(got[r][k].numpy(), want[k].numpy()) <= LOGIT_TOL, (k, r)
+
+
+def test_hbm_tier_is_bit_identical_to_host_path():
+    """HBM session tier: the same multi-turn session with
+    truncation served from the HBM mirror gives bit-identical logits to the
+    host-DRAM path, and the tier is actually hit (no host link on hits)."""
+    engine, model, runner = _mods()
+    from dataclasses import replace
+    shape = replace(model.shape("tiny"), context_window=64)
+    w = runner.LlamaWeights(shape, seed=7)
+    host = engine.Engine(shape, host_blocks=64, block_tokens=16, weights=w, max_new=64,
+                         read_buffer_bytes=16 << 20)
+    tier = engine.Engine(shape, host_blocks=64, block_tokens=16, weights=w, max_new=64,
+                         read_buffer_bytes=16 << 20, hbm_blocks=16)
+    rng = np.random.default_rng(7)
+    loaded = 0
+    for k in range(6):
+        new_ids = torch.as_tensor(rng.integers(0, shape.vocab, 12))
+        out_ids = torch.as_tensor(rng.integers(0, shape.vocab, 9))
+        a = host.turn("s", k, new_ids, out_ids, want_logits=True)
+        b = tier.turn("s", k, new_ids, out_ids, want_logits=True)
+        torch.cuda.synchronize()
+        assert (a.kept, a.drop, a.hit) == (b.kept, b.drop, b.hit)
+        assert torch.equal(a.result.logits, b.result.logits), k
+        loaded += b.result.bytes_loaded
+    assert tier.hbm.hits >= 4 and loaded == 0
+    tier.store.check_invariants()
+    assert len(tier.hbm.tab["s"]) == len(tier.store.block_table("s"))

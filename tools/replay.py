@@ -42,6 +42,8 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--sessions", type=int, default=0)
     ap.add_argument("--host-gb", type=float, default=120.0)
+    ap.add_argument("--hbm-gb", type=float, default=0.0,
+                    help="HBM session tier capacity (SURVEY.md §8f item 1); 0 = DRAM only")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     from paper_2403_19708_b200 import engine, metrics, model
@@ -56,7 +58,8 @@ def main():
     host_blocks = int(a.host_gb * 1e9 // block_bytes)
     weights = LlamaWeights(shape, seed=0)
     eng = engine.Engine(shape, host_blocks=host_blocks, block_tokens=tb, weights=weights,
-                        max_new=2048, read_buffer_bytes=4 << 30)
+                        max_new=2048, read_buffer_bytes=4 << 30,
+                        hbm_blocks=int(a.hbm_gb * 1e9 // block_bytes))
     turns = sorted(((s["arrivals"][k], s["id"], k, s["turns"][k][0], s["turns"][k][1])
                     for s in sessions for k in range(len(s["turns"]))))
     rng = np.random.default_rng(0)
@@ -107,6 +110,8 @@ def main():
                                      "recompute": metrics.percentile(hit_rc, 0.5)},
         "store": {"mem_used": eng.store.mem_used, "items": len(eng.store.items),
                   "arena_blocks": host_blocks},
+        "hbm_tier": ({"gb": a.hbm_gb, "hits": eng.hbm.hits, "promotions": eng.hbm.promotions}
+                     if eng.hbm else None),
         "wall_s_reuse_replay": reuse_wall,
         "note": "TTFT = FIFO serial-prefill queue on measured makespans at the workload's "
                 "arrival times (no read-buffer head start: the load starts with the job)",
