@@ -22,12 +22,28 @@
 #include <cstdint>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "askv_internal.h"
 #include "askv_ptx.cuh"
 
 namespace askv {
 namespace {
+
+// Optional in-kernel timeline (tools/attn_trace.cu builds with ASKV_ATTN_TRACE):
+// globaltimer stamps per CTA at fixed slots.
+#ifdef ASKV_ATTN_TRACE
+__device__ unsigned long long* g_attn_trace = nullptr;
+__device__ __forceinline__ void trace_stamp(int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  if (g_attn_trace) g_attn_trace[cta * 64 + slot] = t;
+}
+#define ATTN_TRACE(slot) trace_stamp(slot)
+#else
+#define ATTN_TRACE(slot) ((void)0)
+#endif
 
 constexpr int kBM = 128;  // query rows per tile (UMMA M)
 constexpr int kBN = 128;  // key rows per tile (UMMA N of S, K of PV)
@@ -123,6 +139,7 @@ __global__ void __launch_bounds__(320, 1)
   const int h = blockIdx.y;
   const int split = blockIdx.z;
   const int kh = h / p.group;
+  if (threadIdx.x == 0) ATTN_TRACE(0);
   // query tiles of this CTA: A at q0, B at q0 + 128 (paired only)
   const int q0 = blockIdx.x * kBM * C::kQTiles;
   const int rows_a = min(kBM, p.n_new - q0);
@@ -183,6 +200,7 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) ATTN_TRACE(1);
 
   if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
@@ -233,6 +251,7 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t idesc_o = idesc_bf16_f32(kBM, HD, 0, 1);
       const uint32_t sk = smem_u32(sK), sv = smem_u32(sV);
       mbar_wait(q_full, 0);
+      ATTN_TRACE(2);
       // S_w(j) = Q_w K_j^T into group w's S columns
       auto issue_s = [&](int w, int j) {
         const uint32_t sq = smem_u32(sQ) + (paired ? w * C::kTileBytes : 0);
@@ -310,7 +329,7 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
     }
-  } else {
+  } else if (warp < 8) {
     // ------------------------------------------------------------ softmax groups
     const int w = warp >> 2;
     const int r = (warp & 3) * 32 + lane;  // row in tile == TMEM lane
@@ -322,33 +341,34 @@ __global__ void __launch_bounds__(320, 1)
     const float sl2 = p.scale_log2;
     const int my_tiles = paired ? (w ? nt_b : nt_a) : (n_tiles - w + 1) / 2;
     float m_acc = -INFINITY, l_acc = 0.f;
-    for (int t = 0; t < my_tiles; ++t) {
-      const int j = paired ? t : 2 * t + w;
-      mbar_wait(&s_full[w], t & 1);
-      tc_fence_after();
-      const int kbase = (t_begin + j) * kBN;
-      const int lim = row_limit - kbase;
-      // group-uniform: does any row of this tile see a masked column here?
-      const bool diag = kbase + kBN - 1 > p.n_cached + qt0;
-      float mx = -INFINITY;
+    // One tile of the online softmax.  The whole 128-column S row is pulled
+    // into registers with four back-to-back tcgen05.ld and a single wait, so
+    // the max pass and the exp pass read registers, not TMEM; the column mask
+    // exists only in the diagonal-tile instance (kMask), keeping the common
+    // off-diagonal tile free of per-element selects.
+    auto tile = [&](auto mask_tag, int t, int lim) {
+      constexpr bool kMask = decltype(mask_tag)::value;
+      uint32_t sr[kBN];
 #pragma unroll
-      for (int c = 0; c < kBN / 32; ++c) {
-        float sv[32];
-        tmem_ld32(t_s + c * 32, sv);
-        if (diag) {
+      for (int c = 0; c < kBN / 32; ++c)
+        tmem_ld32_nowait(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+      tmem_wait_ld();
+      if (kMask) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) mx = fmaxf(mx, (c * 32 + e <= lim) ? sv[e] : -INFINITY);
-        } else {
-          float m0 = fmax3(sv[0], sv[1], sv[2]), m1 = fmax3(sv[3], sv[4], sv[5]);
-#pragma unroll
-          for (int e = 6; e < 30; e += 4) {
-            m0 = fmax3(m0, sv[e], sv[e + 1]);
-            m1 = fmax3(m1, sv[e + 2], sv[e + 3]);
-          }
-          mx = fmax3(mx, fmax3(m0, m1, sv[30]), sv[31]);
-        }
+        for (int e = 0; e < kBN; ++e) sr[e] = (e <= lim) ? sr[e] : 0xff800000u;  // -inf
       }
-      const float m_tile = mx * sl2;
+      float a0 = fmaxf(__uint_as_float(sr[0]), __uint_as_float(sr[1]));
+      float a1 = fmaxf(__uint_as_float(sr[2]), __uint_as_float(sr[3]));
+      float a2 = fmaxf(__uint_as_float(sr[4]), __uint_as_float(sr[5]));
+      float a3 = fmaxf(__uint_as_float(sr[6]), __uint_as_float(sr[7]));
+#pragma unroll
+      for (int e = 8; e < kBN; e += 8) {
+        a0 = fmax3(a0, __uint_as_float(sr[e + 0]), __uint_as_float(sr[e + 1]));
+        a1 = fmax3(a1, __uint_as_float(sr[e + 2]), __uint_as_float(sr[e + 3]));
+        a2 = fmax3(a2, __uint_as_float(sr[e + 4]), __uint_as_float(sr[e + 5]));
+        a3 = fmax3(a3, __uint_as_float(sr[e + 6]), __uint_as_float(sr[e + 7]));
+      }
+      const float m_tile = fmax3(fmax3(a0, a1, a2), a3, -INFINITY) * sl2;
       const bool need = m_tile > m_acc + C::kRescaleLog2;
       if (t == 0) {
         if (need) m_acc = m_tile;
@@ -357,7 +377,7 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(&o_full[w], (t - 1) & 1);
         tc_fence_after();
         const float f = need ? ex2(m_acc - m_tile) : 1.f;
-#pragma unroll
+#pragma unroll 1
         for (int c = 0; c < HD / 32; ++c) {
           float ov[32];
           tmem_ld32(t_o + c * 32, ov);
@@ -373,37 +393,50 @@ __global__ void __launch_bounds__(320, 1)
       }
       const float neg_m = (m_acc == -INFINITY) ? 0.f : -m_acc;
       const float2 sl2v = make_float2(sl2, sl2), negm2 = make_float2(neg_m, neg_m);
-      float2 ls0 = make_float2(0.f, 0.f), ls1 = make_float2(0.f, 0.f);
+      float2 ls0 = make_float2(0.f, 0.f), ls1 = ls0, ls2 = ls0, ls3 = ls0;
 #pragma unroll
       for (int c = 0; c < kBN / 32; ++c) {
-        float sv[32];
-        tmem_ld32(t_s + c * 32, sv);
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          const float2 x = ffma2(make_float2(sv[e], sv[e + 1]), sl2v, negm2);
-          float2 pp = make_float2(ex2(x.x), ex2(x.y));
-          if (diag) {
-            pp.x = (c * 32 + e <= lim) ? pp.x : 0.f;
-            pp.y = (c * 32 + e + 1 <= lim) ? pp.y : 0.f;
+          const int k = c * 32 + e;
+          const float2 x = ffma2(make_float2(__uint_as_float(sr[k]), __uint_as_float(sr[k + 1])),
+                                 sl2v, negm2);
+          const float2 pp = make_float2(ex2(x.x), ex2(x.y));
+          switch ((e >> 1) & 3) {
+            case 0: ls0 = fadd2(ls0, pp); break;
+            case 1: ls1 = fadd2(ls1, pp); break;
+            case 2: ls2 = fadd2(ls2, pp); break;
+            default: ls3 = fadd2(ls3, pp); break;
           }
-          if ((e >> 1) & 1)
-            ls1 = fadd2(ls1, pp);
-          else
-            ls0 = fadd2(ls0, pp);
           pk[e >> 1] = pack_bf16x2(pp.x, pp.y);
         }
-        tmem_st16(t_s + c * 16, pk);  // P over the already-read S columns
+        tmem_st16(t_s + c * 16, pk);  // P (bf16 pairs) over the S columns already read
       }
-      l_acc += (ls0.x + ls0.y) + (ls1.x + ls1.y);
+      const float2 la = fadd2(ls0, ls1), lb = fadd2(ls2, ls3);
+      l_acc += (la.x + la.y) + (lb.x + lb.y);
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&p_full[w]);
+    };
+    for (int t = 0; t < my_tiles; ++t) {
+      const int j = paired ? t : 2 * t + w;
+      mbar_wait(&s_full[w], t & 1);
+      if (threadIdx.x == 0 && t < 28) ATTN_TRACE(8 + 2 * t);
+      tc_fence_after();
+      const int kbase = (t_begin + j) * kBN;
+      // group-uniform: does any row of this tile see a masked column here?
+      if (kbase + kBN - 1 > p.n_cached + qt0)
+        tile(std::true_type{}, t, row_limit - kbase);
+      else
+        tile(std::false_type{}, t, 0);
+      if (threadIdx.x == 0 && t < 28) ATTN_TRACE(9 + 2 * t);
     }
     if (my_tiles > 0) {  // this group's last PV
       mbar_wait(&o_full[w], (my_tiles - 1) & 1);
       tc_fence_after();
     }
+    if (threadIdx.x == 0) ATTN_TRACE(3);
     // ---- epilogue
     float m_fin = m_acc, l_fin = l_acc, f_self = l_acc > 0.f ? 1.f : 0.f, f_other = 0.f;
     int col0 = 0, ncols = HD;
@@ -473,6 +506,7 @@ __global__ void __launch_bounds__(320, 1)
     tc_fence_after();
     tmem_dealloc(tmem, C::kTmemCols);
   }
+  if (threadIdx.x == 0) ATTN_TRACE(4);
 }
 
 // Deterministic split-KV combine: one warp per (query, head), splits in order.
@@ -638,7 +672,7 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
       if (e != cudaSuccess) return cuda_status(e, "attn smem attribute");
       attr = true;
     }
-    kern<<<grid, 320, Cfg<HD, true>::kSmemBytes, stream>>>(mq, mk, mv, prm);
+    kern<<<grid, Cfg<HD, true>::kThreads, Cfg<HD, true>::kSmemBytes, stream>>>(mq, mk, mv, prm);
   } else {
     auto kern = attn_fwd_kernel<HD, false>;
     static bool attr = false;
@@ -648,7 +682,7 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
       if (e != cudaSuccess) return cuda_status(e, "attn smem attribute");
       attr = true;
     }
-    kern<<<grid, 320, Cfg<HD, false>::kSmemBytes, stream>>>(mq, mk, mv, prm);
+    kern<<<grid, Cfg<HD, false>::kThreads, Cfg<HD, false>::kSmemBytes, stream>>>(mq, mk, mv, prm);
   }
   rc = launch_status("attn_fwd launch");
   if (rc || splits == 1) return rc;

@@ -1,0 +1,90 @@
+// In-kernel timeline of the K3 attention kernel: builds attention.cu with
+// ASKV_ATTN_TRACE and prints, per CTA, globaltimer stamps (ns) relative to the
+// earliest CTA start: entry, TMEM ready, Q landed (MMA warp), per-tile
+// S-ready / P-done for softmax WG0, epilogue start, exit.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DASKV_ATTN_TRACE \
+//        -Ipaper_2403_19708_b200/csrc tools/attn_trace.cu -o tools/attn_trace -lcuda
+#include "../paper_2403_19708_b200/csrc/attention.cu"
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <algorithm>
+
+static char g_err[512];
+namespace askv {
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+void clear_error() { g_err[0] = 0; }
+}  // namespace askv
+
+int main(int argc, char** argv) {
+  const int kept = argc > 1 ? atoi(argv[1]) : 2869;
+  const int n = argc > 2 ? atoi(argv[2]) : 301;
+  const int hq = argc > 3 ? atoi(argv[3]) : 40;
+  const int hkv = hq, d = 128;
+  const int rows = kept + n;
+  void *q, *kv, *out, *ws;
+  cudaMalloc(&q, (size_t)n * hq * d * 2);
+  cudaMalloc(&kv, (size_t)rows * 2 * hkv * d * 2);
+  cudaMalloc(&out, (size_t)n * hq * d * 2);
+  cudaMemset(q, 0, (size_t)n * hq * d * 2);
+  cudaMemset(kv, 0, (size_t)rows * 2 * hkv * d * 2);
+  const int splits = askv_attn_num_splits(kept, n, hq, 0);
+  const size_t wsb = askv_attn_workspace_bytes(kept, n, hq, d, splits);
+  cudaMalloc(&ws, wsb + 16);
+  const int ctas = ((n + 127) / 128) * hq * splits;
+  unsigned long long* tr;
+  cudaMalloc(&tr, (size_t)ctas * 64 * 8);
+  cudaMemcpyToSymbol(askv::g_attn_trace, &tr, sizeof(tr));
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaMemset(tr, 0, (size_t)ctas * 64 * 8);
+    int rc = askv_prefill_attn(q, kv, 2LL * hkv * d, kept, n, hq, hkv, d, 0.088f, out, ws, wsb,
+                               splits, nullptr);
+    if (rc) { printf("rc %d %s\n", rc, g_err); return 1; }
+    cudaDeviceSynchronize();
+  }
+  std::vector<unsigned long long> h((size_t)ctas * 64);
+  cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost);
+  unsigned long long t0 = ~0ull, tend = 0;
+  for (int c = 0; c < ctas; ++c) {
+    t0 = std::min(t0, h[c * 64]);
+    tend = std::max(tend, h[c * 64 + 4]);
+  }
+  printf("kept=%d n=%d hq=%d splits=%d ctas=%d span %.2f us\n", kept, n, hq, splits, ctas,
+         (tend - t0) * 1e-3);
+  double s_entry = 0, s_tmem = 0, s_q = 0, s_first = 0, s_loop = 0, s_epi = 0, s_exit = 0;
+  int cnt = 0;
+  for (int c = 0; c < ctas; ++c) {
+    const unsigned long long* r = &h[c * 64];
+    if (!r[3]) continue;
+    ++cnt;
+    s_entry += r[0] - t0;
+    s_tmem += r[1] - r[0];
+    s_q += r[2] - r[1];
+    s_first += r[8] - r[1];
+    int last = 0;
+    for (int t = 0; t < 28; ++t) if (r[9 + 2 * t]) last = t;
+    s_loop += r[9 + 2 * last] - r[8];
+    s_epi += r[3] - r[9 + 2 * last];
+    s_exit += r[4] - r[3];
+  }
+  printf("avg over %d CTAs (us): start offset %.2f | entry->tmem %.2f | tmem->Q %.2f | "
+         "tmem->first S %.2f | WG0 tile loop %.2f | last tile->epilogue %.2f | epilogue->exit %.2f\n",
+         cnt, s_entry / cnt * 1e-3, s_tmem / cnt * 1e-3, s_q / cnt * 1e-3, s_first / cnt * 1e-3,
+         s_loop / cnt * 1e-3, s_epi / cnt * 1e-3, s_exit / cnt * 1e-3);
+  for (int c : {0, ctas / 2, ctas - 1}) {
+    const unsigned long long* r = &h[c * 64];
+    printf("cta %d: entry %.2f tmem %.2f q %.2f |", c, (r[0] - t0) * 1e-3, (r[1] - t0) * 1e-3,
+           (r[2] - t0) * 1e-3);
+    for (int t = 0; t < 28 && r[8 + 2 * t]; ++t)
+      printf(" [%.2f %.2f]", (r[8 + 2 * t] - t0) * 1e-3, (r[9 + 2 * t] - t0) * 1e-3);
+    printf(" | epi %.2f exit %.2f\n", (r[3] - t0) * 1e-3, (r[4] - t0) * 1e-3);
+  }
+  return 0;
+}

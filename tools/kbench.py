@@ -23,6 +23,8 @@ def timeit(fn, reps=20, flush=True):
     for _ in range(reps):
         if flush:
             buf.zero_()
+        else:  # keep the queue busy so e0 does not time the host launch latency
+            torch.cuda._sleep(200000)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         fn()
@@ -50,9 +52,10 @@ def attn(args):
         ws = torch.empty(max(1, ops.attn_workspace_bytes(kept, n, hq, d, s)), dtype=torch.uint8,
                          device="cuda")
         t = timeit(lambda: ops.prefill_attn(q, kv, kept, n, hq, hkv, d, o, ws, num_splits=s),
-                   reps=args.reps)
+                   reps=args.reps, flush=not args.warm)
         fl = attention_flops(kept, n, hq, d)
-        row = dict(kept=kept, n=n, hq=hq, hkv=hkv, splits=s, us=t * 1e6, tflops=fl / t / 1e12)
+        row = dict(kept=kept, n=n, hq=hq, hkv=hkv, splits=s, us=t * 1e6, tflops=fl / t / 1e12,
+                   l2="warm" if args.warm else "flushed")
         out.append(row)
         print(json.dumps(row))
     return out
@@ -103,6 +106,7 @@ if __name__ == "__main__":
     ap.add_argument("--splits", type=int, default=0)
     ap.add_argument("--shape", default="", help="kept,n,hq,hkv")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--warm", action="store_true", help="no L2 flush between reps")
     a = ap.parse_args()
     os.environ["ASKV_ATTN_KERNEL"] = a.kernel
     {"attn": attn, "reembed": reembed, "sweep": sweep}[a.what](a)
