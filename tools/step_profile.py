@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--bg-h2d", action="store_true",
                     help="stream a background pinned H2D copy during the profiled step")
+    ap.add_argument("--no-save", action="store_true", help="jobs without the K4 save")
     a = ap.parse_args()
     import bench
     from paper_2403_19708_b200 import model
@@ -47,7 +48,7 @@ def main():
         if a.mode == "hbm":
             off = torch.as_tensor([b * bb // 2 for b in ids], dtype=torch.int64, device="cuda")
             jobs.append(Job(f"{sid}#{k}", toks.cuda(), kept=kept, source="hbm", block_ids=ids,
-                            save=True, dev_block_off=off))
+                            save=not a.no_save, dev_block_off=off))
         elif a.mode in ("host", "prestage"):
             jobs.append(Job(f"{sid}#{k}", toks.pin_memory(), kept=kept, source="host",
                             block_ids=ids, save=True, prestage=a.mode == "prestage"))
