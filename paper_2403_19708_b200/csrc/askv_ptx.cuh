@@ -293,6 +293,24 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// Packed polynomial exp2 for two lanes: FADD2/FFMA2 on the FMA pipe instead of
+// MUFU (used for a fraction of the softmax elements so MUFU and FMA share the
+// load, as in FA4).  Same range reduction / cubic as ex2_poly.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.0f);
+  x.y = fmaxf(x.y, -126.0f);
+  const float2 magic = make_float2(12582912.0f, 12582912.0f);
+  const float2 t = fadd2(x, magic);
+  const float2 j = fadd2(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = ffma2(j, make_float2(-1.0f, -1.0f), x);
+  float2 p = ffma2(make_float2(0.05508868f, 0.05508868f), f,
+                   make_float2(0.24260405f, 0.24260405f));
+  p = ffma2(p, f, make_float2(0.69327624f, 0.69327624f));
+  p = ffma2(p, f, make_float2(0.99992894f, 0.99992894f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -402,7 +402,10 @@ __global__ void __launch_bounds__(320, 1)
           const int k = c * 32 + e;
           const float2 x = ffma2(make_float2(__uint_as_float(sr[k]), __uint_as_float(sr[k + 1])),
                                  sl2v, negm2);
-          const float2 pp = make_float2(ex2(x.x), ex2(x.y));
+          // a quarter of the exponentials go to the FMA pipe (packed cubic) so
+          // MUFU and FMA share the load; masked tiles keep MUFU (exact zeros)
+          const float2 pp = (!kMask && ((e >> 1) & 3) == 3) ? ex2_poly2(x)
+                                                             : make_float2(ex2(x.x), ex2(x.y));
           switch ((e >> 1) & 3) {
             case 0: ls0 = fadd2(ls0, pp); break;
             case 1: ls1 = fadd2(ls1, pp); break;
