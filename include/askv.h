@@ -231,6 +231,11 @@ typedef struct askv_prefill_plan {
   void* const* ev_attn_end;
   void (*allreduce)(void* ptr, int64_t elems, void* stream, void* ctx);
   void* allreduce_ctx;
+  /* Optional per-layer resident KV (rotated rows [0, kept + n_new) per layer,
+   * row stride 2*Hkv*hd): when set, K2 / rope_new / K3 use kv_layers[l] instead
+   * of the shared `kv` buffer, so the whole context stays resident for decode;
+   * with src_kind 0 and kept > 0 the first `kept` rows are already there. */
+  void* const* kv_layers;
 } askv_prefill_plan;
 
 int askv_prefill_layers(const askv_prefill_plan* plan, void* stream);

@@ -79,6 +79,7 @@ class PrefillPlan(C.Structure):
         ("ev_wait_end", _pp), ("ev_reembed_begin", _pp), ("ev_reembed_end", _pp),
         ("ev_attn_begin", _pp), ("ev_attn_end", _pp),
         ("allreduce", ALLREDUCE_FN), ("allreduce_ctx", C.c_void_p),
+        ("kv_layers", _pp),
     ]
 
 

@@ -173,15 +173,16 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
                "prefill_layers: bad layers=%d n_new=%d kept=%d", p->layers, p->n_new, p->kept);
   ASKV_REQUIRE(p->w_in && p->w_qkv && p->w_o && p->w_post && p->w_gu && p->w_down,
                "prefill_layers: missing weight arrays");
-  ASKV_REQUIRE(p->kept == 0 || (p->src_kind == 1 || p->src_kind == 2) && p->src_layer,
-               "prefill_layers: kept rows need a source");
+  ASKV_REQUIRE(p->kept == 0 || ((p->src_kind == 1 || p->src_kind == 2) && p->src_layer) ||
+                   (p->src_kind == 0 && p->kv_layers),
+               "prefill_layers: kept rows need a source (or resident kv_layers)");
   cudaStream_t s = (cudaStream_t)stream;
   const int n = p->n_new, d = p->d_model, hq = p->n_heads, hkv = p->n_kv_heads,
             hd = p->head_dim, f = p->ffn;
   const int qkv_cols = (hq + 2 * hkv) * hd;
   const int64_t row = 2LL * hkv * hd;
-  auto* kv = static_cast<__nv_bfloat16*>(p->kv);
   for (int l = 0; l < p->layers; ++l) {
+    auto* kv = static_cast<__nv_bfloat16*>(p->kv_layers ? p->kv_layers[l] : p->kv);
     rec(p->ev_layer_begin, l, s);
     ASKV_TRY(askv_rmsnorm(p->x, p->w_in[l], p->h, n, d, p->rms_eps, s));
     ASKV_TRY(gemm(p->h, p->w_qkv[l], p->qkv, n, qkv_cols, d, false, p->gemm_ws,
@@ -191,7 +192,7 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
     ASKV_TRY(askv_rope_new(p->qkv, qkv_cols, n, hq, hkv, hd, p->rope_table, p->rope_positions,
                            p->kept, p->q_rot, kv + (int64_t)p->kept * row, row, save_rows, s));
     if (save_rows) rec(p->ev_save_ready, l, s);
-    if (p->kept > 0) {
+    if (p->kept > 0 && p->src_kind != 0) {
       rec(p->ev_wait_begin, l, s);
       wait(p->ev_src_ready, l, s);
       rec(p->ev_wait_end, l, s);

@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 import torch
 
 from .model import LlamaShape, TierConfig, profile_for
-from .runner import Job, JobResult, LlamaWeights, Runner
+from .runner import Job, JobResult, LlamaWeights, ResidentKv, Runner
 from .store import HitClass, HostArena, KvStore
 
 
@@ -67,6 +67,8 @@ class TurnOutcome:
     result: JobResult                 # last chunk of the input prefill (first-token logits)
     append: JobResult | None          # last chunk of the teacher-forced output append
     results: list = field(default_factory=list)   # every input-prefill chunk (TTFT = sum)
+    decode: list = field(default_factory=list)    # one JobResult per decoded token
+    generated: torch.Tensor | None = None         # decoded token ids (host int64)
 
     def ttft_s(self) -> float:
         """Isolated time to first token: sum of the input chunks' makespans
@@ -211,9 +213,12 @@ class Engine:
         self.tokens[sid] = ids
         return res
 
-    def _prefill(self, sid: str, ids: torch.Tensor, kept: int, want_logits: bool):
+    def _prefill(self, sid: str, ids: torch.Tensor, kept: int, want_logits: bool,
+                 kv_cache: ResidentKv | None = None):
         """Chunked prefill of `ids` after `kept` stored rows, saving every chunk's
         K/V; rolling window truncation before a chunk that would overflow.
+        With `kv_cache` the last chunk leaves every layer's rotated rows resident
+        in it (and reuses them when the cache already holds the kept rows).
         Returns (results, kept_after, rows_dropped)."""
         results, dropped = [], 0
         pos, n = 0, int(ids.numel())
@@ -224,15 +229,23 @@ class Engine:
                 self.store.drop_front_rows(sid, kept - k2)
                 dropped += kept - k2
                 kept = k2
+                if kv_cache is not None:
+                    kv_cache.rows = 0          # positions shifted: re-embed from the store
             tab = self.store.reserve_rows(sid, kept + c)
             job = Job(sid, ids[pos:pos + c], kept=kept, source="host" if kept else "none",
                       block_ids=tab, save=True, head=self.store.head_row(sid))
+            if kv_cache is not None and pos + c == n:
+                job.kv_cache = kv_cache
+                if kept and kv_cache.rows == kept:
+                    job.source = "resident"    # rows already rotated in HBM (decode)
             if self.hbm is not None:
                 resident = sid in self.hbm.valid
                 if self._hbm_sync(sid):
                     hids = list(self.hbm.tab[sid])
                     job.mirror_block_ids = hids
-                    if kept and resident:
+                    if job.source == "resident":
+                        pass
+                    elif kept and resident:
                         job.source = "hbm"        # no host link for this chunk
                         job.dev_block_off = self.hbm.offsets(sid)
                         self.hbm.hits += 1
@@ -302,3 +315,84 @@ class Engine:
         self.store.pinned.discard(sid)
         return TurnOutcome(sid, turn_index, hit.value, kept, hist - kept, new, kept + new,
                            overflowed, results[-1], append, results)
+
+    def generate(self, sid: str, turn_index: int, new_ids: torch.Tensor, steps: int, *,
+                 out_ids: torch.Tensor | None = None, now: float = 0.0,
+                 want_logits: bool = False) -> TurnOutcome:
+        """One turn with a real decode phase: the prompt
+        goes through the reuse prefill, then `steps` tokens are decoded one at a
+        time with every layer's rotated K|V resident in HBM (no re-embed per
+        step); each step's new K|V row is saved to the session's blocks on the
+        save stream while the next step runs — the decode branch of
+        plan_async_save (overlap.py:126-200; sim.py:491-501, 528).  Greedy
+        (argmax, chained on the device) unless `out_ids` teacher-forces the
+        tokens fed at each step.  Store bookkeeping as in `turn` (the outputs
+        are appended to the history, save-time truncation sim.py:576-581)."""
+        if steps < 1:
+            return self.turn(sid, turn_index, new_ids, None, now, want_logits)
+        if out_ids is not None and int(out_ids.numel()) < steps:
+            raise ValueError("out_ids must cover every decode step")
+        cap = self.window + self.chunk
+        if getattr(self, "_kv", None) is None or self._kv.capacity < cap:
+            self._kv = ResidentKv(self.shape, cap, self.runner.device)
+        kv = self._kv
+        kv.rows = 0
+        new_ids = new_ids.reshape(-1).to(torch.int64)
+        hist = self.context.get(sid, 0)
+        new = int(new_ids.numel())
+        overflowed = hist + new > self.window
+        kept = hist
+        if overflowed:
+            kept = overflow_kept(hist, new, self.window, self.cut)
+            if self.store.peek(sid) is not None:
+                if kept == 0:
+                    self.store.remove(sid)
+                else:
+                    self.store.truncate_item(sid, kept, now)
+            self.context[sid] = kept
+            if sid in self.tokens:
+                self.tokens[sid] = self.tokens[sid][hist - kept:]
+        hit = HitClass.MISS
+        if turn_index > 0:
+            hit = self.store.lookup(sid, now)
+            if hit is not HitClass.MISS and self.store.peek(sid).tokens != kept:
+                self.store.remove(sid)
+                hit = HitClass.MISS
+        self.store.pinned.add(sid)
+        hist_ids = self.tokens.get(sid, torch.empty(0, dtype=torch.int64))
+        if hit is HitClass.MISS or kept == 0:
+            hit = HitClass.MISS
+            if self.store.peek(sid) is None:
+                self.store.release_rows(sid)
+            if self.hbm is not None:
+                self.hbm.drop(sid)
+            results, rows, _ = self._prefill(sid, torch.cat([hist_ids, new_ids]), 0,
+                                             want_logits, kv_cache=kv)
+        else:
+            results, rows, _ = self._prefill(sid, new_ids, kept, want_logits, kv_cache=kv)
+        dev = self.runner.device
+        tok = (out_ids.reshape(-1)[:1].to(dev) if out_ids is not None
+               else results[-1].next_token)
+        fed, decode = [], []
+        for s in range(steps):
+            fed.append(tok)
+            res, rows, _ = self._prefill(sid, tok.reshape(1), rows, want_logits, kv_cache=kv)
+            decode.append(res[-1])
+            if s + 1 < steps:
+                tok = (out_ids.reshape(-1)[s + 1:s + 2].to(dev) if out_ids is not None
+                       else res[-1].next_token)
+        gen = torch.cat([t.reshape(1) for t in fed]).cpu()
+        raw = kept + new + steps
+        ctx = save_truncate(raw, self.window, self.cut)
+        if ctx != rows:
+            raise AssertionError(f"rolling window {rows} != save truncation {ctx}")
+        all_ids = torch.cat([hist_ids, new_ids, gen])
+        self.tokens[sid] = all_ids[raw - ctx:]
+        self.context[sid] = ctx
+        if ctx > 0:
+            self.store.save(sid, ctx, now)
+        self._hbm_sync(sid)
+        self.store.pinned.discard(sid)
+        return TurnOutcome(sid, turn_index, hit.value, kept, hist - kept, new, kept + new,
+                           overflowed, results[-1], None, results, decode, gen)
+

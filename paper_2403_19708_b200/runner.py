@@ -138,6 +138,9 @@ class Job:
     promote_block_ids: list | None = None
     head: int = 0   # row of session token 0 inside block_ids[0] (store.head_row)
     prestage: bool = False  # start the job only once all its layers are pre-loaded
+    # resident rotated KV (decode): the job writes all its
+    # layers' rows into kv_cache; source "resident" = kept rows already there
+    kv_cache: "ResidentKv | None" = None
 
     @property
     def n_new(self) -> int:
@@ -158,6 +161,23 @@ class JobResult:
     logits: torch.Tensor | None = None  # (vocab,) fp32 if requested
     bytes_loaded: int = 0
     bytes_saved: int = 0
+    next_token: torch.Tensor | None = None  # (1,) int64 argmax on the device (greedy decode)
+
+
+class ResidentKv:
+    """One session's rotated K|V rows for every layer, kept in HBM across the
+    jobs of a turn (prefill, then one decode step per generated token):
+    [layers][capacity][2][Hkv][hd] bf16.  `rows` = valid rows (positions
+    0..rows-1)."""
+
+    def __init__(self, shape: LlamaShape, capacity: int, device="cuda"):
+        self.capacity = int(capacity)
+        self.buf = torch.empty((shape.layers, self.capacity, shape.row_elems), dtype=BF16,
+                               device=device)
+        self.rows = 0
+
+    def layer_ptrs(self) -> list[int]:
+        return [self.buf[l].data_ptr() for l in range(self.buf.shape[0])]
 
 
 def attention_flops(kept: int, n: int, hq: int, hd: int) -> int:
@@ -503,7 +523,10 @@ class Runner:
             raise ValueError("context exceeds the runner's RoPE table")
         if job.save and len(job.block_ids) * self.block_tokens < job.head + kept + n:
             raise ValueError("save needs block_ids covering kept + new rows")
-        if kept and job.source not in ("host", "hbm"):
+        if job.source == "resident":
+            if job.kv_cache is None or job.kv_cache.rows != kept:
+                raise ValueError("resident job needs kv_cache holding exactly its kept rows")
+        elif kept and job.source not in ("host", "hbm"):
             raise ValueError(f"job with kept={kept} needs a source")
         if kept and job.source == "hbm" and job.dev_block_off is None:
             raise ValueError("hbm job needs dev_block_off")
@@ -567,7 +590,12 @@ class Runner:
             p.h = self._bufs["h"].data_ptr()
             p.qkv = self._buf("qkv", n, s.qkv_cols).data_ptr()
             p.q_rot = self._buf("q", n, hq * hd).data_ptr()
-            p.kv = self._buf("kv", kept + n, self.row_elems).data_ptr()
+            if job.kv_cache is not None:
+                if kept + n > job.kv_cache.capacity:
+                    raise ValueError("context exceeds the resident KV capacity")
+                p.kv_layers = arr(job.kv_cache.layer_ptrs())
+            else:
+                p.kv = self._buf("kv", kept + n, self.row_elems).data_ptr()
             p.attn_out = self._buf("ao", n, hq * hd).data_ptr()
             p.gu = self._buf("gu", n, 2 * s.ffn).data_ptr()
             p.act = self._buf("act", n, s.ffn).data_ptr()
@@ -594,7 +622,7 @@ class Runner:
                 for u in units:
                     if u.times:
                         rec["loads"].append(u.times)
-            elif kept:
+            elif kept and job.source == "hbm":
                 p.src_kind = 2
                 base = self.hbm_arena.data_ptr()
                 p.src_layer = arr([base + l * self.chunk_bytes for l in range(L)])
@@ -614,17 +642,18 @@ class Runner:
                 lb, le = [T() for _ in range(L)], [T() for _ in range(L)]
                 p.ev_layer_begin, p.ev_layer_end = arr(lb), arr(le)
                 rec["layers"] = list(zip(lb, le))
-                if kept:
+                if kept and job.source != "resident":
                     wb, we = [T() for _ in range(L)], [T() for _ in range(L)]
                     p.ev_wait_begin, p.ev_wait_end = arr(wb), arr(we)
                     rec["waits"] = list(zip(wb, we))
             if self.probe is not None:
                 rb, re_, ab, ae = [], [], [], []
+                reemb = kept and job.source != "resident"
                 for _ in range(L):
-                    if kept:
+                    if reemb:
                         self._probe_pair("reembed", 2 * kept * s.row_bytes, rb, re_)
                     self._probe_pair("attention", attention_flops(kept, n, hq, hd), ab, ae)
-                if kept:
+                if reemb:
                     p.ev_reembed_begin, p.ev_reembed_end = arr(rb), arr(re_)
                 p.ev_attn_begin, p.ev_attn_end = arr(ab), arr(ae)
             if self._ar_cb is not None:
@@ -634,7 +663,8 @@ class Runner:
                        "prefill_layers")
             if self._cb_error is not None:
                 raise RuntimeError("tensor-parallel all-reduce failed") from self._cb_error
-            self.launches += L * (4 + (1 if kept else 0) + (2 if splits > 1 else 1)
+            self.launches += L * (4 + (1 if kept and job.source != "resident" else 0)
+                                  + (2 if splits > 1 else 1)
                                   + (2 if self.tp_reduce is not None else 0))
             if units is not None:
                 for u in units:
@@ -655,7 +685,8 @@ class Runner:
                 self._last_save[job.session_id] = (sess_ev, flag)
             hl = ops.rmsnorm(x[-1:], self.w.w_final, 1e-5, stream=cs)
             logits = F.linear(hl, self.w.lm_head).float()
-            ops.copy_sm(first, logits.argmax(dim=-1), stream=cs)
+            nxt = logits.argmax(dim=-1)
+            ops.copy_sm(first, nxt, stream=cs)
             self.launches += 2
             if want_logits:
                 logits_out = logits[0].clone()
@@ -664,7 +695,10 @@ class Runner:
                 t1.record(cs)
         res = JobResult(job.session_id, kept, n, None, first, logits_out,
                         bytes_loaded=kept * s.kv_bytes_per_token if job.source == "host" else 0,
-                        bytes_saved=n * s.kv_bytes_per_token if job.save else 0)
+                        bytes_saved=n * s.kv_bytes_per_token if job.save else 0,
+                        next_token=nxt)
+        if job.kv_cache is not None:
+            job.kv_cache.rows = kept + n
         res._events = (t0, t1, rec, lease) if lease else None
         return res
 

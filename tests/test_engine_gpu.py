@@ -278,3 +278,79 @@ def test_hbm_tier_is_bit_identical_to_host_path():
     assert tier.hbm.hits >= 4 and loaded == 0
     tier.store.check_invariants()
     assert len(tier.hbm.tab["s"]) == len(tier.store.block_table("s"))
+
+
+def test_decode_teacher_forced_matches_oracle():
+    """Decode phase: after the reuse prefill every layer's
+    rotated K|V stays resident and tokens are decoded one at a time, each
+    step's K|V saved asynchronously.  Teacher-forced, every step's logits match
+    the float64 forward of the whole sequence at that position, and the next
+    turn — which re-loads the decode-saved rows from host DRAM — matches too."""
+    engine, model, runner = _mods()
+    shape = model.shape("tiny")
+    eng = engine.Engine(shape, host_blocks=64, block_tokens=16, seed=0, max_new=64,
+                        read_buffer_bytes=64 << 20)
+    wnp = eng.runner.w.to_numpy()
+    rng = np.random.default_rng(5)
+    for k in range(3):
+        new_ids = torch.as_tensor(rng.integers(0, shape.vocab, 20))
+        out_ids = torch.as_tensor(rng.integers(0, shape.vocab, 8))
+        hist_ids = eng.tokens.get("d", torch.empty(0, dtype=torch.int64)).clone()
+        o = eng.generate("d", k, new_ids, 8, out_ids=out_ids, now=float(k), want_logits=True)
+        torch.cuda.synchronize()
+        seq = torch.cat([hist_ids, new_ids]).numpy()
+        got = o.result.logits.cpu().numpy().astype(np.float64)
+        assert rope_ref.rel_err(got, oracle_logits(wnp, shape, seq)) <= LOGIT_TOL, k
+        assert len(o.decode) == 8 and torch.equal(o.generated, out_ids)
+        for s in range(8):
+            seq_s = np.concatenate([seq, out_ids[: s + 1].numpy()])
+            got = o.decode[s].logits.cpu().numpy().astype(np.float64)
+            assert rope_ref.rel_err(got, oracle_logits(wnp, shape, seq_s)) <= LOGIT_TOL, (k, s)
+        assert eng.context["d"] == len(seq) + 8
+        if k > 0:
+            assert o.hit == "memory_hit"
+    eng.store.check_invariants()
+
+
+def test_decode_greedy_is_deterministic_and_follows_argmax():
+    """Greedy decode chains the argmax on the device; two identical engines
+    produce the same tokens, and each token is the argmax of the oracle's
+    logits wherever the top-2 margin is clear of bf16 noise."""
+    engine, model, runner = _mods()
+    shape = model.shape("tiny")
+    gens = []
+    for _ in range(2):
+        eng = engine.Engine(shape, host_blocks=64, block_tokens=16, seed=3, max_new=64,
+                            read_buffer_bytes=64 << 20)
+        ids = torch.as_tensor(np.random.default_rng(7).integers(0, shape.vocab, 30))
+        o = eng.generate("g", 0, ids, 6, want_logits=True)
+        torch.cuda.synchronize()
+        gens.append(o.generated)
+    assert torch.equal(gens[0], gens[1])
+    wnp = eng.runner.w.to_numpy()
+    seq = ids.numpy()
+    for s in range(6):
+        want = oracle_logits(wnp, shape, np.concatenate([seq, gens[0][:s].numpy()]))
+        top2 = np.sort(want)[-2:]
+        if top2[1] - top2[0] > 0.05:
+            assert int(gens[0][s]) == int(np.argmax(want)), s
+
+
+def test_decode_across_window_truncation():
+    """Decoding past the window truncates like the reference (keep the most
+    recent rows, sim.py:468-483): the resident cache is invalidated and the
+    next step re-embeds the kept rows from the store; the context and the store
+    stay consistent with save-time truncation (sim.py:576-581)."""
+    engine, model, runner = _mods()
+    from dataclasses import replace
+    shape = replace(model.shape("tiny"), context_window=64)
+    eng = engine.Engine(shape, host_blocks=64, block_tokens=16, seed=2, max_new=64,
+                        read_buffer_bytes=32 << 20)
+    rng = np.random.default_rng(2)
+    o = eng.generate("w", 0, torch.as_tensor(rng.integers(0, shape.vocab, 50)), 30,
+                     want_logits=True)
+    torch.cuda.synchronize()
+    assert len(o.decode) == 30
+    assert all(np.isfinite(r.logits.cpu().numpy()).all() for r in o.decode)
+    assert eng.context["w"] == engine.save_truncate(80, 64, 32)
+    eng.store.check_invariants()
