@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--turns", type=int, default=16, help="hit turns per GPU per step")
     ap.add_argument("--block-tokens", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--decode-steps", type=int, default=32,
+                    help="greedy decode steps measured after the prefill legs (0 = skip)")
     ap.add_argument("--profile-attn", action="store_true",
                     help="run only a few hbm steps (for ncu captures)")
     return ap.parse_args()
@@ -287,7 +289,11 @@ def main():
     tb = args.block_tokens
     block_bytes = tb * shape.kv_bytes_per_token
     nbs = [-(-(kept + new) // tb) for _, _, kept, new in turns]
-    n_blocks = sum(nbs)
+    dec_steps = args.decode_steps
+    # decode probe (§8f-2): the first sampled turn gets its own blocks with room
+    # for the decoded tokens
+    dec_nb = -(-(turns[0][2] + turns[0][3] + dec_steps) // tb) if dec_steps else 0
+    n_blocks = sum(nbs) + dec_nb
     max_new = max(new for *_, new in turns)
     max_kept = max(kept for *_, kept, _ in turns)
     # arenas: the same block ids in the pinned host arena and the HBM arena
@@ -326,6 +332,7 @@ def main():
         jobs["hbm"].append(Job(sid, new_ids.to(dev), kept=kept, source="hbm", block_ids=bids,
                                save=True, dev_block_off=off))
         jobs["recompute"].append(Job(sid, prompt_ids.to(dev)))
+    dec_bids = [int(b) for b in ids_perm[pos:pos + dec_nb]]
     prompt_tokens = sum(kept + new for *_, kept, new in turns)
     new_tokens = sum(new for *_, new in turns)
 
@@ -389,6 +396,48 @@ def main():
     _, res_pre, _, _ = timed("host", 1, 1)
     for j in jobs["host"]:
         j.prestage = False
+
+    decode = None
+    if dec_steps:
+        from paper_2403_19708_b200.runner import ResidentKv
+        _, _, d_kept, d_new = turns[0]
+        kvres = ResidentKv(shape, d_kept + d_new + dec_steps, dev)
+        d_ids = torch.as_tensor(trng.integers(0, shape.vocab, d_new)).pin_memory()
+
+        def decode_turn():
+            # prompt from host DRAM into the resident cache, then greedy steps;
+            # every step's K|V row is saved to host DRAM on the save stream
+            kvres.rows = 0
+            r0 = runner.run([Job("decode", d_ids, kept=d_kept, source="host", block_ids=dec_bids,
+                                 save=True, kv_cache=kvres)])[0]
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(runner.s_compute)
+            tok, steps_res = r0.next_token, []
+            for s in range(dec_steps):
+                r = runner.run([Job("decode", tok, kept=d_kept + d_new + s, source="resident",
+                                    block_ids=dec_bids, save=True, kv_cache=kvres)])[0]
+                steps_res.append(r)
+                tok = r.next_token
+            e1.record(runner.s_compute)
+            runner.join()
+            torch.cuda.synchronize()
+            Runner.finalize([r0] + steps_res)
+            return e0.elapsed_time(e1), steps_res
+
+        decode_turn()  # warm-up
+        d_ms, d_res = decode_turn()
+        spans = [r.timeline.makespan for r in d_res]
+        saves = [b - a for r in d_res for a, b in r.timeline.save_intervals]
+        decode = {"steps": dec_steps, "context": d_kept + d_new,
+                  "tpot_ms": d_ms / dec_steps,
+                  "tpot_makespan_p50_ms": percentile(spans, 0.5) * 1e3,
+                  "tokens_per_s": dec_steps / (d_ms * 1e-3),
+                  "d2h_bytes_per_token": shape.kv_bytes_per_token,
+                  "save_busy_ms_per_token": sum(saves) / dec_steps * 1e3,
+                  "note": "batch-1 greedy decode with every layer's rotated KV resident in "
+                          "HBM; per-token K|V saved to pinned host DRAM asynchronously "
+                          "(overlap.py:126-200 decode branch); weight-bandwidth bound"}
 
     steps_re = max(2, args.steps // 2)
     t_host = max_over_ranks(ms_host) * 1e-3
@@ -493,6 +542,7 @@ def main():
         "roofline_reembed": {"kernel": "askv_reembed (K2)", "bound": "hbm",
                              "achieved": emb_gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": emb_gbs / hbm_peak},
+        "decode": decode,
         "gpu_launches": launches,
         "clocks": clocks,
         "cpu_baseline": cpu,
