@@ -23,7 +23,7 @@ import torch
 
 from .model import LlamaShape, TierConfig, profile_for
 from .runner import Job, JobResult, LlamaWeights, ResidentKv, Runner
-from .store import HitClass, HostArena, KvStore
+from .store import CapacityError, HitClass, HostArena, KvStore, Tier
 
 
 def overflow_kept(hist: int, new: int, window: int, cut: int) -> int:
@@ -154,16 +154,24 @@ class Engine:
                  device="cuda", seed: int = 0, weights: LlamaWeights | None = None,
                  read_buffer_bytes: int = 1 << 30, max_new: int = 1024,
                  truncation_ratio: float = 0.5, ttl: float = math.inf, pin: bool = True,
-                 tp_reduce=None, hbm_blocks: int = 0):
+                 tp_reduce=None, hbm_blocks: int = 0, disk_dir: str | None = None,
+                 disk_blocks: int = 0):
         self.shape = shape
         self.profile = profile_for(shape, truncation_ratio=truncation_ratio)
         self.block_tokens = block_tokens
         block_bytes = block_tokens * shape.kv_bytes_per_token
         self.arena = HostArena(host_blocks, block_bytes, pin=pin)
-        tiers = TierConfig(dram_capacity=host_blocks * block_bytes, disk_capacity=0)
+        disk = None
+        if disk_dir is not None and disk_blocks > 0:
+            from .disk import DiskTier
+            disk = DiskTier(disk_dir, block_bytes)
+        tiers = TierConfig(dram_capacity=host_blocks * block_bytes,
+                           disk_capacity=disk_blocks * block_bytes if disk else 0)
         self.store = KvStore(self.profile, tiers, block_bytes=block_bytes, ttl=ttl,
                              evictor=self._make_room, arena=self.arena,
-                             block_tokens=block_tokens)
+                             block_tokens=block_tokens, disk=disk)
+        self.disk_evictions = 0
+        self.disk_promotions = 0
         self.window = shape.context_window
         self.cut = self.profile.cut_tokens
         self.chunk = max(1, min(max_new, self.cut))
@@ -177,17 +185,85 @@ class Engine:
         self.tokens: dict[str, torch.Tensor] = {}   # conversation token ids (for misses)
 
     def _make_room(self, needed: float) -> None:
-        """Evict least-recently-used unpinned sessions (no disk tier here)."""
+        """Free DRAM by least-recently-used unpinned sessions: demoted to the
+        disk tier when there is one (making disk room by evicting its LRU items
+        out), else evicted out (sim.py:300-327 with the LRU baseline policy)."""
         freed = 0.0
         for it in sorted(self.store.memory_items(), key=lambda i: (i.last_access, i.seq)):
             if freed >= needed:
                 break
-            if it.session_id in self.store.pinned:
+            sid = it.session_id
+            if sid in self.store.pinned:
                 continue
-            freed += self.store.charge(it.bytes)
-            self.store.remove(it.session_id)
+            blocks = self.store.charge(it.bytes)
+            freed += blocks
             if self.hbm is not None:
-                self.hbm.drop(it.session_id)
+                self.hbm.drop(sid)
+            if self.store.disk is not None and blocks <= self.store.disk_capacity:
+                for old in sorted(self.store.disk_items(), key=lambda i: (i.last_access, i.seq)):
+                    if self.store.disk_free >= blocks:
+                        break
+                    self.store.remove(old.session_id)
+                self.store.move(sid, Tier.DISK)
+                self.disk_evictions += 1
+            else:
+                self.store.remove(sid)
+
+    def _ensure_arena(self, sid: str, rows: int) -> None:
+        """Physical room for the session's rows before the saver writes them
+        (the accounting follows at save()): demote / evict LRU sessions."""
+        st = self.store
+        need = -(-(st.head_row(sid) + rows) // self.block_tokens) - len(st.tables.get(sid, ()))
+        while st.arena.free_blocks < need:
+            before = st.arena.free_blocks
+            self._make_room((need - before) * st.block_bytes)
+            if st.arena.free_blocks == before:
+                raise CapacityError(f"host arena full: {need} blocks for {sid}")
+
+    def _admit(self, sid: str, turn_index: int, kept: int, now: float) -> HitClass:
+        """Store lookup at job start (sim.py:419-431).  A disk hit is promoted
+        to DRAM first (read from its file into arena blocks, unless a prefetch
+        already brought it in); the turn then takes the normal pre-load path."""
+        hit = HitClass.MISS
+        if turn_index > 0:
+            hit = self.store.lookup(sid, now)
+            if hit is not HitClass.MISS and self.store.peek(sid).tokens != kept:
+                self.store.remove(sid)
+                hit = HitClass.MISS
+        self.store.pinned.add(sid)
+        if hit is HitClass.DISK_HIT and self.store.disk is not None:
+            self._promote(sid, wait=True)
+        elif sid in self.store.pending:
+            self.store.wait(sid)
+        return hit
+
+    def _promote(self, sid: str, wait: bool) -> None:
+        it = self.store.peek(sid)
+        blocks = self.store.charge(it.bytes)
+        target = blocks + self.store.mem_buffer_reserve
+        if self.store.mem_free < target:
+            self._make_room(target - self.store.mem_free)
+        self.store.move(sid, Tier.MEMORY, wait=wait)
+        self.disk_promotions += 1
+
+    def prefetch(self, sids) -> list[str]:
+        """Scheduler-aware prefetch (policy.py:122-150, sim.py:329-366): start
+        disk -> DRAM reads for the sessions of upcoming jobs; the reads run on
+        the disk IO threads while the current prefill proceeds."""
+        started = []
+        for sid in sids:
+            it = self.store.peek(sid)
+            if it is None or it.tier is not Tier.DISK or self.store.disk is None:
+                continue
+            self.store.pinned.add(sid)       # not a victim of its own room-making
+            try:
+                self._promote(sid, wait=False)
+                started.append(sid)
+            except CapacityError:
+                pass
+            finally:
+                self.store.pinned.discard(sid)
+        return started
 
     def _hbm_sync(self, sid: str) -> bool:
         if self.hbm is None:
@@ -231,6 +307,7 @@ class Engine:
                 kept = k2
                 if kv_cache is not None:
                     kv_cache.rows = 0          # positions shifted: re-embed from the store
+            self._ensure_arena(sid, kept + c)
             tab = self.store.reserve_rows(sid, kept + c)
             job = Job(sid, ids[pos:pos + c], kept=kept, source="host" if kept else "none",
                       block_ids=tab, save=True, head=self.store.head_row(sid))
@@ -278,13 +355,7 @@ class Engine:
             self.context[sid] = kept
             if sid in self.tokens:
                 self.tokens[sid] = self.tokens[sid][hist - kept:]
-        hit = HitClass.MISS
-        if turn_index > 0:
-            hit = self.store.lookup(sid, now)
-            if hit is not HitClass.MISS and self.store.peek(sid).tokens != kept:
-                self.store.remove(sid)
-                hit = HitClass.MISS
-        self.store.pinned.add(sid)
+        hit = self._admit(sid, turn_index, kept, now)
         hist_ids = self.tokens.get(sid, torch.empty(0, dtype=torch.int64))
         if hit is HitClass.MISS or kept == 0:
             hit = HitClass.MISS
@@ -352,13 +423,7 @@ class Engine:
             self.context[sid] = kept
             if sid in self.tokens:
                 self.tokens[sid] = self.tokens[sid][hist - kept:]
-        hit = HitClass.MISS
-        if turn_index > 0:
-            hit = self.store.lookup(sid, now)
-            if hit is not HitClass.MISS and self.store.peek(sid).tokens != kept:
-                self.store.remove(sid)
-                hit = HitClass.MISS
-        self.store.pinned.add(sid)
+        hit = self._admit(sid, turn_index, kept, now)
         hist_ids = self.tokens.get(sid, torch.empty(0, dtype=torch.int64))
         if hit is HitClass.MISS or kept == 0:
             hit = HitClass.MISS

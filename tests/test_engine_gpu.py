@@ -354,3 +354,34 @@ def test_decode_across_window_truncation():
     assert all(np.isfinite(r.logits.cpu().numpy()).all() for r in o.decode)
     assert eng.context["w"] == engine.save_truncate(80, 64, 32)
     eng.store.check_invariants()
+
+
+def test_disk_tier_turns_are_bit_identical(tmp_path):
+    """with DRAM for only a couple of sessions, LRU
+    sessions are demoted to the disk tier (their blocks written to files and
+    freed) and promoted back on their next turn (disk hit).  The data path is
+    byte-exact, so every turn's logits equal those of an engine whose DRAM
+    holds everything."""
+    engine, model, runner = _mods()
+    wl = json.loads((G / "workload_c1.json").read_text())
+    shape = model.shape("tiny")
+    kw = dict(block_tokens=16, seed=0, max_new=64, read_buffer_bytes=64 << 20)
+    big = engine.Engine(shape, host_blocks=64, **kw)
+    small = engine.Engine(shape, host_blocks=12, disk_dir=str(tmp_path / "kv"),
+                          disk_blocks=64, **kw)
+    rng = np.random.default_rng(0)
+    hits = []
+    for k in range(3):
+        for s in wl["sessions"]:
+            new, out = s["turns"][k]
+            new_ids = torch.as_tensor(rng.integers(0, shape.vocab, new))
+            out_ids = torch.as_tensor(rng.integers(0, shape.vocab, out))
+            a = big.turn(s["id"], k, new_ids, out_ids, now=float(k), want_logits=True)
+            b = small.turn(s["id"], k, new_ids, out_ids, now=float(k), want_logits=True)
+            torch.cuda.synchronize()
+            assert torch.equal(a.result.logits, b.result.logits), (s["id"], k)
+            hits.append(b.hit)
+            small.store.check_invariants()
+    assert "disk_hit" in hits
+    assert small.disk_evictions > 0 and small.disk_promotions > 0
+    assert small.store.disk.bytes_read > 0 and small.store.disk.bytes_written > 0

@@ -150,3 +150,74 @@ def test_rolling_window_chunks_equal_save_truncation(kept, sizes, w):
     kept = min(kept, w)
     assert rolling_kept(kept, sizes, w, cut) == layout_ref.save_truncate(kept + sum(sizes), w,
                                                                           0.5)
+
+
+def _disk_store(tmp_path, blocks=16, tb=16, kvb=1024, disk_blocks=64):
+    from paper_2403_19708_b200.disk import DiskTier
+    prof = model.ModelProfile(name="p", kv_bytes_per_token=float(kvb),
+                              prefill_seconds_per_token=1e-4, decode_seconds_per_step=1e-3,
+                              context_window=4096, layers=2)
+    bb = tb * kvb
+    arena = HostArena(blocks, bb, pin=False)
+    disk = DiskTier(str(tmp_path / "kv"), bb, io_threads=4, chunk_bytes=4096)
+    stor = KvStore(prof, model.TierConfig(dram_capacity=blocks * bb, disk_capacity=disk_blocks * bb),
+                   block_bytes=bb, arena=arena, block_tokens=tb, disk=disk)
+    return stor, arena, disk
+
+
+def _fill(stor, arena, sid, rows, seed):
+    tab = stor.reserve_rows(sid, rows)
+    stor.mark_written(sid, rows)
+    buf = arena.buffer.numpy()
+    rng = np.random.default_rng(seed)
+    for b in tab:
+        buf[b * arena.block_bytes:(b + 1) * arena.block_bytes] = rng.integers(
+            0, 256, arena.block_bytes, dtype=np.uint8)
+    return [bytes(buf[b * arena.block_bytes:(b + 1) * arena.block_bytes]) for b in tab]
+
+
+def test_disk_tier_round_trip_is_bit_exact(tmp_path):
+    """move(sid, DISK) writes the session's blocks to its file and frees them
+    from the arena; move(sid, MEMORY) reads them back into fresh blocks, bytes
+    identical.  Accounting stays the reference's."""
+    stor, arena, disk = _disk_store(tmp_path)
+    want = _fill(stor, arena, "a", 70, 0)            # 5 blocks of 16 rows
+    stor.save("a", 70, 0.0)
+    free0 = arena.free_blocks
+    moved = stor.move("a", Tier.DISK)
+    assert moved == stor.peek("a").bytes and stor.peek("a").tier is Tier.DISK
+    assert arena.free_blocks == free0 + 5 and stor.block_table("a") == []
+    assert (tmp_path / "kv").exists() and disk.bytes_written == 5 * arena.block_bytes
+    stor.check_invariants()
+    assert stor.lookup("a", 1.0) is HitClass.DISK_HIT
+    _fill(stor, arena, "b", 64, 1)                    # reuse the freed blocks meanwhile
+    stor.save("b", 64, 1.0)
+    stor.move("a", Tier.MEMORY, wait=False)           # async prefetch
+    stor.wait("a")
+    buf = arena.buffer.numpy()
+    got = [bytes(buf[b * arena.block_bytes:(b + 1) * arena.block_bytes])
+           for b in stor.block_table("a")]
+    assert got == want and not stor.on_disk("a")
+    stor.check_invariants()
+
+
+def test_disk_tier_truncation_and_remove(tmp_path):
+    """Truncating an item while it sits on disk is a file front-offset edit;
+    after promotion the table holds exactly the kept suffix's blocks."""
+    stor, arena, disk = _disk_store(tmp_path)
+    want = _fill(stor, arena, "t", 80, 2)             # 5 blocks
+    stor.save("t", 80, 0.0)
+    stor.move("t", Tier.DISK)
+    stor.truncate_item("t", 40, 1.0)                  # drop 40 rows = 2 whole blocks + 8
+    assert disk.meta["t"].nblocks == 3 and disk.meta["t"].head == 8
+    stor.check_invariants()
+    stor.move("t", Tier.MEMORY)
+    buf = arena.buffer.numpy()
+    got = [bytes(buf[b * arena.block_bytes:(b + 1) * arena.block_bytes])
+           for b in stor.block_table("t")]
+    assert got == want[2:] and stor.head_row("t") == 8
+    stor.move("t", Tier.DISK)
+    path = disk.path("t")
+    stor.remove("t")
+    assert not Path(path).exists() and "t" not in disk.meta
+    stor.check_invariants()
