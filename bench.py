@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--turns", type=int, default=16, help="hit turns per GPU per step")
     ap.add_argument("--block-tokens", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--disk-dir", default="/tmp",
+                    help="directory for the disk-tier probe ('none' = skip)")
     ap.add_argument("--decode-steps", type=int, default=32,
                     help="greedy decode steps measured after the prefill legs (0 = skip)")
     ap.add_argument("--profile-attn", action="store_true",
@@ -244,6 +246,44 @@ def run_reference(args, shape, turns):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+
+def disk_probe(root, arena, bids, block_bytes, rows):
+    """Disk tier (§8f-4): write one session's blocks from the pinned arena to
+    a file and read them back (IO-thread pool, O_DIRECT when the file system
+    allows); GB/s of each direction on this box's disk."""
+    import shutil
+    import tempfile
+    from paper_2403_19708_b200.disk import DiskTier
+    d = tempfile.mkdtemp(prefix="askv-disk-", dir=root)
+    fs = "?"
+    try:
+        best = ""
+        for line in open("/proc/mounts"):
+            parts = line.split()
+            if len(parts) > 2 and d.startswith(parts[1]) and len(parts[1]) > len(best):
+                best, fs = parts[1], parts[2]
+    except OSError:
+        pass
+    tier = DiskTier(d, block_bytes)
+    try:
+        nbytes = len(bids) * block_bytes
+        t0 = time.perf_counter()
+        tier.write("probe", arena, bids, 0, rows, 0).result()
+        os.sync()
+        t_w = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        tier.read("probe", arena, bids).result()
+        t_r = time.perf_counter() - t0
+        direct = tier.direct
+    finally:
+        tier.close()
+        shutil.rmtree(d, ignore_errors=True)
+    return {"session_bytes": nbytes, "write_gbs": nbytes / t_w / 1e9,
+            "read_gbs": nbytes / t_r / 1e9, "read_s": t_r, "fs": fs,
+            "o_direct_requested": direct,
+            "note": "one C3 session's blocks, pinned DRAM <-> file; a disk hit adds read_s "
+                    "before the layer-wise pre-load"}
+
 
 def main():
     args = parse()
@@ -439,6 +479,11 @@ def main():
                           "HBM; per-token K|V saved to pinned host DRAM asynchronously "
                           "(overlap.py:126-200 decode branch); weight-bandwidth bound"}
 
+    disk = None
+    if args.disk_dir != "none" and rank == 0:
+        disk = disk_probe(args.disk_dir, arena, [int(b) for b in ids_perm[:nbs[0]]],
+                          block_bytes, turns[0][2] + turns[0][3])
+
     steps_re = max(2, args.steps // 2)
     t_host = max_over_ranks(ms_host) * 1e-3
     t_hbm = max_over_ranks(ms_hbm) * 1e-3
@@ -543,6 +588,7 @@ def main():
                              "achieved": emb_gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": emb_gbs / hbm_peak},
         "decode": decode,
+        "disk": disk,
         "gpu_launches": launches,
         "clocks": clocks,
         "cpu_baseline": cpu,
