@@ -17,6 +17,7 @@ the next turn finds a complete history (SURVEY.md §7.2 "Output tokens' KV").
 from __future__ import annotations
 
 import math
+import time
 from dataclasses import dataclass, field
 
 import torch
@@ -172,6 +173,8 @@ class Engine:
                              block_tokens=block_tokens, disk=disk)
         self.disk_evictions = 0
         self.disk_promotions = 0
+        self.last_disk_wait_s = 0.0
+        self.prefetched: set[str] = set()
         self.window = shape.context_window
         self.cut = self.profile.cut_tokens
         self.chunk = max(1, min(max_new, self.cut))
@@ -189,7 +192,11 @@ class Engine:
         disk tier when there is one (making disk room by evicting its LRU items
         out), else evicted out (sim.py:300-327 with the LRU baseline policy)."""
         freed = 0.0
-        for it in sorted(self.store.memory_items(), key=lambda i: (i.last_access, i.seq)):
+        # sessions prefetched for upcoming jobs go last (scheduler-aware eviction,
+        # policy.py select_evict_to_disk avoids the queue window)
+        order = sorted(self.store.memory_items(),
+                       key=lambda i: (i.session_id in self.prefetched, i.last_access, i.seq))
+        for it in order:
             if freed >= needed:
                 break
             sid = it.session_id
@@ -231,10 +238,13 @@ class Engine:
                 self.store.remove(sid)
                 hit = HitClass.MISS
         self.store.pinned.add(sid)
+        self.prefetched.discard(sid)
+        t0 = time.perf_counter()
         if hit is HitClass.DISK_HIT and self.store.disk is not None:
             self._promote(sid, wait=True)
         elif sid in self.store.pending:
-            self.store.wait(sid)
+            self.store.wait(sid)      # prefetched: only the rest of the read is exposed
+        self.last_disk_wait_s = time.perf_counter() - t0
         return hit
 
     def _promote(self, sid: str, wait: bool) -> None:
@@ -258,6 +268,7 @@ class Engine:
             self.store.pinned.add(sid)       # not a victim of its own room-making
             try:
                 self._promote(sid, wait=False)
+                self.prefetched.add(sid)
                 started.append(sid)
             except CapacityError:
                 pass

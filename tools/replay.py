@@ -44,6 +44,12 @@ def main():
     ap.add_argument("--host-gb", type=float, default=120.0)
     ap.add_argument("--hbm-gb", type=float, default=0.0,
                     help="HBM session tier capacity (SURVEY.md §8f item 1); 0 = DRAM only")
+    ap.add_argument("--disk-gb", type=float, default=0.0,
+                    help="disk tier capacity (SURVEY.md §8f item 4); 0 = no disk tier")
+    ap.add_argument("--disk-dir", default="/tmp/askv-replay-disk")
+    ap.add_argument("--prefetch", type=int, default=0,
+                    help="scheduler-aware prefetch window: disk->DRAM reads for the "
+                         "sessions of the next N turns (policy.py:122-150)")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     from paper_2403_19708_b200 import engine, metrics, model
@@ -59,20 +65,30 @@ def main():
     weights = LlamaWeights(shape, seed=0)
     eng = engine.Engine(shape, host_blocks=host_blocks, block_tokens=tb, weights=weights,
                         max_new=2048, read_buffer_bytes=4 << 30,
-                        hbm_blocks=int(a.hbm_gb * 1e9 // block_bytes))
+                        hbm_blocks=int(a.hbm_gb * 1e9 // block_bytes),
+                        disk_dir=a.disk_dir if a.disk_gb else None,
+                        disk_blocks=int(a.disk_gb * 1e9 // block_bytes))
     turns = sorted(((s["arrivals"][k], s["id"], k, s["turns"][k][0], s["turns"][k][1])
                     for s in sessions for k in range(len(s["turns"]))))
     rng = np.random.default_rng(0)
     recs = []
     t_wall = time.time()
-    for arr, sid, k, new, out in turns:
+    for i, (arr, sid, k, new, out) in enumerate(turns):
         ids = torch.as_tensor(rng.integers(0, shape.vocab, new)).pin_memory()
         oids = torch.as_tensor(rng.integers(0, shape.vocab, out)) if out else None
+        if a.prefetch and eng.store.disk is not None:
+            ahead = [t[1] for t in turns[i + 1:i + 1 + a.prefetch] if t[1] != sid]
+            eng.store.pinned.add(sid)
+            eng.prefetch(ahead)
+            eng.store.pinned.discard(sid)
         o = eng.turn(sid, k, ids, oids, now=arr)
         torch.cuda.synchronize()
         eng.runner.finalize(o.results)
+        # a disk hit's read (or the unfinished part of its prefetch) precedes the
+        # layer-wise pre-load: it is part of the prefill service time
         recs.append(dict(arrival=arr, session=sid, turn=k, hit=o.hit, kept=o.kept, new=new,
-                         prompt=o.prompt, makespan=o.ttft_s(),
+                         prompt=o.prompt, makespan=o.ttft_s() + eng.last_disk_wait_s,
+                         disk_wait=eng.last_disk_wait_s,
                          stall=sum(r.timeline.stall_total for r in o.results)))
     reuse_wall = time.time() - t_wall
     # recompute mode: the same prompts, whole prompt prefilled, no store
@@ -112,6 +128,14 @@ def main():
                   "arena_blocks": host_blocks},
         "hbm_tier": ({"gb": a.hbm_gb, "hits": eng.hbm.hits, "promotions": eng.hbm.promotions}
                      if eng.hbm else None),
+        "disk_tier": ({"gb": a.disk_gb, "prefetch_window": a.prefetch,
+                       "disk_hits": sum(r["hit"] == "disk_hit" for r in recs),
+                       "evictions_to_disk": eng.disk_evictions,
+                       "promotions": eng.disk_promotions,
+                       "read_gb": eng.store.disk.bytes_read / 1e9,
+                       "write_gb": eng.store.disk.bytes_written / 1e9,
+                       "exposed_disk_wait_s": float(sum(r["disk_wait"] for r in recs))}
+                      if eng.store.disk else None),
         "wall_s_reuse_replay": reuse_wall,
         "note": "TTFT = FIFO serial-prefill queue on measured makespans at the workload's "
                 "arrival times (no read-buffer head start: the load starts with the job)",
