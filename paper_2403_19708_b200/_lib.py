@@ -91,6 +91,24 @@ class AskvError(RuntimeError):
     pass
 
 
+def _preload_torch_cublaslt() -> None:
+    """libaskv.so needs libcublasLt.so.12.  torch ships its own copy (pip
+    nvidia-cublas); if ours (the CUDA toolkit's) were loaded first, torch's
+    libcublas would bind to a mismatched cuBLASLt and fail (CUBLAS_STATUS_
+    INVALID_VALUE).  Load torch's copy first, globally, so one cuBLASLt serves
+    both."""
+    try:
+        import nvidia.cublas as nc
+    except ImportError:
+        return
+    import os
+    for base in nc.__path__:
+        path = os.path.join(base, "lib", "libcublasLt.so.12")
+        if os.path.exists(path):
+            C.CDLL(path, mode=C.RTLD_GLOBAL)
+            return
+
+
 def lib():
     """Load libaskv.so once; raise loudly if it is absent."""
     global _lib
@@ -102,6 +120,7 @@ def lib():
                 raise AskvError(
                     f"{LIB_PATH} is not built; run `python -m paper_2403_19708_b200.build` "
                     "(there is no non-CUDA fallback)")
+            _preload_torch_cublaslt()
             handle = C.CDLL(str(LIB_PATH))
             for name, (res, args) in SIGNATURES.items():
                 fn = getattr(handle, name)
