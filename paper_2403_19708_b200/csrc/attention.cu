@@ -597,15 +597,29 @@ int sm_count() {
   return n;
 }
 
+// Pair two query tiles per CTA (M = 256 per K/V tile: half the K/V fill bytes
+// per FLOP, the per-SM L2->SMEM fill rate being what bounds K3) only when one
+// tile per CTA would need more than one wave of SMs; below that, pairing halves
+// the CTA count and loses more than it saves (profiles/r01b_summary.md).
+// ASKV_ATTN_PAIR=0/1 forces it off/on.
+bool use_pairs(int q_tiles, int hq, int sms) {
+  static int knob = -2;
+  if (knob == -2) {
+    const char* e = getenv("ASKV_ATTN_PAIR");
+    knob = (e && e[0] == '1') ? 1 : (e && e[0] == '0') ? 0 : -1;
+  }
+  if (q_tiles < 2) return false;
+  if (knob >= 0) return knob == 1;
+  return q_tiles * hq > sms;
+}
+
 // Split count minimising waves x (tiles per split + fixed per-CTA overhead).
 // Split-KV policy, fitted to a B200 sweep (tools/kbench.py sweep): one CTA per
 // SM at most (one wave), and at least 4 KV tiles per split so the per-CTA
 // prologue / epilogue and the combine pass stay amortised.
 int choose_splits(int n_cached, int n_new, int hq, int sms) {
   const int q_tiles = (n_new + kBM - 1) / kBM;
-  const char* pk = getenv("ASKV_ATTN_PAIR");
-  const bool pair = pk && pk[0] == '1';
-  const int q_groups = (pair && q_tiles >= 2) ? (q_tiles + 1) / 2 : q_tiles;
+  const int q_groups = use_pairs(q_tiles, hq, sms) ? (q_tiles + 1) / 2 : q_tiles;
   const int kv_tiles = (n_cached + n_new + kBN - 1) / kBN;
   const int ctas = q_groups * hq;
   int best = 1;
@@ -631,16 +645,7 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
   if (rc) return rc;
 
   const int q_tiles = (n_new + kBM - 1) / kBM;
-  // Pairing two query tiles per CTA (ASKV_ATTN_PAIR=1) halves L2->SM bytes per
-  // FLOP but halves the CTA count and loses the alternate-tile ping-pong; on
-  // B200 at the path's shapes it measured slower (profiles/r01_attn_experiments.md),
-  // so the default is one query tile per CTA.
-  static int pair_knob = -1;
-  if (pair_knob < 0) {
-    const char* e = getenv("ASKV_ATTN_PAIR");
-    pair_knob = (e && e[0] == '1') ? 1 : 0;
-  }
-  const bool paired = pair_knob && q_tiles >= 2;
+  const bool paired = use_pairs(q_tiles, hq, sm_count());
   const int q_groups = paired ? (q_tiles + 1) / 2 : q_tiles;
   const int kv_tiles = (rows + kBN - 1) / kBN;
   const int tps = (kv_tiles + splits - 1) / splits;

@@ -156,6 +156,10 @@ ATTN_CASES = [
     (4000, 96, 2, 2, 128, 7),
     (0, 1100, 2, 2, 128, 0),
     (3000, 640, 4, 4, 128, 1),
+    # more than one wave of query tiles: two query tiles share each K/V tile
+    (1000, 600, 64, 16, 128, 0),
+    (0, 700, 40, 40, 128, 0),
+    (3600, 700, 40, 40, 64, 0),
 ]
 
 
