@@ -495,8 +495,10 @@ def main():
     recompute = tok_all * steps_re / t_re
 
     # roofline of the dominant kernel (K3 attention), live CUDA-event durations
-    att = [(e0.elapsed_time(e1) * 1e-3, w) for kind, e0, e1, w in probe if kind == "attention"]
-    emb = [(e0.elapsed_time(e1) * 1e-3, w) for kind, e0, e1, w in probe if kind == "reembed"]
+    # device timestamps (globaltimer) around each K3 / K2 launch inside the layer graphs
+    dur = runner.probe_durations(probe)
+    att = [(t, w) for kind, t, w in dur if kind == "attention"]
+    emb = [(t, w) for kind, t, w in dur if kind == "reembed"]
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     tflops_peak = peaks.get("bf16_tflops_sustained", 1400.0)

@@ -221,14 +221,17 @@ typedef struct askv_prefill_plan {
   const int64_t* promote_block_ids; /* host array */
   int32_t promote_nblocks;
   int64_t block_bytes, chunk_bytes, row_bytes;
-  void* const* ev_layer_begin;
-  void* const* ev_layer_end;
-  void* const* ev_wait_begin;
-  void* const* ev_wait_end;
-  void* const* ev_reembed_begin;
-  void* const* ev_reembed_end;
-  void* const* ev_attn_begin;
-  void* const* ev_attn_end;
+  /* Optional device timestamps (globaltimer ns, written by 1-thread stamp
+   * kernels on `stream`; CUDA timing events cost ~24 us each while the host
+   * link is saturated, see profiles/r02_summary.md).  Layout:
+   *   stamps[0]                 loop begin
+   *   stamps[1 + 7*l + 0]       layer l end
+   *   stamps[1 + 7*l + 1 / 2]   pre-load wait begin / end   (stamp_flags & 1, with ev_src_ready)
+   *   stamps[1 + 7*l + 3 / 4]   K2 re-embed begin / end     (stamp_flags & 2, kept > 0 and a source)
+   *   stamps[1 + 7*l + 5 / 6]   K3 attention begin / end    (stamp_flags & 2)
+   * Entries whose stage does not run are left untouched. */
+  uint64_t* stamps;
+  int32_t stamp_flags;
   void (*allreduce)(void* ptr, int64_t elems, void* stream, void* ctx);
   void* allreduce_ctx;
   /* Optional per-layer resident KV (rotated rows [0, kept + n_new) per layer,
@@ -236,9 +239,16 @@ typedef struct askv_prefill_plan {
    * of the shared `kv` buffer, so the whole context stays resident for decode;
    * with src_kind 0 and kept > 0 the first `kept` rows are already there. */
   void* const* kv_layers;
+  /* 1: capture the loop into a CUDA graph (cached per shape, updated in
+   * place) and launch that; 0: issue every kernel on `stream`.  Ignored
+   * (stream issue) with `allreduce` or `promote_base` set. */
+  int32_t graph;
 } askv_prefill_plan;
 
 int askv_prefill_layers(const askv_prefill_plan* plan, void* stream);
+/* Write the device globaltimer (ns) to *dst (device memory) in stream order:
+ * a timing mark that stays cheap while the host link is saturated. */
+int askv_stamp(uint64_t* dst, void* stream);
 /* sizeof(askv_prefill_plan), so FFI mirrors can check their struct layout. */
 size_t askv_prefill_plan_size(void);
 

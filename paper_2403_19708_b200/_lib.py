@@ -47,6 +47,7 @@ SIGNATURES = {
     "askv_event_elapsed_ms": (_i32, [_vp, _vp, C.POINTER(C.c_float)]),
     "askv_prefill_layers": (_i32, [_vp, _vp]),
     "askv_prefill_plan_size": (_sz, []),
+    "askv_stamp": (_i32, [_vp, _vp]),
     "askv_silu_mul": (_i32, [_vp, _vp, _i32, _i32, _vp]),
 }
 
@@ -75,11 +76,9 @@ class PrefillPlan(C.Structure):
         ("promote_base", C.c_void_p), ("promote_block_ids", C.POINTER(C.c_int64)),
         ("promote_nblocks", C.c_int32),
         ("block_bytes", C.c_int64), ("chunk_bytes", C.c_int64), ("row_bytes", C.c_int64),
-        ("ev_layer_begin", _pp), ("ev_layer_end", _pp), ("ev_wait_begin", _pp),
-        ("ev_wait_end", _pp), ("ev_reembed_begin", _pp), ("ev_reembed_end", _pp),
-        ("ev_attn_begin", _pp), ("ev_attn_end", _pp),
+        ("stamps", C.c_void_p), ("stamp_flags", C.c_int32),
         ("allreduce", ALLREDUCE_FN), ("allreduce_ctx", C.c_void_p),
-        ("kv_layers", _pp),
+        ("kv_layers", _pp), ("graph", C.c_int32),
     ]
 
 

@@ -17,6 +17,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <vector>
 
 #include "askv_internal.h"
 
@@ -111,11 +112,55 @@ __global__ void add_inplace_kernel(__nv_bfloat16* __restrict__ x,
   }
 }
 
+// Cross-stream events.  Under stream capture they become external event
+// record / wait nodes, so the pre-loader / saver streams (outside the graph)
+// still order against the graph's layers exactly as in stream issue.
+thread_local bool g_capturing = false;
 inline void rec(void* const* evs, int l, cudaStream_t s) {
-  if (evs && evs[l]) cudaEventRecord((cudaEvent_t)evs[l], s);
+  if (evs && evs[l])
+    cudaEventRecordWithFlags((cudaEvent_t)evs[l], s,
+                             g_capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
 }
 inline void wait(void* const* evs, int l, cudaStream_t s) {
-  if (evs && evs[l]) cudaStreamWaitEvent(s, (cudaEvent_t)evs[l], 0);
+  if (evs && evs[l])
+    cudaStreamWaitEvent(s, (cudaEvent_t)evs[l],
+                        g_capturing ? cudaEventWaitExternal : cudaEventWaitDefault);
+}
+
+__global__ void stamp_kernel(uint64_t* dst) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *dst = t;
+}
+inline void stamp(const askv_prefill_plan* p, int flag, int idx, cudaStream_t s) {
+  if (p->stamps && (p->stamp_flags & flag)) stamp_kernel<<<1, 1, 0, s>>>(p->stamps + idx);
+}
+
+// Executable-graph cache of the layer loop, keyed by everything that shapes
+// the graph's topology (sizes, which optional stages / events are present).
+// A hit re-captures the loop (new pointers / events) and applies it with
+// cudaGraphExecUpdate, which only affects later launches; a miss
+// instantiates.  Each entry keeps an event recorded after its last launch so
+// eviction never destroys an executable that is still running.
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  cudaEvent_t done = nullptr;
+  uint64_t last_use = 0;
+};
+std::mutex g_graph_mu;
+std::map<std::vector<int64_t>, GraphEntry> g_graphs;
+uint64_t g_graph_clock = 0;
+constexpr size_t kMaxGraphs = 96;
+
+std::vector<int64_t> graph_key(const askv_prefill_plan* p, cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto has = [](const void* q) -> int64_t { return q != nullptr; };
+  return {dev, p->layers, p->d_model, p->n_heads, p->n_kv_heads, p->head_dim, p->ffn, p->n_new,
+          p->kept, p->head > 0, p->attn_splits, p->src_kind, p->block_tokens,
+          has(p->save_rows), has(p->ev_src_ready), has(p->ev_src_free), has(p->ev_save_free),
+          has(p->ev_save_ready), p->stamps ? p->stamp_flags : -1, has(p->kv_layers),
+          (int64_t)(intptr_t)s};
 }
 
 #define ASKV_TRY(expr)          \
@@ -163,12 +208,89 @@ extern "C" int askv_event_elapsed_ms(void* start, void* end, float* ms) {
                      "cudaEventElapsedTime");
 }
 
+extern "C" int askv_stamp(uint64_t* dst, void* stream) {
+  clear_error();
+  ASKV_REQUIRE(dst != nullptr, "stamp: null destination");
+  stamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(dst);
+  return launch_status("stamp");
+}
+
 // ------------------------------------------------------------------ layer loop
 extern "C" size_t askv_prefill_plan_size(void) { return sizeof(askv_prefill_plan); }
+
+static int issue_layers(const askv_prefill_plan* p, cudaStream_t s);
 
 extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
   clear_error();
   ASKV_REQUIRE(p != nullptr, "prefill_layers: null plan");
+  cudaStream_t s = (cudaStream_t)stream;
+  // Graph issue: one launch per job instead of ~11 per layer.  While the
+  // pre-loader saturates the host link, every stream launch's command fetch
+  // queues behind the H2D DMA and the GPU idles between kernels (r02
+  // profiles); a graph's nodes are resident on the device.  The tensor-parallel
+  // host callback and the HBM-tier promotion (batched D2D copies) issue as
+  // streams.
+  if (!p->graph || p->allreduce || p->promote_base) return issue_layers(p, s);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+    return issue_layers(p, s);  // caller is capturing already: record into its graph
+  int rc = cuda_status(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed),
+                       "cudaStreamBeginCapture");
+  if (rc != ASKV_OK) return rc;
+  g_capturing = true;
+  rc = issue_layers(p, s);
+  g_capturing = false;
+  cudaGraph_t g = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(s, &g);
+  if (rc != ASKV_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (ec != cudaSuccess) return cuda_status(ec, "cudaStreamEndCapture");
+  const auto key = graph_key(p, s);
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  auto it = g_graphs.find(key);
+  bool ready = false;
+  if (it != g_graphs.end()) {
+    cudaGraphExecUpdateResultInfo info;
+    ready = cudaGraphExecUpdate(it->second.exec, g, &info) == cudaSuccess;
+    if (!ready) {
+      cudaGetLastError();
+      cudaEventSynchronize(it->second.done);
+      cudaGraphExecDestroy(it->second.exec);
+      cudaEventDestroy(it->second.done);
+      g_graphs.erase(it);
+      it = g_graphs.end();
+    }
+  }
+  if (!ready) {
+    if (g_graphs.size() >= kMaxGraphs) {  // evict the least recently used
+      auto lru = g_graphs.begin();
+      for (auto j = g_graphs.begin(); j != g_graphs.end(); ++j)
+        if (j->second.last_use < lru->second.last_use) lru = j;
+      cudaEventSynchronize(lru->second.done);
+      cudaGraphExecDestroy(lru->second.exec);
+      cudaEventDestroy(lru->second.done);
+      g_graphs.erase(lru);
+    }
+    GraphEntry e;
+    cudaError_t ei = cudaGraphInstantiate(&e.exec, g, 0);
+    if (ei == cudaSuccess) ei = cudaEventCreateWithFlags(&e.done, cudaEventDisableTiming);
+    if (ei != cudaSuccess) {
+      if (e.exec) cudaGraphExecDestroy(e.exec);
+      cudaGraphDestroy(g);
+      return cuda_status(ei, "cudaGraphInstantiate");
+    }
+    it = g_graphs.emplace(key, e).first;
+  }
+  cudaGraphDestroy(g);
+  it->second.last_use = ++g_graph_clock;
+  rc = cuda_status(cudaGraphLaunch(it->second.exec, s), "cudaGraphLaunch");
+  if (rc == ASKV_OK) rc = cuda_status(cudaEventRecord(it->second.done, s), "cudaEventRecord");
+  return rc;
+}
+
+static int issue_layers(const askv_prefill_plan* p, cudaStream_t s) {
   ASKV_REQUIRE(p->layers > 0 && p->n_new > 0 && p->kept >= 0 && p->head >= 0,
                "prefill_layers: bad layers=%d n_new=%d kept=%d", p->layers, p->n_new, p->kept);
   ASKV_REQUIRE(p->w_in && p->w_qkv && p->w_o && p->w_post && p->w_gu && p->w_down,
@@ -176,14 +298,14 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
   ASKV_REQUIRE(p->kept == 0 || ((p->src_kind == 1 || p->src_kind == 2) && p->src_layer) ||
                    (p->src_kind == 0 && p->kv_layers),
                "prefill_layers: kept rows need a source (or resident kv_layers)");
-  cudaStream_t s = (cudaStream_t)stream;
   const int n = p->n_new, d = p->d_model, hq = p->n_heads, hkv = p->n_kv_heads,
             hd = p->head_dim, f = p->ffn;
   const int qkv_cols = (hq + 2 * hkv) * hd;
   const int64_t row = 2LL * hkv * hd;
+  stamp(p, 1, 0, s);
   for (int l = 0; l < p->layers; ++l) {
     auto* kv = static_cast<__nv_bfloat16*>(p->kv_layers ? p->kv_layers[l] : p->kv);
-    rec(p->ev_layer_begin, l, s);
+    const int st = 1 + 7 * l;
     ASKV_TRY(askv_rmsnorm(p->x, p->w_in[l], p->h, n, d, p->rms_eps, s));
     ASKV_TRY(gemm(p->h, p->w_qkv[l], p->qkv, n, qkv_cols, d, false, p->gemm_ws,
                   p->gemm_ws_bytes, s));
@@ -193,10 +315,10 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
                            p->kept, p->q_rot, kv + (int64_t)p->kept * row, row, save_rows, s));
     if (save_rows) rec(p->ev_save_ready, l, s);
     if (p->kept > 0 && p->src_kind != 0) {
-      rec(p->ev_wait_begin, l, s);
+      if (p->ev_src_ready) stamp(p, 1, st + 1, s);
       wait(p->ev_src_ready, l, s);
-      rec(p->ev_wait_end, l, s);
-      rec(p->ev_reembed_begin, l, s);
+      if (p->ev_src_ready) stamp(p, 1, st + 2, s);
+      stamp(p, 2, st + 3, s);
       if (p->src_kind == 1) {
         ASKV_TRY(askv_reembed(p->src_layer[l], nullptr, 0, p->src_row_stride, p->head, p->kept,
                               hkv, hd, p->rope_table, p->rope_positions, nullptr, 0, kv, row, s));
@@ -205,7 +327,7 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
                               p->src_row_stride, p->head, p->kept, hkv, hd, p->rope_table,
                               p->rope_positions, nullptr, 0, kv, row, s));
       }
-      rec(p->ev_reembed_end, l, s);
+      stamp(p, 2, st + 4, s);
       if (p->promote_base) {  // HBM tier: keep the pre-loaded rows resident
         const auto* src = static_cast<const char*>(p->src_layer[l]) +
                           (int64_t)p->head * p->row_bytes;
@@ -215,14 +337,14 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
       }
       rec(p->ev_src_free, l, s);
     }
-    rec(p->ev_attn_begin, l, s);
+    stamp(p, 2, st + 5, s);
     ASKV_TRY(askv_prefill_attn(p->q_rot, kv, row, p->kept, n, hq, hkv, hd, p->attn_scale,
                                p->attn_out, p->attn_ws, p->attn_ws_bytes, p->attn_splits, s));
-    rec(p->ev_attn_end, l, s);
+    stamp(p, 2, st + 6, s);
     if (p->allreduce) {  // tensor parallel: row-parallel W_o partial -> all-reduce -> residual
       ASKV_TRY(gemm(p->attn_out, p->w_o[l], p->h, n, d, hq * hd, false, p->gemm_ws,
                     p->gemm_ws_bytes, s));
-      p->allreduce(p->h, (int64_t)n * d, stream, p->allreduce_ctx);
+      p->allreduce(p->h, (int64_t)n * d, (void*)s, p->allreduce_ctx);
       add_inplace_kernel<<<148 * 4, 256, 0, s>>>(static_cast<__nv_bfloat16*>(p->x),
                                                  static_cast<const __nv_bfloat16*>(p->h),
                                                  (int64_t)n * d);
@@ -236,14 +358,14 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
     if (p->allreduce) {
       ASKV_TRY(gemm(p->act, p->w_down[l], p->h, n, d, f, false, p->gemm_ws, p->gemm_ws_bytes,
                     s));
-      p->allreduce(p->h, (int64_t)n * d, stream, p->allreduce_ctx);
+      p->allreduce(p->h, (int64_t)n * d, (void*)s, p->allreduce_ctx);
       add_inplace_kernel<<<148 * 4, 256, 0, s>>>(static_cast<__nv_bfloat16*>(p->x),
                                                  static_cast<const __nv_bfloat16*>(p->h),
                                                  (int64_t)n * d);
     } else {
       ASKV_TRY(gemm(p->act, p->w_down[l], p->x, n, d, f, true, p->gemm_ws, p->gemm_ws_bytes, s));
     }
-    rec(p->ev_layer_end, l, s);
+    stamp(p, 1, st, s);
   }
   return launch_status("prefill_layers");
 }

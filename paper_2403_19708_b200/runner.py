@@ -278,8 +278,9 @@ class Runner:
                  block_tokens: int = 128, host_arena=None, hbm_arena: torch.Tensor | None = None,
                  read_buffer_bytes: int = 4 << 30, write_buffer_bytes: int = 2 << 30,
                  max_new: int = 1024, max_ctx: int | None = None, timeline: bool = True,
-                 tp_reduce=None, gemm_workspace_bytes: int = 32 << 20):
+                 tp_reduce=None, gemm_workspace_bytes: int = 32 << 20, graph: bool = True):
         self.shape = s = shape
+        self.graph = graph   # issue each job's layer loop as one CUDA graph launch
         self.device = torch.device(device)
         self.w = weights or LlamaWeights(shape, seed=seed, device=device)
         self.block_tokens = block_tokens
@@ -326,6 +327,12 @@ class Runner:
         self._last_save: dict = {}                   # session -> (event, host flag)
         self._pool = _EventPool()
         self._leases: dict = {}
+        # device timestamp ring (globaltimer ns) for the compute-stream timeline:
+        # a CUDA timing event on the compute stream costs ~24 us while the
+        # pre-loader saturates the host link (tools/event_probe.cu), a stamp
+        # kernel inside the layer graph ~1 us.
+        self._stamps = torch.zeros(1 << 18, dtype=torch.int64, device=self.device)
+        self._stamp_pos = 0
         self._bufs = {}
         self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
         self._gemm_ws = torch.empty(gemm_workspace_bytes, dtype=torch.uint8, device=self.device)
@@ -364,6 +371,34 @@ class Runner:
             self.tp_reduce(h[:elems], self.s_compute)
         except BaseException as exc:  # re-raised after the native call returns
             self._cb_error = exc
+
+    def _stamp_slice(self, n: int) -> tuple[int, int]:
+        """Reserve n ring entries; returns (offset, allocation count after)."""
+        cap = self._stamps.numel()
+        off = self._stamp_pos % cap
+        if off + n > cap:
+            self._stamp_pos += cap - off
+            off = 0
+        self._stamp_pos += n
+        return off, self._stamp_pos
+
+    def _stamp_values(self, off: int, end: int, n: int) -> list[int]:
+        if self._stamp_pos - end + n > self._stamps.numel():
+            raise RuntimeError("timeline stamps overwritten: finalize() results sooner")
+        return self._stamps[off:off + n].tolist()
+
+    def _stamp_ptr(self, off: int, i: int) -> int:
+        return self._stamps.data_ptr() + 8 * (off + i)
+
+    def probe_durations(self, probe) -> list[tuple[str, float, float]]:
+        """(kind, seconds, work) of each probed launch (after synchronising)."""
+        out, cache = [], {}
+        for kind, off, end, n, i0, i1, work in probe:
+            if (off, end) not in cache:
+                cache[(off, end)] = self._stamp_values(off, end, n)
+            v = cache[(off, end)]
+            out.append((kind, (v[i1] - v[i0]) * 1e-9, work))
+        return out
 
     def _lease(self, jid):
         if not self.timeline:
@@ -505,12 +540,6 @@ class Runner:
             if t.error is not None:
                 raise RuntimeError(f"{t.name} failed") from t.error
 
-    def _probe_pair(self, kind, work, starts, ends):
-        e0, e1 = ops.NativeEvent(timing=True), ops.NativeEvent(timing=True)
-        starts.append(e0.handle)
-        ends.append(e1.handle)
-        self.probe.append((kind, e0, e1, work))
-
     def _run_job(self, jid, job: Job, want_logits: bool) -> JobResult:
         s = self.shape
         L = s.layers
@@ -540,7 +569,10 @@ class Runner:
         cs = self.s_compute
         lease = self._lease(jid)
         self._leases.pop(jid, None)
-        T = (lambda: lease.get().handle) if lease else (lambda: None)  # noqa: E731
+        # stamp slice: [0] job begin, [1] job end, [2:] the native loop's stamps
+        n_st = 3 + 7 * L
+        st_off, st_end = self._stamp_slice(n_st) if (lease or self.probe is not None) \
+            else (0, 0)
         keep = []                       # ctypes arrays alive through the native call
 
         def arr(items):
@@ -550,7 +582,7 @@ class Runner:
 
         first = torch.empty(1, dtype=torch.int64, pin_memory=True)
         logits_out = None
-        rec = {"layers": [], "waits": [], "saves": [], "loads": []}
+        rec = {"saves": [], "loads": []}
         with torch.cuda.stream(cs):
             if job.source == "hbm" or job.mirror_block_ids is not None:
                 # HBM-tier rows written by this session's previous saves (save stream)
@@ -564,7 +596,9 @@ class Runner:
                 if job.prestage:   # start only once the whole job is resident
                     self._slot_ready[units[-1].slot].wait(cs)
             t0 = lease.get() if lease else None
-            if t0:
+            if t0:   # one timing event: the base of the copy streams' intervals
+                _lib.check(_lib.lib().askv_stamp(self._stamp_ptr(st_off, 0), cs.cuda_stream),
+                           "stamp")
                 t0.record(cs)
             if job.token_ids.is_cuda:
                 ids = job.token_ids
@@ -638,26 +672,22 @@ class Runner:
                 p.save_rows = arr([self.wbuf[w].data_ptr() for w in wslots])
                 p.ev_save_free = arr([self._wdone[w].handle for w in wslots])
                 p.ev_save_ready = arr([self._wready[w].handle for w in wslots])
-            if lease:
-                lb, le = [T() for _ in range(L)], [T() for _ in range(L)]
-                p.ev_layer_begin, p.ev_layer_end = arr(lb), arr(le)
-                rec["layers"] = list(zip(lb, le))
-                if kept and job.source != "resident":
-                    wb, we = [T() for _ in range(L)], [T() for _ in range(L)]
-                    p.ev_wait_begin, p.ev_wait_end = arr(wb), arr(we)
-                    rec["waits"] = list(zip(wb, we))
+            reemb = bool(kept) and job.source != "resident"
+            if lease or self.probe is not None:
+                p.stamps = self._stamp_ptr(st_off, 2)
+                p.stamp_flags = (1 if lease else 0) | (2 if self.probe is not None else 0)
+                rec["waited"] = reemb and units is not None
             if self.probe is not None:
-                rb, re_, ab, ae = [], [], [], []
-                reemb = kept and job.source != "resident"
-                for _ in range(L):
+                for l in range(L):
+                    b = 2 + 1 + 7 * l
                     if reemb:
-                        self._probe_pair("reembed", 2 * kept * s.row_bytes, rb, re_)
-                    self._probe_pair("attention", attention_flops(kept, n, hq, hd), ab, ae)
-                if reemb:
-                    p.ev_reembed_begin, p.ev_reembed_end = arr(rb), arr(re_)
-                p.ev_attn_begin, p.ev_attn_end = arr(ab), arr(ae)
+                        self.probe.append(("reembed", st_off, st_end, n_st, b + 3, b + 4,
+                                           2 * kept * s.row_bytes))
+                    self.probe.append(("attention", st_off, st_end, n_st, b + 5, b + 6,
+                                       attention_flops(kept, n, hq, hd)))
             if self._ar_cb is not None:
                 p.allreduce = self._ar_cb
+            p.graph = 1 if self.graph else 0
             self._cb_error = None
             _lib.check(_lib.lib().askv_prefill_layers(C.addressof(p), cs.cuda_stream),
                        "prefill_layers")
@@ -690,16 +720,16 @@ class Runner:
             self.launches += 2
             if want_logits:
                 logits_out = logits[0].clone()
-            t1 = lease.get() if lease else None
-            if t1:
-                t1.record(cs)
+            if lease:
+                _lib.check(_lib.lib().askv_stamp(self._stamp_ptr(st_off, 1), cs.cuda_stream),
+                           "stamp")
         res = JobResult(job.session_id, kept, n, None, first, logits_out,
                         bytes_loaded=kept * s.kv_bytes_per_token if job.source == "host" else 0,
                         bytes_saved=n * s.kv_bytes_per_token if job.save else 0,
                         next_token=nxt)
         if job.kv_cache is not None:
             job.kv_cache.rows = kept + n
-        res._events = (t0, t1, rec, lease) if lease else None
+        res._events = (self, t0, (st_off, st_end, n_st), rec, lease) if lease else None
         return res
 
     def join(self) -> None:
@@ -717,32 +747,38 @@ class Runner:
             evs = getattr(r, "_events", None)
             if not evs:
                 continue
-            t0, t1, rec, lease = evs
+            runner, t0, (off, end, n_st), rec, lease = evs
             ms = C.c_float()
             lib = _lib.lib()
 
-            def f(e):
+            def f(e):   # copy-stream timing event -> seconds after job begin
                 h = e if isinstance(e, int) else e.handle
                 _lib.check(lib.askv_event_elapsed_ms(t0.handle, h, C.byref(ms)), "elapsed")
                 return float(ms.value) * 1e-3
 
+            v = runner._stamp_values(off, end, n_st)
+            g = lambda i: (v[i] - v[0]) * 1e-9  # noqa: E731  compute-stream stamp -> seconds
+
             tl = Timeline()
-            tl.makespan = f(t1)
-            waits = [(f(a), f(b)) for a, b in rec["waits"]]
-            stall = sum(b - a for a, b in waits)
+            tl.makespan = g(1)
+            L = (n_st - 3) // 7
             tl.load_intervals = [(f(a), f(b)) for a, b in rec["loads"]]
             for *_, flag in rec["saves"]:
                 flag.wait()
             tl.save_intervals = [(f(a), f(b)) for a, b, _ in rec["saves"]]
-            comp = []
-            wi = iter(waits)
-            for a, b in rec["layers"]:
-                la, lb = f(a), f(b)
-                if waits:
-                    wa, wb = next(wi)
-                    comp.extend([(la, wa), (wb, lb)])
+            comp, waits = [], []
+            begin = g(2)
+            for l in range(L):
+                b = 3 + 7 * l
+                end_l = g(b)
+                if rec.get("waited"):
+                    wa, wb = g(b + 1), g(b + 2)
+                    waits.append((wa, wb))
+                    comp.extend([(begin, wa), (wb, end_l)])
                 else:
-                    comp.append((la, lb))
+                    comp.append((begin, end_l))
+                begin = end_l
+            stall = sum(b - a for a, b in waits)
             tl.compute_intervals = comp
             tl.stall_total = stall if stall > 1e-9 else 0.0
             tl.max_gap = max((b - a for a, b in waits), default=0.0)

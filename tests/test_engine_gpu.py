@@ -165,6 +165,16 @@ def test_reuse_equals_gpu_recompute_13b_layer_shapes():
     tl = o.result.timeline
     assert tl is not None and len(tl.load_intervals) == shape.layers
     assert tl.makespan > 0 and tl.stall_total <= tl.makespan
+    # device-stamped compute intervals: per layer [begin, wait) + [wait end, end),
+    # ordered and inside the job's makespan
+    assert len(tl.compute_intervals) == 2 * shape.layers
+    flat = [t for iv in tl.compute_intervals for t in iv]
+    assert all(a <= b for a, b in zip(flat, flat[1:]))
+    assert 0 <= flat[0] and flat[-1] <= tl.makespan
+    rec.timeline = None
+    eng.runner.finalize([rec])
+    assert len(rec.timeline.compute_intervals) == shape.layers   # recompute: no waits
+    assert rec.timeline.stall_total == 0.0
 
 
 def test_c4_long_context_32k_history_truncated_reuse():
