@@ -129,7 +129,11 @@ def select_turns(cfg: str, rank: int, world: int, n: int):
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+              "timestamp")
+    # nvidia-smi is started before the warm-up (its NVML start-up stalls CUDA
+    # host calls for a moment) and only the samples whose timestamp falls in
+    # the timed window [window[0], window[1]] (host clock) are summarised.
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
@@ -156,12 +160,21 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
-    def summary(self) -> dict:
+    def summary(self, window=None) -> dict:
+        import datetime
         rows = []
         try:
             for line in open(self.path):
                 parts = [p.strip() for p in line.split(",")]
-                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                if len(parts) >= 10 and parts[1].replace(".", "").isdigit():
+                    if window is not None:
+                        try:
+                            ts = datetime.datetime.strptime(
+                                parts[9], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                        except ValueError:
+                            ts = None
+                        if ts is not None and not window[0] <= ts <= window[1]:
+                            continue
                     rows.append(parts)
         except OSError:
             pass
@@ -353,7 +366,9 @@ def main():
     runner = Runner(shape, device=dev, seed=rank if tp > 1 else 0, block_tokens=tb,
                     host_arena=arena, tp_reduce=tp_hook,
                     hbm_arena=hbm, read_buffer_bytes=4 << 30, write_buffer_bytes=1 << 30,
-                    max_new=max(max_new, 1), max_ctx=max(shape.context_window, max_kept + 1))
+                    max_new=max(max_new, 1), max_ctx=max(shape.context_window, max_kept + 1),
+                    # tune the GEMMs over the recompute baseline's prompt lengths too
+                    autotune=max(shape.context_window, max_kept + 1) + max(max_new, 1))
     ids_perm = np.random.default_rng(99 + rank).permutation(n_blocks)
     jobs = {"host": [], "hbm": [], "recompute": []}
     pos = 0
@@ -388,6 +403,11 @@ def main():
 
     def timed(mode: str, steps: int, warmup: int, probe: bool = False, clocks=None):
         js = jobs[mode]
+        sampler = ClockSampler(local) if clocks is not None and \
+            os.environ.get("ASKV_BENCH_CLOCKS", "1") != "0" else None
+        if sampler:
+            sampler.__enter__()
+        runner.probe = [] if probe else None   # same graph shapes as the timed steps
         for _ in range(warmup):
             runner.run(js)
             runner.join()
@@ -398,9 +418,7 @@ def main():
         cs = runner.s_compute
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        sampler = ClockSampler(local) if clocks is not None else None
-        if sampler:
-            sampler.__enter__()
+        w0 = time.time()
         e0.record(cs)
         res = None
         for _ in range(steps):
@@ -408,9 +426,10 @@ def main():
             runner.join()
         e1.record(cs)
         torch.cuda.synchronize()
+        w1 = time.time()
         if sampler:
             sampler.__exit__(None, None, None)
-            clocks.update(sampler.summary())
+            clocks.update(sampler.summary((w0, w1)))
         barrier()
         ms = e0.elapsed_time(e1)
         launches = runner.launches - launches0
@@ -427,7 +446,9 @@ def main():
     # e2e (headline) — KV from the pinned host arena, clocks sampled here
     ms_host, res_host, launches, _ = timed("host", args.steps, args.warmup, clocks=clocks)
     # value — KV resident in HBM; probe the attention / re-embed launches
-    ms_hbm, res_hbm, _, probe = timed("hbm", args.steps, args.warmup, probe=True)
+    clocks_value: dict = {}
+    ms_hbm, res_hbm, _, probe = timed("hbm", args.steps, args.warmup, probe=True,
+                                      clocks=clocks_value)
     # recompute baseline
     ms_re, res_re, _, _ = timed("recompute", max(2, args.steps // 2), 1)
     # prestaged TTFT: each turn starts once its whole KV sits in the read buffer
@@ -592,7 +613,8 @@ def main():
         "decode": decode,
         "disk": disk,
         "gpu_launches": launches,
-        "clocks": clocks,
+        "clocks": clocks_value,          # during the `value` timed region
+        "clocks_e2e": clocks,            # during the `e2e` timed region
         "cpu_baseline": cpu,
     }
     if rank == 0:

@@ -251,6 +251,11 @@ int askv_prefill_layers(const askv_prefill_plan* plan, void* stream);
 int askv_stamp(uint64_t* dst, void* stream);
 /* sizeof(askv_prefill_plan), so FFI mirrors can check their struct layout. */
 size_t askv_prefill_plan_size(void);
+/* Time cuBLASLt's top candidate algorithms for y[n][m] = x[n][k] W[m][k]^T at
+ * n = 32, 64, ..., 1024, then every 512 up to n_max (scratch operands, on
+ * `stream`, synchronising), and make the layer loop use each n bucket's
+ * fastest one.  Optional; call once per projection shape before serving. */
+int askv_gemm_autotune(int m, int k, int n_max, size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -48,6 +48,7 @@ SIGNATURES = {
     "askv_prefill_layers": (_i32, [_vp, _vp]),
     "askv_prefill_plan_size": (_sz, []),
     "askv_stamp": (_i32, [_vp, _vp]),
+    "askv_gemm_autotune": (_i32, [_i32, _i32, _i32, _sz, _vp]),
     "askv_silu_mul": (_i32, [_vp, _vp, _i32, _i32, _vp]),
 }
 

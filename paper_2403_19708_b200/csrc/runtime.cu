@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -46,6 +48,39 @@ cublasLtHandle_t handle_for_device() {
   g_handles[dev] = h;
   return h;
 }
+
+// Autotuned algorithms per (device, m, k, n bucket): cuBLASLt's heuristic #0 is
+// up to ~15 % off the best of its own top candidates at the skinny n of a
+// reuse prefill (tools/gemm_probe.cu; QKV and gate|up), so askv_gemm_autotune
+// times the top candidates once per bucket and plan_for prefers the winner
+// when cublasLtMatmulAlgoCheck accepts it for the exact shape.
+struct Tuned {
+  cublasLtMatmulAlgo_t algo;
+};
+std::map<std::tuple<int, int, int, int>, Tuned> g_tuned;
+inline int n_bucket(int n) { return n <= 1024 ? (n + 31) / 32 * 32 : (n + 511) / 512 * 512; }
+
+struct Layouts {
+  cublasLtMatmulDesc_t op = nullptr;
+  cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
+  bool make(int m, int n, int k) {
+    if (cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F, CUDA_R_32F) != CUBLAS_STATUS_SUCCESS)
+      return false;
+    cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
+    cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof(ta));
+    cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof(tb));
+    cublasLtMatrixLayoutCreate(&a, CUDA_R_16BF, k, m, k);  // W: [m][k] row-major
+    cublasLtMatrixLayoutCreate(&b, CUDA_R_16BF, k, n, k);  // x: [n][k] row-major
+    cublasLtMatrixLayoutCreate(&c, CUDA_R_16BF, m, n, m);  // y: [n][m] row-major
+    return a && b && c;
+  }
+  void destroy() {
+    if (a) cublasLtMatrixLayoutDestroy(a);
+    if (b) cublasLtMatrixLayoutDestroy(b);
+    if (c) cublasLtMatrixLayoutDestroy(c);
+    if (op) cublasLtMatmulDescDestroy(op);
+  }
+};
 
 // Row-major y[n][m] (+)= x[n][k] . W[m][k]^T  ==  column-major Y(m x n) = W^T(m x k) X(k x n)
 const GemmPlan* plan_for(int m, int n, int k, bool accumulate, size_t ws_bytes) {
@@ -81,6 +116,19 @@ const GemmPlan* plan_for(int m, int n, int k, bool accumulate, size_t ws_bytes) 
   p.algo = res.algo;
   p.ws = res.workspaceSize;
   std::lock_guard<std::mutex> lk(g_mu);
+  auto tu = g_tuned.find(std::make_tuple(dev, m, k, n_bucket(n)));
+  if (tu != g_tuned.end()) {
+    cublasLtMatmulHeuristicResult_t chk = {};
+    if (cublasLtMatmulAlgoCheck(h, p.op, p.a, p.b, p.c, p.c, &tu->second.algo, &chk) ==
+            CUBLAS_STATUS_SUCCESS &&
+        chk.workspaceSize <= ws_bytes) {
+      p.algo = tu->second.algo;
+      p.ws = chk.workspaceSize;
+      if (getenv("ASKV_GEMM_DEBUG")) fprintf(stderr, "plan m=%d n=%d k=%d: tuned\n", m, n, k);
+    } else if (getenv("ASKV_GEMM_DEBUG")) {
+      fprintf(stderr, "plan m=%d n=%d k=%d: tuned algo rejected\n", m, n, k);
+    }
+  }
   auto ins = g_plans.emplace(key, p);
   return &ins.first->second;
 }
@@ -213,6 +261,117 @@ extern "C" int askv_stamp(uint64_t* dst, void* stream) {
   ASKV_REQUIRE(dst != nullptr, "stamp: null destination");
   stamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(dst);
   return launch_status("stamp");
+}
+
+// ------------------------------------------------------------------ GEMM autotune
+__global__ void fill_random_kernel(__nv_bfloat16* p, size_t n, uint32_t seed) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    uint32_t x = (uint32_t)i * 2654435761u ^ seed;
+    x ^= x >> 13;
+    x *= 0x5bd1e995u;
+    x ^= x >> 15;
+    p[i] = __float2bfloat16(((int)(x & 0xffff) - 32768) * (0.02f / 32768.f));
+  }
+}
+
+extern "C" int askv_gemm_autotune(int m, int k, int n_max, size_t ws_bytes, void* stream) {
+  clear_error();
+  ASKV_REQUIRE(m > 0 && k > 0 && n_max > 0, "gemm_autotune: bad shape %d x %d x %d", m, n_max, k);
+  cublasLtHandle_t h = handle_for_device();
+  if (!h) {
+    set_error("cuBLASLt handle");
+    return ASKV_ECUDA;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int n_top = n_bucket(n_max);
+  // scratch operands with random N(0, 0.02)-ish data: tensor-core power (and
+  // so clocks) depends on the data, zeros would flatter some candidates
+  void *w = nullptr, *x = nullptr, *y = nullptr, *ws = nullptr;
+  cudaError_t e = cudaMalloc(&w, (size_t)m * k * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&x, (size_t)n_top * k * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&y, (size_t)n_top * m * 2);
+  if (e == cudaSuccess && ws_bytes) e = cudaMalloc(&ws, ws_bytes);
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (e == cudaSuccess) e = cudaEventCreate(&a);
+  if (e == cudaSuccess) e = cudaEventCreate(&b);
+  int rc = cuda_status(e, "gemm_autotune alloc");
+  if (rc == ASKV_OK) {
+    fill_random_kernel<<<1184, 256, 0, s>>>((__nv_bfloat16*)w, (size_t)m * k, 17u);
+    fill_random_kernel<<<1184, 256, 0, s>>>((__nv_bfloat16*)x, (size_t)n_top * k, 99u);
+  }
+  const float alpha = 1.f, beta = 0.f;
+  for (int n = 32; rc == ASKV_OK && n <= n_top; n = n < 1024 ? n + 32 : n + 512) {
+    if (n > 1024 && n % 512) n = n_bucket(n);
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      if (g_tuned.count(std::make_tuple(dev, m, k, n))) continue;
+    }
+    Layouts L;
+    if (!L.make(m, n, k)) {
+      L.destroy();
+      set_error("gemm_autotune: cuBLASLt layouts");
+      rc = ASKV_ECUDA;
+      break;
+    }
+    cublasLtMatmulPreference_t pref = nullptr;
+    cublasLtMatmulPreferenceCreate(&pref);
+    cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES,
+                                         &ws_bytes, sizeof(ws_bytes));
+    cublasLtMatmulHeuristicResult_t res[8];
+    int found = 0;
+    cublasLtMatmulAlgoGetHeuristic(h, L.op, L.a, L.b, L.c, L.c, pref, 8, res, &found);
+    cublasLtMatmulPreferenceDestroy(pref);
+    float best = 1e30f;
+    int best_i = -1;
+    for (int i = 0; i < found; ++i) {
+      auto run = [&] {
+        return cublasLtMatmul(h, L.op, &alpha, w, L.a, x, L.b, &beta, y, L.c, y, L.c,
+                              &res[i].algo, ws, res[i].workspaceSize, s);
+      };
+      if (res[i].workspaceSize > ws_bytes || run() != CUBLAS_STATUS_SUCCESS) continue;
+      run();
+      const int iters = n <= 1024 ? 8 : 4;
+      cudaEventRecord(a, s);
+      for (int it = 0; it < iters; ++it) run();
+      cudaEventRecord(b, s);
+      if (cudaEventSynchronize(b) != cudaSuccess) break;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, a, b);
+      if (ms < best) {
+        best = ms;
+        best_i = i;
+      }
+    }
+    L.destroy();
+    if (getenv("ASKV_GEMM_DEBUG"))
+      fprintf(stderr, "autotune m=%d k=%d n=%d: %d candidates, best #%d %.1f us\n", m, k, n,
+              found, best_i, best * 1e3f / (n <= 1024 ? 8 : 4));
+    if (best_i >= 0) {
+      std::lock_guard<std::mutex> lk(g_mu);
+      g_tuned[std::make_tuple(dev, m, k, n)] = Tuned{res[best_i].algo};
+    }
+    rc = launch_status("gemm_autotune");
+  }
+  if (a) cudaEventDestroy(a);
+  if (b) cudaEventDestroy(b);
+  cudaFree(w);
+  cudaFree(x);
+  cudaFree(y);
+  cudaFree(ws);
+  {  // re-plan this (m, k) so cached plans pick the tuned algorithms up
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto it = g_plans.begin(); it != g_plans.end();) {
+      if (std::get<0>(it->first) == dev && std::get<1>(it->first) == m &&
+          std::get<3>(it->first) == k)
+        it = g_plans.erase(it);
+      else
+        ++it;
+    }
+  }
+  return rc;
 }
 
 // ------------------------------------------------------------------ layer loop

@@ -278,7 +278,8 @@ class Runner:
                  block_tokens: int = 128, host_arena=None, hbm_arena: torch.Tensor | None = None,
                  read_buffer_bytes: int = 4 << 30, write_buffer_bytes: int = 2 << 30,
                  max_new: int = 1024, max_ctx: int | None = None, timeline: bool = True,
-                 tp_reduce=None, gemm_workspace_bytes: int = 32 << 20, graph: bool = True):
+                 tp_reduce=None, gemm_workspace_bytes: int = 32 << 20, graph: bool = True,
+                 autotune: bool | int = True):
         self.shape = s = shape
         self.graph = graph   # issue each job's layer loop as one CUDA graph launch
         self.device = torch.device(device)
@@ -336,6 +337,16 @@ class Runner:
         self._bufs = {}
         self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
         self._gemm_ws = torch.empty(gemm_workspace_bytes, dtype=torch.uint8, device=self.device)
+        if autotune:   # once per projection shape (cached in-process by the library)
+            # n range: the new tokens of a reuse job (an int widens it, e.g. to
+            # the full prompts of recompute jobs)
+            tune_n = max_new if autotune is True else int(autotune)
+            tp_n = s.n_heads * s.head_dim
+            for m_, k_ in ((s.qkv_cols, s.d_model), (s.d_model, tp_n),
+                           (2 * s.ffn, s.d_model), (s.d_model, s.ffn)):
+                _lib.check(_lib.lib().askv_gemm_autotune(
+                    m_, k_, tune_n, gemm_workspace_bytes,
+                    self.s_compute.cuda_stream), "gemm_autotune")
         self._w_arrays = {
             key: _ptr_array([lw[key].data_ptr() for lw in self.w.layers])
             for key in ("w_in", "wqkv", "wo", "w_post", "wgu", "wd")}
