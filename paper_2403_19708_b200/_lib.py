@@ -7,10 +7,11 @@ every operation raises (north star: "no CPU fallback").
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libaskv.so"
+LIB_PATH = Path(os.environ.get("ASKV_LIB") or Path(__file__).resolve().parent / "libaskv.so")
 
 ASKV_OK = 0
 ASKV_EINVAL = -1
