@@ -38,7 +38,7 @@ __device__ __forceinline__ void trace_stamp(int slot) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-  if (g_attn_trace) g_attn_trace[cta * 64 + slot] = t;
+  if (g_attn_trace) g_attn_trace[cta * 128 + slot] = t;
 }
 #define ATTN_TRACE(slot) trace_stamp(slot)
 #else

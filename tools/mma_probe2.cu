@@ -1,0 +1,120 @@
+// Micro-probe 2: tcgen05.mma cost per instruction in the attention kernels'
+// operand patterns (one SM and all SMs), with and without concurrent shared-
+// memory writes (what the TMA K/V fill does to the smem ports).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/mma_probe2 tools/mma_probe2.cu
+// Modes (M = 128, K = 16 per instruction, 8 instructions per "tile"):
+//   0 SS N=128, A fixed (Q), B walks 3 K tiles       (S = Q K^T, kernel 1)
+//   1 SS N=64,  A fixed (Q), B walks 6 half tiles     (S, kernel 2)
+//   2 TS N=128, A in TMEM (P), B walks 3 V tiles      (O += P V)
+//   3 SS N=256, A fixed, B walks                      (S for a 256-key tile)
+//   4 TS N=128 with A = Q in TMEM, B walks K tiles    (S with Q resident in TMEM)
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+
+#include "../paper_2403_19708_b200/csrc/askv_ptx.cuh"
+using namespace askv;
+
+template <int MODE>
+__global__ void probe(long long* out, int iters, int writers) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  __shared__ volatile int done;
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    done = 0;
+  }
+  if (warp == 0) tmem_alloc(&slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  for (int i = threadIdx.x; i < 160 * 1024 / 4; i += blockDim.x)
+    ((uint32_t*)smem)[i] = 0x3c003c00u ^ (i * 2654435761u & 0x00ff00ffu);
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 32768);
+    constexpr int N = MODE == 1 ? 64 : MODE == 3 ? 256 : 128;
+    const uint32_t idesc = idesc_bf16_f32(128, N, 0, MODE == 2 ? 1 : 0);
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const uint32_t tile = sb + (it % 3) * 32768 + (MODE == 1 ? (it & 1) * 8192 : 0);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
+        if (MODE == 2)
+          umma_bf16_tmem_a(tmem + 256, tmem + k * 8, sdesc_sw128(tile + k * 2048, 16384, 1024),
+                           idesc, k > 0);
+        else if (MODE == 4)
+          umma_bf16_tmem_a(tmem + 256, tmem + k * 8, sdesc_sw128(tile + off, 16, 1024), idesc,
+                           k > 0);
+        else
+          umma_bf16(tmem, sdesc_sw128(sa + off, 16, 1024), sdesc_sw128(tile + off, 16, 1024),
+                    idesc, k > 0);
+      }
+    }
+    umma_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+    done = 1;
+  } else if (warp >= 1 && warp <= writers) {
+    // smem writer: 16-byte stores over a 32 KB region (a TMA fill stand-in)
+    uint4* w = reinterpret_cast<uint4*>(smem + 131072);
+    const uint4 v = make_uint4(1, 2, 3, 4);
+    int i = (warp - 1) * 32 + (threadIdx.x & 31);
+    while (!done) {
+#pragma unroll 8
+      for (int r = 0; r < 64; ++r) w[(i + r * 128) & 2047] = v;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+int main() {
+  long long* d;
+  cudaMalloc(&d, 148 * sizeof(long long));
+  const int smem = 170 * 1024;
+  const char* names[] = {"SS N=128 (S, kernel 1)", "SS N=64 (S, kernel 2)", "TS N=128 (PV)",
+                         "SS N=256", "TS N=128 A=Q in TMEM (S)"};
+  auto run = [&](auto kern, int mode) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int writers : {0, 4}) {
+      for (int grid : {1, 148}) {
+        const int iters = 400;
+        kern<<<grid, 160, smem>>>(d, iters, writers);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e) {
+          printf("err %s\n", cudaGetErrorString(e));
+          return;
+        }
+        long long h[148];
+        cudaMemcpy(h, d, grid * sizeof(long long), cudaMemcpyDeviceToHost);
+        double mx = 0;
+        for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
+        const int n = mode == 1 ? 64 : mode == 3 ? 256 : 128;
+        printf("%-26s grid=%3d smem-writers=%d: %6.1f cycles/MMA (%5.0f MAC/clk/SM)\n",
+               names[mode], grid, writers, mx / (iters * 8.0),
+               128.0 * n * 16 * iters * 8 / mx);
+      }
+    }
+  };
+  run(probe<0>, 0);
+  run(probe<1>, 1);
+  run(probe<2>, 2);
+  run(probe<3>, 3);
+  run(probe<4>, 4);
+  return 0;
+}
