@@ -115,14 +115,18 @@ __global__ void __launch_bounds__(kThreads)
   const int k_units = hkv * kUnitsPerHead;
   const int row_units = 2 * k_units;
   const int total = nrows * row_units;
-  constexpr int kIlp = 4;
+  // 13B: 2 rows x 1280 vectors = two rounds of 5 per thread; the row of a
+  // vector is a compare (kReRows == 2), not an integer division (K2 was
+  // issue-bound: ncu 45-50 % issue slots, profiles/r01d_summary.md)
+  static_assert(kReRows == 2, "row index below assumes two rows per CTA");
+  constexpr int kIlp = 5;
   for (int base = threadIdx.x; base < total; base += kThreads * kIlp) {
     int4 v[kIlp];
 #pragma unroll
     for (int k = 0; k < kIlp; ++k) {
       const int g = base + k * kThreads;
       if (g < total) {
-        const int rr = g / row_units;
+        const int rr = g >= row_units ? 1 : 0;
         v[k] = ld_nc16(srow_s[rr] + (g - rr * row_units) * 8);
       }
     }
@@ -130,7 +134,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int k = 0; k < kIlp; ++k) {
       const int g = base + k * kThreads;
       if (g < total) {
-        const int rr = g / row_units;
+        const int rr = g >= row_units ? 1 : 0;
         const int u = g - rr * row_units;
         int4 x = v[k];
         if (u < k_units) x = rotate8(x, cs_s + (rr * kHalf + (u % kUnitsPerHead) * 4) * 2);
