@@ -260,6 +260,29 @@ def run_reference(args, shape, turns):
 # GPU arm
 # ---------------------------------------------------------------------------
 
+def link_peak(host_u8: torch.Tensor, dev_u8: torch.Tensor, nbytes: int = 1 << 30) -> dict:
+    """Host-link peak of this box: one plain pinned-host <-> HBM cudaMemcpyAsync
+    of `nbytes` per direction (best of 3, CUDA events).  The roofline the
+    pre-loader (K1) and saver (K4) are judged against."""
+    import torch
+    n = min(nbytes, host_u8.numel(), dev_u8.numel())
+    s = torch.cuda.Stream()
+    out = {}
+    for name, dst, src in (("h2d", dev_u8[:n], host_u8[:n]), ("d2h", host_u8[:n], dev_u8[:n])):
+        best = None
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(s):
+                e0.record()
+                dst.copy_(src, non_blocking=True)
+                e1.record()
+            e1.synchronize()
+            t = e0.elapsed_time(e1) * 1e-3
+            best = t if best is None else min(best, t)
+        out[name] = n / best / 1e9
+    return out
+
+
 def disk_probe(root, arena, bids, block_bytes, rows):
     """Disk tier (§8f-4): write one session's blocks from the pinned arena to
     a file and read them back (IO-thread pool, O_DIRECT when the file system
@@ -500,6 +523,8 @@ def main():
                           "HBM; per-token K|V saved to pinned host DRAM asynchronously "
                           "(overlap.py:126-200 decode branch); weight-bandwidth bound"}
 
+    # host-link roofline (plain 1 GB copies each way, after the timed regions)
+    link = link_peak(arena.buffer, hbm.view(torch.uint8))
     disk = None
     if args.disk_dir != "none" and rank == 0:
         disk = disk_probe(args.disk_dir, arena, [int(b) for b in ids_perm[:nbs[0]]],
@@ -607,6 +632,14 @@ def main():
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                      "flops_per_launch": statistics.fmean(w for _, w in att),
                      "launches": len(att)},
+        "roofline_link": {"kernel": "K1 askv_preload_layer (H2D DMA batches)", "bound": "host link",
+                          "achieved": h2d_bytes / load_busy / 1e9 if load_busy else None,
+                          "peak": link["h2d"], "unit": "GB/s",
+                          "frac": (h2d_bytes / load_busy / 1e9) / link["h2d"] if load_busy else None,
+                          "e2e_frac": (h2d_step / (ms_host / args.steps * 1e-3) / 1e9) / link["h2d"],
+                          "d2h_peak": link["d2h"],
+                          "peak_source": "measured in this run: one 1 GB pinned-host->HBM "
+                                         "cudaMemcpyAsync, best of 3"},
         "roofline_reembed": {"kernel": "askv_reembed (K2)", "bound": "hbm",
                              "achieved": emb_gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": emb_gbs / hbm_peak},
