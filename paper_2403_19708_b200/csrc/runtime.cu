@@ -204,8 +204,12 @@ std::vector<int64_t> graph_key(const askv_prefill_plan* p, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   auto has = [](const void* q) -> int64_t { return q != nullptr; };
+  // `kept` only changes kernel parameters (grids, offsets), so jobs that differ
+  // only in it (every decode step) update one executable instead of
+  // instantiating a graph each; the split count and n (GEMM algorithms) shape
+  // the topology and stay in the key
   return {dev, p->layers, p->d_model, p->n_heads, p->n_kv_heads, p->head_dim, p->ffn, p->n_new,
-          p->kept, p->head > 0, p->attn_splits, p->src_kind, p->block_tokens,
+          p->kept > 0, p->attn_splits, p->src_kind, p->block_tokens,
           has(p->save_rows), has(p->ev_src_ready), has(p->ev_src_free), has(p->ev_save_free),
           has(p->ev_save_ready), p->stamps ? p->stamp_flags : -1, has(p->kv_layers),
           (int64_t)(intptr_t)s};
