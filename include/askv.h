@@ -256,6 +256,11 @@ size_t askv_prefill_plan_size(void);
  * `stream`, synchronising), and make the layer loop use each n bucket's
  * fastest one.  Optional; call once per projection shape before serving. */
 int askv_gemm_autotune(int m, int k, int n_max, size_t workspace_bytes, void* stream);
+/* Set the device's persisting-L2 set-aside (clamped to the device maximum) so
+ * the evict_last hints on the layer's rotated K/V rows (K2 / rope_new stores,
+ * K3 loads) can hold them in L2 between producer and consumer; *applied (may
+ * be NULL) receives the size the driver set. */
+int askv_l2_persist(size_t bytes, size_t* applied);
 
 #ifdef __cplusplus
 }

@@ -50,6 +50,7 @@ SIGNATURES = {
     "askv_prefill_plan_size": (_sz, []),
     "askv_stamp": (_i32, [_vp, _vp]),
     "askv_gemm_autotune": (_i32, [_i32, _i32, _i32, _sz, _vp]),
+    "askv_l2_persist": (_i32, [_sz, C.POINTER(C.c_size_t)]),
     "askv_silu_mul": (_i32, [_vp, _vp, _i32, _i32, _vp]),
 }
 

@@ -29,6 +29,20 @@ __device__ __forceinline__ int4 ld_nc16(const void* p) {
                : "l"(p));
   return r;
 }
+// Read-once load that asks L2 to evict the line first (K2's source rows must
+// not displace the rotated rows it writes for K3).
+__device__ __forceinline__ int4 ld_nc16_ef(const void* p, uint64_t pol) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void st16(void* p, int4 v) {
   asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w)
@@ -120,6 +134,7 @@ __global__ void __launch_bounds__(kThreads)
   // issue-bound: ncu 45-50 % issue slots, profiles/r01d_summary.md)
   static_assert(kReRows == 2, "row index below assumes two rows per CTA");
   constexpr int kIlp = 5;
+  const uint64_t pol_src = policy_evict_first();
   for (int base = threadIdx.x; base < total; base += kThreads * kIlp) {
     int4 v[kIlp];
 #pragma unroll
@@ -127,7 +142,7 @@ __global__ void __launch_bounds__(kThreads)
       const int g = base + k * kThreads;
       if (g < total) {
         const int rr = g >= row_units ? 1 : 0;
-        v[k] = ld_nc16(srow_s[rr] + (g - rr * row_units) * 8);
+        v[k] = ld_nc16_ef(srow_s[rr] + (g - rr * row_units) * 8, pol_src);
       }
     }
 #pragma unroll

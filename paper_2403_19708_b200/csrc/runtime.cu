@@ -267,6 +267,27 @@ extern "C" int askv_stamp(uint64_t* dst, void* stream) {
   return launch_status("stamp");
 }
 
+// ------------------------------------------------------------------ L2 set-aside
+// K2 / rope_new store the layer's rotated K/V rows with an L2 evict_last hint
+// and K3 loads them the same way; the device's persisting-L2 set-aside bounds
+// how much of L2 such lines may hold (0 by default).  Returns the bytes set.
+extern "C" int askv_l2_persist(size_t bytes, size_t* applied) {
+  clear_error();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int mx = 0;
+  cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
+  const size_t want = bytes < (size_t)mx ? bytes : (size_t)mx;
+  const int rc = cuda_status(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want),
+                             "cudaDeviceSetLimit(PersistingL2CacheSize)");
+  if (applied) {
+    size_t v = 0;
+    cudaDeviceGetLimit(&v, cudaLimitPersistingL2CacheSize);
+    *applied = v;
+  }
+  return rc;
+}
+
 // ------------------------------------------------------------------ GEMM autotune
 __global__ void fill_random_kernel(__nv_bfloat16* p, size_t n, uint32_t seed) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;

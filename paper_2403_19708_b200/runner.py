@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import queue
 import threading
 from dataclasses import dataclass, field
@@ -337,6 +338,12 @@ class Runner:
         self._bufs = {}
         self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
         self._gemm_ws = torch.empty(gemm_workspace_bytes, dtype=torch.uint8, device=self.device)
+        # L2 set-aside for the evict_last K/V rows (ASKV_L2_PERSIST_MB, default 0 = off)
+        persist_mb = int(os.environ.get("ASKV_L2_PERSIST_MB", "0"))
+        if persist_mb > 0:
+            got = C.c_size_t()
+            _lib.check(_lib.lib().askv_l2_persist(persist_mb << 20, C.byref(got)), "l2_persist")
+            self.l2_persist_bytes = got.value
         if autotune:   # once per projection shape (cached in-process by the library)
             # n range: the new tokens of a reuse job (an int widens it, e.g. to
             # the full prompts of recompute jobs)
