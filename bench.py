@@ -260,6 +260,16 @@ def run_reference(args, shape, turns):
 # GPU arm
 # ---------------------------------------------------------------------------
 
+def host_mem_available() -> int:
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 1 << 62
+
+
 def link_peak(host_u8: torch.Tensor, dev_u8: torch.Tensor, nbytes: int = 1 << 30) -> dict:
     """Host-link peak of this box: one plain pinned-host <-> HBM cudaMemcpyAsync
     of `nbytes` per direction (best of 3, CUDA events).  The roofline the
@@ -365,6 +375,11 @@ def main():
     tb = args.block_tokens
     block_bytes = tb * shape.kv_bytes_per_token
     nbs = [-(-(kept + new) // tb) for _, _, kept, new in turns]
+    # every rank pins its turns' blocks in host DRAM (13B: ~1.9 GB per turn);
+    # keep all ranks of the node within half the available memory
+    host_budget = host_mem_available() // 2 // int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+    while len(turns) > 4 and sum(nbs) * block_bytes > host_budget:
+        turns, nbs = turns[:-1], nbs[:-1]
     dec_steps = args.decode_steps
     # decode probe (§8f-2): the first sampled turn gets its own blocks with room
     # for the decoded tokens
@@ -576,7 +591,7 @@ def main():
     d2h_step = d2h_bytes + 8 * len(jobs["host"])
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:   # N=1 only (contract)
         cb = cpu_reference(turns, shape, pairs_per_turn=24)
         cpu = {"value": cb["value"], "unit": "tokens/s", "cores": cb["cores"], "kind": "port",
                "sample": (f"oracle port of attention_with_decoupled_cache (rope.py:118-144, "
