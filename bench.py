@@ -360,11 +360,17 @@ def main():
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    # ASKV_BENCH_ONE_GPU=1 (test hook): every rank on cuda:0 with a gloo group,
+    # to exercise the N>1 path (sharding, barriers, max/sum over ranks) on a
+    # 1-GPU box; never used for reported numbers
+    one_gpu = os.environ.get("ASKV_BENCH_ONE_GPU") == "1"
+    local = 0 if one_gpu else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_2403_19708_b200 import dist as pdist
     if world > 1:
-        pdist.init("nccl", dev)
+        pdist.init("gloo" if one_gpu else "nccl", dev)
+
 
     from paper_2403_19708_b200 import build as _build
     from paper_2403_19708_b200.metrics import percentile
@@ -433,11 +439,13 @@ def main():
         if world > 1:
             dist.barrier()
 
+    red_dev = torch.device("cpu") if one_gpu else dev
+
     def max_over_ranks(x: float) -> float:
-        return pdist.max_over_ranks(x, dev)
+        return pdist.max_over_ranks(x, red_dev)
 
     def sum_over_ranks(x: float) -> float:
-        return pdist.sum_over_ranks(x, dev)
+        return pdist.sum_over_ranks(x, red_dev)
 
     def timed(mode: str, steps: int, warmup: int, probe: bool = False, clocks=None):
         js = jobs[mode]
