@@ -559,6 +559,8 @@ def main():
     t_re = max_over_ranks(ms_re) * 1e-3
     # weak scaling: ranks serve disjoint sessions (sum); C5 TP: one replica (its tokens)
     tok_all = prompt_tokens if tp > 1 else sum_over_ranks(prompt_tokens)
+    new_all = new_tokens if tp > 1 else sum_over_ranks(new_tokens)
+    turns_all = len(turns) if tp > 1 else sum_over_ranks(len(turns))
     value = tok_all * args.steps / t_hbm
     e2e = tok_all * args.steps / t_host
     recompute = tok_all * steps_re / t_re
@@ -637,6 +639,12 @@ def main():
                             f"sessions sharded, no collective ({world} independent ranks)")},
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d_step,
                 "d2h_bytes_per_step": d2h_step, "ms_per_step": ms_host / args.steps},
+        # SURVEY.md §8d/§8e companions: new-token throughput and sessions (turns)/s,
+        # whole job (all ranks), HBM-resident and host-link modes
+        "new_tokens_per_s": {"value_mode": new_all * args.steps / t_hbm,
+                             "e2e_mode": new_all * args.steps / t_host},
+        "sessions_per_s": {"value_mode": turns_all * args.steps / t_hbm,
+                           "e2e_mode": turns_all * args.steps / t_host},
         "recompute": {"value": recompute, "unit": "tokens/s",
                       "ms_per_step": ms_re / steps_re},
         "speedup_vs_recompute": {"value_mode": value / recompute, "e2e_mode": e2e / recompute},
