@@ -78,30 +78,47 @@ __global__ void __launch_bounds__(kNormThreads)
   }
 }
 
+// grid.y = row, grid.x strides the row's 16-byte vectors with kSiluIlp of
+// them in flight per thread (no 64-bit division per vector).
+constexpr int kSiluIlp = 4;
+
 __global__ void __launch_bounds__(256)
     silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out,
-                    int rows, int ffn) {
+                    int ffn) {
   const int vpr = ffn / 8;
-  const int64_t total = (int64_t)rows * vpr;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(i / vpr);
-    const int c = (int)(i - (int64_t)r * vpr);
-    const uint4 g = reinterpret_cast<const uint4*>(gu + (int64_t)r * 2 * ffn)[c];
-    const uint4 u = reinterpret_cast<const uint4*>(gu + (int64_t)r * 2 * ffn + ffn)[c];
-    const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&g);
-    const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&u);
-    uint4 o;
-    uint32_t* op = reinterpret_cast<uint32_t*>(&o);
+  const int r = blockIdx.y;
+  const uint4* gr = reinterpret_cast<const uint4*>(gu + (int64_t)r * 2 * ffn);
+  const uint4* ur = gr + vpr;
+  uint4* orow = reinterpret_cast<uint4*>(out + (int64_t)r * ffn);
+  for (int c0 = blockIdx.x * 256 * kSiluIlp + threadIdx.x; c0 < vpr;
+       c0 += gridDim.x * 256 * kSiluIlp) {
+    uint4 g[kSiluIlp], u[kSiluIlp];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float2 a = __bfloat1622float2(gh[k]);
-      const float2 b = __bfloat1622float2(uh[k]);
-      __nv_bfloat162 r2 = __floats2bfloat162_rn(a.x / (1.f + __expf(-a.x)) * b.x,
-                                                a.y / (1.f + __expf(-a.y)) * b.y);
-      op[k] = *reinterpret_cast<uint32_t*>(&r2);
+    for (int k = 0; k < kSiluIlp; ++k) {
+      const int c = c0 + k * 256;
+      if (c < vpr) {
+        g[k] = gr[c];
+        u[k] = ur[c];
+      }
     }
-    reinterpret_cast<uint4*>(out + (int64_t)r * ffn)[c] = o;
+#pragma unroll
+    for (int k = 0; k < kSiluIlp; ++k) {
+      const int c = c0 + k * 256;
+      if (c >= vpr) break;
+      const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&g[k]);
+      const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&u[k]);
+      uint4 o;
+      uint32_t* op = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 a = __bfloat1622float2(gh[e]);
+        const float2 b = __bfloat1622float2(uh[e]);
+        __nv_bfloat162 r2 = __floats2bfloat162_rn(__fdividef(a.x, 1.f + __expf(-a.x)) * b.x,
+                                                  __fdividef(a.y, 1.f + __expf(-a.y)) * b.y);
+        op[e] = *reinterpret_cast<uint32_t*>(&r2);
+      }
+      orow[c] = o;
+    }
   }
 }
 
@@ -139,13 +156,10 @@ extern "C" int askv_silu_mul(const void* gu, void* out, int rows, int ffn, void*
                ffn);
   if (rows == 0) return ASKV_OK;
   ASKV_REQUIRE(gu && out, "silu_mul: null pointer");
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t units = (int64_t)rows * (ffn / 8);
-  int64_t grid = (units + 255) / 256;
-  if (grid > (int64_t)sms * 8) grid = (int64_t)sms * 8;
-  silu_mul_kernel<<<(int)grid, 256, 0, (cudaStream_t)stream>>>(
-      static_cast<const __nv_bfloat16*>(gu), static_cast<__nv_bfloat16*>(out), rows, ffn);
+  ASKV_REQUIRE(rows <= 65535, "silu_mul: %d rows exceed the grid's y limit", rows);
+  const int vpr = ffn / 8;
+  const dim3 grid((vpr + 256 * kSiluIlp - 1) / (256 * kSiluIlp), rows);
+  silu_mul_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      static_cast<const __nv_bfloat16*>(gu), static_cast<__nv_bfloat16*>(out), ffn);
   return launch_status("silu_mul launch");
 }
