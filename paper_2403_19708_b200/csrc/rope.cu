@@ -159,6 +159,10 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// grid.y = new token, grid.x strides its 16-byte vectors (q heads, then K, V)
+// with kRopeIlp loads in flight per thread.
+constexpr int kRopeIlp = 4;
+
 template <int HD>
 __global__ void __launch_bounds__(kThreads)
     rope_new_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t qkv_row_stride, int n_new,
@@ -169,20 +173,30 @@ __global__ void __launch_bounds__(kThreads)
   const int q_units = hq * kUnitsPerHead;
   const int k_units = hkv * kUnitsPerHead;
   const int row_units = q_units + 2 * k_units;
-  const int64_t total = (int64_t)n_new * row_units;
-  for (int64_t g = blockIdx.x * (int64_t)kThreads + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * kThreads) {
-    const int i = (int)(g / row_units);
-    const int u = (int)(g - (int64_t)i * row_units);
-    const int4 x = ld_nc16(qkv + (int64_t)i * qkv_row_stride + u * 8);
-    const int d0 = (u % kUnitsPerHead) * 8;
-    const float* cs = table + ((int64_t)(pos0 + i) * (HD / 2) + d0 / 2) * 2;
-    if (u < q_units) {
-      st16(q_out + (int64_t)i * q_units * 8 + u * 8, rotate8(x, cs));
-    } else {
-      const int ku = u - q_units;  // [0, 2*k_units): K then V, same as the row layout
-      if (save_out != nullptr) st16(save_out + (int64_t)i * 2 * k_units * 8 + ku * 8, x);
-      st16_keep(kv_out + (int64_t)i * kv_row_stride + ku * 8, ku < k_units ? rotate8(x, cs) : x);
+  const int i = blockIdx.y;
+  const __nv_bfloat16* src = qkv + (int64_t)i * qkv_row_stride;
+  const float* cs_row = table + (int64_t)(pos0 + i) * HD;  // (cos, sin) x HD/2
+  for (int u0 = blockIdx.x * kThreads * kRopeIlp + threadIdx.x; u0 < row_units;
+       u0 += gridDim.x * kThreads * kRopeIlp) {
+    int4 x[kRopeIlp];
+#pragma unroll
+    for (int k = 0; k < kRopeIlp; ++k) {
+      const int u = u0 + k * kThreads;
+      if (u < row_units) x[k] = ld_nc16(src + u * 8);
+    }
+#pragma unroll
+    for (int k = 0; k < kRopeIlp; ++k) {
+      const int u = u0 + k * kThreads;
+      if (u >= row_units) break;
+      const float* cs = cs_row + (u % kUnitsPerHead) * 8;
+      if (u < q_units) {
+        st16(q_out + (int64_t)i * q_units * 8 + u * 8, rotate8(x[k], cs));
+      } else {
+        const int ku = u - q_units;  // [0, 2*k_units): K then V, same as the row layout
+        if (save_out != nullptr) st16(save_out + (int64_t)i * 2 * k_units * 8 + ku * 8, x[k]);
+        st16_keep(kv_out + (int64_t)i * kv_row_stride + ku * 8,
+                  ku < k_units ? rotate8(x[k], cs) : x[k]);
+      }
     }
   }
 }
@@ -286,8 +300,9 @@ extern "C" int askv_rope_new(const void* qkv, int64_t qkv_row_stride, int n_new,
                "rope_new: row strides must be multiples of 8 elements");
   if (n_new == 0) return ASKV_OK;
   ASKV_REQUIRE(qkv && q_out && kv_out && rope_table, "rope_new: null pointer");
-  const int64_t units = (int64_t)n_new * (n_heads + 2 * n_kv_heads) * (head_dim / 8);
-  const int grid = grid_for(units);
+  ASKV_REQUIRE(n_new <= 65535, "rope_new: %d new tokens exceed the grid's y limit", n_new);
+  const int row_units = (n_heads + 2 * n_kv_heads) * (head_dim / 8);
+  const dim3 grid((row_units + kThreads * kRopeIlp - 1) / (kThreads * kRopeIlp), n_new);
   auto* x = static_cast<const __nv_bfloat16*>(qkv);
   auto* qo = static_cast<__nv_bfloat16*>(q_out);
   auto* kvo = static_cast<__nv_bfloat16*>(kv_out);
