@@ -410,8 +410,10 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   // Graph issue: one launch per job instead of ~11 per layer.  While the
   // pre-loader saturates the host link, every stream launch's command fetch
-  // queues behind the H2D DMA and the GPU idles between kernels (r02
-  // profiles); a graph's nodes are resident on the device.  The tensor-parallel
+  // queues behind the H2D DMA and the GPU idles between kernels
+  // (profiles/r01d_summary.md); a graph's nodes are resident on the device.
+  // If the driver refuses the capture or the instantiation, the job is issued
+  // on the stream instead (same kernels, same order).  The tensor-parallel
   // host callback and the HBM-tier promotion (batched D2D copies) issue as
   // streams.
   if (!p->graph || p->allreduce || p->promote_base) return issue_layers(p, s);
@@ -430,7 +432,11 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
     if (g) cudaGraphDestroy(g);
     return rc;
   }
-  if (ec != cudaSuccess) return cuda_status(ec, "cudaStreamEndCapture");
+  if (ec != cudaSuccess) {  // capture invalidated: issue on the stream
+    cudaGetLastError();
+    if (g) cudaGraphDestroy(g);
+    return issue_layers(p, s);
+  }
   const auto key = graph_key(p, s);
   std::lock_guard<std::mutex> lk(g_graph_mu);
   auto it = g_graphs.find(key);
@@ -460,10 +466,12 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
     GraphEntry e;
     cudaError_t ei = cudaGraphInstantiate(&e.exec, g, 0);
     if (ei == cudaSuccess) ei = cudaEventCreateWithFlags(&e.done, cudaEventDisableTiming);
-    if (ei != cudaSuccess) {
+    if (ei != cudaSuccess) {  // not instantiable: issue on the stream
       if (e.exec) cudaGraphExecDestroy(e.exec);
       cudaGraphDestroy(g);
-      return cuda_status(ei, "cudaGraphInstantiate");
+      cudaGetLastError();
+      clear_error();
+      return issue_layers(p, s);
     }
     it = g_graphs.emplace(key, e).first;
   }
