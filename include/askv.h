@@ -223,13 +223,15 @@ typedef struct askv_prefill_plan {
   int64_t block_bytes, chunk_bytes, row_bytes;
   /* Optional device timestamps (globaltimer ns, written by 1-thread stamp
    * kernels on `stream`; CUDA timing events cost ~24 us each while the host
-   * link is saturated, see profiles/r02_summary.md).  Layout:
+   * link is saturated, see profiles/r01d_summary.md).  Layout:
    *   stamps[0]                 loop begin
    *   stamps[1 + 7*l + 0]       layer l end
    *   stamps[1 + 7*l + 1 / 2]   pre-load wait begin / end   (stamp_flags & 1, with ev_src_ready)
    *   stamps[1 + 7*l + 3 / 4]   K2 re-embed begin / end     (stamp_flags & 2, kept > 0 and a source)
    *   stamps[1 + 7*l + 5 / 6]   K3 attention begin / end    (stamp_flags & 2)
-   * Entries whose stage does not run are left untouched. */
+   * K2 / K3 write their own pair (no extra launch): begin = start of CTA 0,
+   * end = latest CTA end (incl. the split-KV combine).  Entries whose stage
+   * does not run are left untouched. */
   uint64_t* stamps;
   int32_t stamp_flags;
   void (*allreduce)(void* ptr, int64_t elems, void* stream, void* ctx);

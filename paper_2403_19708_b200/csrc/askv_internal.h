@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 #include <cstdarg>
 #include <cstdio>
 #include <string>
@@ -29,5 +31,18 @@ inline int launch_status(const char* what) { return cuda_status(cudaGetLastError
       return ASKV_EINVAL;                \
     }                                    \
   } while (0)
+
+// Entry points of the native layer loop with in-kernel launch timestamps
+// ({begin, end} globaltimer ns, see attention.cu launch_stamp_*); the C ABI
+// functions call these with stamp == nullptr.
+int prefill_attn_stamped(const void* q, const void* kv, int64_t kv_row_stride, int n_cached,
+                         int n_new, int n_heads, int n_kv_heads, int head_dim, float scale,
+                         void* out, void* workspace, size_t workspace_bytes, int num_splits,
+                         void* stream, unsigned long long* stamp);
+int reembed_stamped(const void* src_base, const int64_t* src_block_off, int block_tokens,
+                    int64_t src_row_stride, int64_t first_token, int kept, int n_kv_heads,
+                    int head_dim, const float* rope_table, int table_positions,
+                    const int32_t* positions, int pos0, void* dst, int64_t dst_row_stride,
+                    void* stream, unsigned long long* stamp);
 
 }  // namespace askv

@@ -45,6 +45,23 @@ __device__ __forceinline__ void trace_stamp(int slot) {
 #define ATTN_TRACE(slot) ((void)0)
 #endif
 
+// Launch timestamps without extra launches (bench probes, plan.stamps):
+// stamp[0] = globaltimer at the start of CTA (0,0,0) -- the first wave starts
+// together -- and stamp[1] = max over CTAs of their end time (atomicMax; the
+// ring slot's stale value is an older, smaller time, so no reset is needed).
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void launch_stamp_begin(unsigned long long* st) {
+  if (st && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+    st[0] = gtimer();
+}
+__device__ __forceinline__ void launch_stamp_end(unsigned long long* st) {
+  if (st && threadIdx.x == 0) atomicMax(st + 1, gtimer());
+}
+
 constexpr int kBM = 128;  // query rows per tile (UMMA M)
 constexpr int kBN = 128;  // key rows per tile (UMMA N of S, K of PV)
 constexpr int kMaxSplits = 32;
@@ -58,6 +75,7 @@ struct AttnParams {
   int tiles_per_split;
   float scale_log2;
   __nv_bfloat16* out;  // [n_new][hq][HD]
+  unsigned long long* stamp;  // optional {begin, end} launch timestamps
   float* part_o;       // [splits][n_new][hq][HD]
   float* part_lse;     // [splits][n_new][hq]   (log2 units)
 };
@@ -140,6 +158,7 @@ __global__ void __launch_bounds__(320, 1)
   const int split = blockIdx.z;
   const int kh = h / p.group;
   if (threadIdx.x == 0) ATTN_TRACE(0);
+  launch_stamp_begin(p.stamp);
   // query tiles of this CTA: A at q0, B at q0 + 128 (paired only)
   const int q0 = blockIdx.x * kBM * C::kQTiles;
   const int rows_a = min(kBM, p.n_new - q0);
@@ -510,13 +529,15 @@ __global__ void __launch_bounds__(320, 1)
     tmem_dealloc(tmem, C::kTmemCols);
   }
   if (threadIdx.x == 0) ATTN_TRACE(4);
+  if (p.num_splits == 1) launch_stamp_end(p.stamp);
 }
 
 // Deterministic split-KV combine: one warp per (query, head), splits in order.
 template <int HD>
 __global__ void __launch_bounds__(128)
     attn_combine_kernel(const float* __restrict__ part_o, const float* __restrict__ part_lse,
-                        int num_splits, int rows, __nv_bfloat16* __restrict__ out) {
+                        int num_splits, int rows, __nv_bfloat16* __restrict__ out,
+                        unsigned long long* stamp) {
   const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -540,6 +561,7 @@ __global__ void __launch_bounds__(128)
   for (int e = 0; e < kPer; e += 2)
     *reinterpret_cast<__nv_bfloat162*>(dst + e) =
         __floats2bfloat162_rn(acc[e] * inv, acc[e + 1] * inv);
+  if (stamp && lane == 0) atomicMax(stamp + 1, gtimer());  // per warp: rows may exit early
 }
 
 // ---------------------------------------------------------------- host side
@@ -634,7 +656,7 @@ int choose_splits(int n_cached, int n_new, int hq, int sms) {
 template <int HD>
 int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cached, int n_new,
                 int hq, int hkv, float scale, void* out, void* ws, size_t ws_bytes,
-                int splits, cudaStream_t stream) {
+                int splits, cudaStream_t stream, unsigned long long* stamp) {
   const int rows = n_cached + n_new;
   CUtensorMap mq, mk, mv;
   int rc = make_map(&mq, q, HD, hq, HD, n_new, (int64_t)hq * HD);
@@ -659,6 +681,7 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
   prm.tiles_per_split = tps;
   prm.scale_log2 = scale * 1.4426950408889634f;
   prm.out = static_cast<__nv_bfloat16*>(out);
+  prm.stamp = stamp;
   prm.part_o = nullptr;
   prm.part_lse = nullptr;
   if (splits > 1) {
@@ -696,7 +719,7 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
   if (rc || splits == 1) return rc;
   const int rows_qh = n_new * hq;
   attn_combine_kernel<HD><<<(rows_qh + 3) / 4, 128, 0, stream>>>(
-      prm.part_o, prm.part_lse, splits, rows_qh, static_cast<__nv_bfloat16*>(out));
+      prm.part_o, prm.part_lse, splits, rows_qh, static_cast<__nv_bfloat16*>(out), stamp);
   return launch_status("attn_combine launch");
 }
 
@@ -723,6 +746,16 @@ extern "C" int askv_prefill_attn(const void* q, const void* kv, int64_t kv_row_s
                                  int head_dim, float scale, void* out, void* workspace,
                                  size_t workspace_bytes, int num_splits, void* stream) {
   clear_error();
+  return askv::prefill_attn_stamped(q, kv, kv_row_stride, n_cached, n_new, n_heads, n_kv_heads,
+                                    head_dim, scale, out, workspace, workspace_bytes, num_splits,
+                                    stream, nullptr);
+}
+
+int askv::prefill_attn_stamped(const void* q, const void* kv, int64_t kv_row_stride,
+                               int n_cached, int n_new, int n_heads, int n_kv_heads,
+                               int head_dim, float scale, void* out, void* workspace,
+                               size_t workspace_bytes, int num_splits, void* stream,
+                               unsigned long long* stamp) {
   ASKV_REQUIRE(n_cached >= 0 && n_new >= 0, "prefill_attn: negative lengths");
   ASKV_REQUIRE(n_heads > 0 && n_kv_heads > 0 && n_heads % n_kv_heads == 0,
                "prefill_attn: Hq=%d must be a positive multiple of Hkv=%d", n_heads,
@@ -739,7 +772,7 @@ extern "C" int askv_prefill_attn(const void* q, const void* kv, int64_t kv_row_s
   int splits = num_splits > 0 ? num_splits : choose_splits(n_cached, n_new, n_heads, sm_count());
   if (head_dim == 128)
     return launch_attn<128>(q, kv, kv_row_stride, n_cached, n_new, n_heads, n_kv_heads, scale,
-                            out, workspace, workspace_bytes, splits, (cudaStream_t)stream);
+                            out, workspace, workspace_bytes, splits, (cudaStream_t)stream, stamp);
   return launch_attn<64>(q, kv, kv_row_stride, n_cached, n_new, n_heads, n_kv_heads, scale, out,
-                         workspace, workspace_bytes, splits, (cudaStream_t)stream);
+                         workspace, workspace_bytes, splits, (cudaStream_t)stream, stamp);
 }

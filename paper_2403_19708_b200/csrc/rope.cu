@@ -103,9 +103,16 @@ __global__ void __launch_bounds__(kThreads)
     reembed_kernel(const __nv_bfloat16* __restrict__ src, const int64_t* __restrict__ blk_off,
                    int block_tokens, int64_t src_row_stride, int64_t first_token, int kept,
                    int hkv, const float* __restrict__ table, const int32_t* __restrict__ positions,
-                   int pos0, __nv_bfloat16* __restrict__ dst, int64_t dst_row_stride) {
+                   int pos0, __nv_bfloat16* __restrict__ dst, int64_t dst_row_stride,
+                   unsigned long long* __restrict__ stamp) {
   constexpr int kHalf = HD / 2;
   constexpr int kUnitsPerHead = HD / 8;
+  // optional launch timestamps {begin of CTA 0, max CTA end} (attention.cu)
+  if (stamp && threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    stamp[0] = t;
+  }
   __shared__ __align__(16) float cs_s[kReRows * kHalf * 2];
   __shared__ const __nv_bfloat16* srow_s[kReRows];
   const int row0 = blockIdx.x * kReRows;
@@ -155,6 +162,14 @@ __global__ void __launch_bounds__(kThreads)
         if (u < k_units) x = rotate8(x, cs_s + (rr * kHalf + (u % kUnitsPerHead) * 4) * 2);
         st16_keep(dst + (int64_t)(row0 + rr) * dst_row_stride + u * 8, x);
       }
+    }
+  }
+  if (stamp) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(stamp + 1, t);
     }
   }
 }
@@ -257,6 +272,17 @@ extern "C" int askv_reembed(const void* src_base, const int64_t* src_block_off,
                             int table_positions, const int32_t* positions, int pos0, void* dst,
                             int64_t dst_row_stride, void* stream) {
   clear_error();
+  return askv::reembed_stamped(src_base, src_block_off, block_tokens, src_row_stride,
+                               first_token, kept, n_kv_heads, head_dim, rope_table,
+                               table_positions, positions, pos0, dst, dst_row_stride, stream,
+                               nullptr);
+}
+
+int askv::reembed_stamped(const void* src_base, const int64_t* src_block_off, int block_tokens,
+                          int64_t src_row_stride, int64_t first_token, int kept, int n_kv_heads,
+                          int head_dim, const float* rope_table, int table_positions,
+                          const int32_t* positions, int pos0, void* dst, int64_t dst_row_stride,
+                          void* stream, unsigned long long* stamp) {
   ASKV_REQUIRE(kept >= 0 && n_kv_heads > 0 && first_token >= 0 && pos0 >= 0,
                "reembed: bad kept=%d hkv=%d first_token=%lld pos0=%d", kept, n_kv_heads,
                (long long)first_token, pos0);
@@ -276,11 +302,11 @@ extern "C" int askv_reembed(const void* src_base, const int64_t* src_block_off,
   if (head_dim == 128)
     reembed_kernel<128><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
         s, src_block_off, block_tokens, src_row_stride, first_token, kept, n_kv_heads,
-        rope_table, positions, pos0, d, dst_row_stride);
+        rope_table, positions, pos0, d, dst_row_stride, stamp);
   else
     reembed_kernel<64><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
         s, src_block_off, block_tokens, src_row_stride, first_token, kept, n_kv_heads,
-        rope_table, positions, pos0, d, dst_row_stride);
+        rope_table, positions, pos0, d, dst_row_stride, stamp);
   return launch_status("reembed launch");
 }
 

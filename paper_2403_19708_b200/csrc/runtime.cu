@@ -510,16 +510,19 @@ static int issue_layers(const askv_prefill_plan* p, cudaStream_t s) {
       if (p->ev_src_ready) stamp(p, 1, st + 1, s);
       wait(p->ev_src_ready, l, s);
       if (p->ev_src_ready) stamp(p, 1, st + 2, s);
-      stamp(p, 2, st + 3, s);
+      // probes: K2's own {first CTA begin, last CTA end} into stamps[st + 3 .. 4]
+      unsigned long long* k2_st = (p->stamps && (p->stamp_flags & 2))
+                                      ? reinterpret_cast<unsigned long long*>(p->stamps + st + 3)
+                                      : nullptr;
       if (p->src_kind == 1) {
-        ASKV_TRY(askv_reembed(p->src_layer[l], nullptr, 0, p->src_row_stride, p->head, p->kept,
-                              hkv, hd, p->rope_table, p->rope_positions, nullptr, 0, kv, row, s));
+        ASKV_TRY(reembed_stamped(p->src_layer[l], nullptr, 0, p->src_row_stride, p->head,
+                                 p->kept, hkv, hd, p->rope_table, p->rope_positions, nullptr, 0,
+                                 kv, row, s, k2_st));
       } else {
-        ASKV_TRY(askv_reembed(p->src_layer[l], p->src_block_off, p->block_tokens,
-                              p->src_row_stride, p->head, p->kept, hkv, hd, p->rope_table,
-                              p->rope_positions, nullptr, 0, kv, row, s));
+        ASKV_TRY(reembed_stamped(p->src_layer[l], p->src_block_off, p->block_tokens,
+                                 p->src_row_stride, p->head, p->kept, hkv, hd, p->rope_table,
+                                 p->rope_positions, nullptr, 0, kv, row, s, k2_st));
       }
-      stamp(p, 2, st + 4, s);
       if (p->promote_base) {  // HBM tier: keep the pre-loaded rows resident
         const auto* src = static_cast<const char*>(p->src_layer[l]) +
                           (int64_t)p->head * p->row_bytes;
@@ -529,10 +532,12 @@ static int issue_layers(const askv_prefill_plan* p, cudaStream_t s) {
       }
       rec(p->ev_src_free, l, s);
     }
-    stamp(p, 2, st + 5, s);
-    ASKV_TRY(askv_prefill_attn(p->q_rot, kv, row, p->kept, n, hq, hkv, hd, p->attn_scale,
-                               p->attn_out, p->attn_ws, p->attn_ws_bytes, p->attn_splits, s));
-    stamp(p, 2, st + 6, s);
+    ASKV_TRY(prefill_attn_stamped(
+        p->q_rot, kv, row, p->kept, n, hq, hkv, hd, p->attn_scale, p->attn_out, p->attn_ws,
+        p->attn_ws_bytes, p->attn_splits, s,
+        (p->stamps && (p->stamp_flags & 2))
+            ? reinterpret_cast<unsigned long long*>(p->stamps + st + 5)
+            : nullptr));
     if (p->allreduce) {  // tensor parallel: row-parallel W_o partial -> all-reduce -> residual
       ASKV_TRY(gemm(p->attn_out, p->w_o[l], p->h, n, d, hq * hd, false, p->gemm_ws,
                     p->gemm_ws_bytes, s));

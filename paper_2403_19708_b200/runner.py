@@ -714,8 +714,6 @@ class Runner:
             n_stamps = 0
             if lease:
                 n_stamps += L * (1 + (2 if rec.get("waited") else 0)) + 3   # + job begin/end, loop begin
-            if self.probe is not None:
-                n_stamps += L * (2 + (2 if reemb else 0))
             self.launches += L * (4 + (1 if kept and job.source != "resident" else 0)
                                   + (2 if splits > 1 else 1)
                                   + (2 if self.tp_reduce is not None else 0)) + n_stamps

@@ -24,6 +24,11 @@ METRICS = [
     ("gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "memory throughput"),
     ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
      "tensor pipe active (elapsed)"),
+    ("TPC.TriageCompute.sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg",
+     "tensor (hmma/tcgen05) subpipe active cycles per SM"),
+    ("sm__cycles_elapsed.avg", "SM cycles elapsed"),
+    ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+     "tensor memory (TMEM) active, % of active cycles"),
     ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU (MUFU) pipe"),
     ("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "issue slots busy (elapsed)"),
     ("launch__grid_size", "grid"),
