@@ -38,7 +38,7 @@ __device__ __forceinline__ void trace_stamp(int slot) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-  if (g_attn_trace) g_attn_trace[cta * 128 + slot] = t;
+  if (g_attn_trace) g_attn_trace[cta * 160 + slot] = t;
 }
 #define ATTN_TRACE(slot) trace_stamp(slot)
 #else
@@ -100,7 +100,7 @@ struct AttnParams {
 // TMEM (A operand in tensor memory); O accumulates in TMEM across tiles and is
 // rescaled in place only when a row max grows by more than 2^8.  K and V have
 // separate TMA rings.  Split-KV partials go to a deterministic combine kernel.
-// Warps: 0-3 WG0, 4-7 WG1, 8 TMA (+ TMEM alloc), 9 MMA.
+// Warps: 0-3 WG0, 4-7 WG1, 8 TMA Q + K (+ TMEM alloc), 9 MMA, 10 TMA V.
 // ============================================================================
 
 template <int HD, bool kAllowPair>
@@ -124,13 +124,13 @@ struct Cfg {
   // TMEM columns: S of group w at 128*w, O of group w at 256 + 128*w
   __host__ __device__ static constexpr uint32_t col_s(int w) { return 128u * (uint32_t)w; }
   __host__ __device__ static constexpr uint32_t col_o(int w) { return 256u + 128u * (uint32_t)w; }
-  static constexpr int kThreads = 320;
+  static constexpr int kThreads = 352;
   static constexpr float kRescaleLog2 = 8.0f;
   static_assert(kSmemBytes <= 232448, "smem budget");
 };
 
 template <int HD, bool kAllowPair>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(352, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
@@ -238,29 +238,32 @@ __global__ void __launch_bounds__(320, 1)
         for (int c = 0; c < C::kChunks; ++c)
           tma_load_3d_hint(sQ + t * C::kTileBytes + c * (kBM * 128), &tm_q, q_full, c * 64, h,
                            q0 + t * kBM, pol_q);
-      // K runs up to kKStages tiles ahead, V up to kVStages; interleave so a
-      // blocked V slot never holds back the next K.
-      int jk = 0, jv = 0;
-      while (jk < n_tiles || jv < n_tiles) {
-        if (jk < n_tiles && jk <= jv + C::kKStages - C::kVStages) {
-          const int st = jk % C::kKStages;
-          if (jk >= C::kKStages) mbar_wait(&k_empty[st], ((jk / C::kKStages) - 1) & 1);
-          mbar_expect_tx(&k_full[st], C::kTileBytes);
+      // K tiles: as far ahead as the K ring allows (S(j) needs K(j) well before
+      // PV(j) needs V(j)); V tiles come from warp 10, so a V slot still held by
+      // a PV in flight never delays the next K (in-kernel trace: with one
+      // ordered producer the MMA warp waited ~0.55 us per tile for K(j+2)).
+      for (int jk = 0; jk < n_tiles; ++jk) {
+        const int st = jk % C::kKStages;
+        if (jk >= C::kKStages) mbar_wait(&k_empty[st], ((jk / C::kKStages) - 1) & 1);
+        mbar_expect_tx(&k_full[st], C::kTileBytes);
 #pragma unroll
-          for (int c = 0; c < C::kChunks; ++c)
-            tma_load_3d_hint(sK + st * C::kTileBytes + c * (kBN * 128), &tm_k, &k_full[st],
-                             c * 64, kh, (t_begin + jk) * kBN, pol_kv);
-          ++jk;
-        } else {
-          const int st = jv % C::kVStages;
-          if (jv >= C::kVStages) mbar_wait(&v_empty[st], ((jv / C::kVStages) - 1) & 1);
-          mbar_expect_tx(&v_full[st], C::kTileBytes);
+        for (int c = 0; c < C::kChunks; ++c)
+          tma_load_3d_hint(sK + st * C::kTileBytes + c * (kBN * 128), &tm_k, &k_full[st],
+                           c * 64, kh, (t_begin + jk) * kBN, pol_kv);
+      }
+    }
+  } else if (warp == 10) {
+    // ------------------------------------------------------------ TMA producer (V)
+    if (lane == 0) {
+      const uint64_t pol_kv = l2_policy_evict_last();
+      for (int jv = 0; jv < n_tiles; ++jv) {
+        const int st = jv % C::kVStages;
+        if (jv >= C::kVStages) mbar_wait(&v_empty[st], ((jv / C::kVStages) - 1) & 1);
+        mbar_expect_tx(&v_full[st], C::kTileBytes);
 #pragma unroll
-          for (int c = 0; c < C::kChunks; ++c)
-            tma_load_3d_hint(sV + st * C::kTileBytes + c * (kBN * 128), &tm_v, &v_full[st],
-                             c * 64, kh, (t_begin + jv) * kBN, pol_kv);
-          ++jv;
-        }
+        for (int c = 0; c < C::kChunks; ++c)
+          tma_load_3d_hint(sV + st * C::kTileBytes + c * (kBN * 128), &tm_v, &v_full[st],
+                           c * 64, kh, (t_begin + jv) * kBN, pol_kv);
       }
     }
   } else if (warp == 9) {
@@ -337,11 +340,14 @@ __global__ void __launch_bounds__(320, 1)
         for (int j = 0; j < n_tiles; ++j) {
           const int w = j & 1;
           mbar_wait(&p_full[w], (j >> 1) & 1);
+          if (j < 28) ATTN_TRACE(64 + j);
           wait_v(j);
+          if (j < 28) ATTN_TRACE(96 + j);
           issue_pv(w, j, j < 2);
           umma_commit(&v_empty[j % C::kVStages]);
           if (j + 2 < n_tiles) {
             wait_k(j + 2);
+            if (j < 28) ATTN_TRACE(128 + j);
             issue_s(w, j + 2);
             umma_commit(&k_empty[(j + 2) % C::kKStages]);
           }
