@@ -103,32 +103,41 @@ const GemmPlan* plan_for(int m, int n, int k, bool accumulate, size_t ws_bytes) 
   cublasLtMatrixLayoutCreate(&p.a, CUDA_R_16BF, k, m, k);  // W: [m][k] row-major
   cublasLtMatrixLayoutCreate(&p.b, CUDA_R_16BF, k, n, k);  // x: [n][k] row-major
   cublasLtMatrixLayoutCreate(&p.c, CUDA_R_16BF, m, n, m);  // y: [n][m] row-major
-  cublasLtMatmulPreference_t pref = nullptr;
-  cublasLtMatmulPreferenceCreate(&pref);
-  cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws_bytes,
-                                       sizeof(ws_bytes));
-  cublasLtMatmulHeuristicResult_t res = {};
-  int found = 0;
-  cublasStatus_t st =
-      cublasLtMatmulAlgoGetHeuristic(h, p.op, p.a, p.b, p.c, p.c, pref, 1, &res, &found);
-  cublasLtMatmulPreferenceDestroy(pref);
-  if (st != CUBLAS_STATUS_SUCCESS || found == 0) return nullptr;
-  p.algo = res.algo;
-  p.ws = res.workspaceSize;
-  std::lock_guard<std::mutex> lk(g_mu);
-  auto tu = g_tuned.find(std::make_tuple(dev, m, k, n_bucket(n)));
-  if (tu != g_tuned.end()) {
-    cublasLtMatmulHeuristicResult_t chk = {};
-    if (cublasLtMatmulAlgoCheck(h, p.op, p.a, p.b, p.c, p.c, &tu->second.algo, &chk) ==
-            CUBLAS_STATUS_SUCCESS &&
-        chk.workspaceSize <= ws_bytes) {
-      p.algo = tu->second.algo;
-      p.ws = chk.workspaceSize;
-      if (getenv("ASKV_GEMM_DEBUG")) fprintf(stderr, "plan m=%d n=%d k=%d: tuned\n", m, n, k);
-    } else if (getenv("ASKV_GEMM_DEBUG")) {
-      fprintf(stderr, "plan m=%d n=%d k=%d: tuned algo rejected\n", m, n, k);
+  // the autotuned algorithm of n's bucket, when cuBLASLt accepts it for this
+  // exact n: no heuristic query (~1 ms of host time per new shape, which an
+  // isolated request with a new prompt length would pay before its first GEMM)
+  bool have = false;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto tu = g_tuned.find(std::make_tuple(dev, m, k, n_bucket(n)));
+    if (tu != g_tuned.end()) {
+      cublasLtMatmulHeuristicResult_t chk = {};
+      if (cublasLtMatmulAlgoCheck(h, p.op, p.a, p.b, p.c, p.c, &tu->second.algo, &chk) ==
+              CUBLAS_STATUS_SUCCESS &&
+          chk.workspaceSize <= ws_bytes) {
+        p.algo = tu->second.algo;
+        p.ws = chk.workspaceSize;
+        have = true;
+      }
     }
   }
+  if (!have) {
+    cublasLtMatmulPreference_t pref = nullptr;
+    cublasLtMatmulPreferenceCreate(&pref);
+    cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES,
+                                         &ws_bytes, sizeof(ws_bytes));
+    cublasLtMatmulHeuristicResult_t res = {};
+    int found = 0;
+    cublasStatus_t st =
+        cublasLtMatmulAlgoGetHeuristic(h, p.op, p.a, p.b, p.c, p.c, pref, 1, &res, &found);
+    cublasLtMatmulPreferenceDestroy(pref);
+    if (st != CUBLAS_STATUS_SUCCESS || found == 0) return nullptr;
+    p.algo = res.algo;
+    p.ws = res.workspaceSize;
+  }
+  if (getenv("ASKV_GEMM_DEBUG"))
+    fprintf(stderr, "plan m=%d n=%d k=%d: %s\n", m, n, k, have ? "tuned" : "heuristic");
+  std::lock_guard<std::mutex> lk(g_mu);
   auto ins = g_plans.emplace(key, p);
   return &ins.first->second;
 }
@@ -188,8 +197,8 @@ inline void stamp(const askv_prefill_plan* p, int flag, int idx, cudaStream_t s)
 // the graph's topology (sizes, which optional stages / events are present).
 // A hit re-captures the loop (new pointers / events) and applies it with
 // cudaGraphExecUpdate, which only affects later launches; a miss
-// instantiates.  Each entry keeps an event recorded after its last launch so
-// eviction never destroys an executable that is still running.
+// instantiates.  Each entry keeps an event recorded after its last launch;
+// replaced / evicted executables are destroyed only once it has completed.
 struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
   cudaEvent_t done = nullptr;
@@ -197,6 +206,23 @@ struct GraphEntry {
 };
 std::mutex g_graph_mu;
 std::map<std::vector<int64_t>, GraphEntry> g_graphs;
+// executables replaced or evicted while a launch of theirs may still run:
+// destroyed once their `done` event has completed (never a host sync here)
+std::vector<GraphEntry> g_retired;
+void retire(GraphEntry e) { g_retired.push_back(e); }
+void sweep_retired() {
+  for (size_t i = 0; i < g_retired.size();) {
+    if (cudaEventQuery(g_retired[i].done) == cudaSuccess) {
+      cudaGraphExecDestroy(g_retired[i].exec);
+      cudaEventDestroy(g_retired[i].done);
+      g_retired[i] = g_retired.back();
+      g_retired.pop_back();
+    } else {
+      ++i;
+    }
+  }
+  cudaGetLastError();  // cudaErrorNotReady from the queries
+}
 uint64_t g_graph_clock = 0;
 constexpr size_t kMaxGraphs = 96;
 
@@ -204,12 +230,14 @@ std::vector<int64_t> graph_key(const askv_prefill_plan* p, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   auto has = [](const void* q) -> int64_t { return q != nullptr; };
-  // `kept` only changes kernel parameters (grids, offsets), so jobs that differ
-  // only in it (every decode step) update one executable instead of
-  // instantiating a graph each; the split count and n (GEMM algorithms) shape
-  // the topology and stay in the key
-  return {dev, p->layers, p->d_model, p->n_heads, p->n_kv_heads, p->head_dim, p->ffn, p->n_new,
-          p->kept > 0, p->attn_splits, p->src_kind, p->block_tokens,
+  // `kept` and n within one GEMM-autotune bucket only change kernel parameters
+  // (grids, offsets, the same tuned GEMM kernels), so such jobs -- every decode
+  // step, prompts of nearby lengths -- update one executable instead of
+  // instantiating a graph each (~7 ms of host time for a 13B job); the split
+  // count shapes the topology and stays in the key.  An update that fails
+  // (different kernels) re-instantiates.
+  return {dev, p->layers, p->d_model, p->n_heads, p->n_kv_heads, p->head_dim, p->ffn,
+          n_bucket(p->n_new), p->kept > 0, p->attn_splits, p->src_kind, p->block_tokens,
           has(p->save_rows), has(p->ev_src_ready), has(p->ev_src_free), has(p->ev_save_free),
           has(p->ev_save_ready), p->stamps ? p->stamp_flags : -1, has(p->kv_layers),
           (int64_t)(intptr_t)s};
@@ -439,16 +467,15 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
   }
   const auto key = graph_key(p, s);
   std::lock_guard<std::mutex> lk(g_graph_mu);
+  sweep_retired();
   auto it = g_graphs.find(key);
   bool ready = false;
   if (it != g_graphs.end()) {
     cudaGraphExecUpdateResultInfo info;
     ready = cudaGraphExecUpdate(it->second.exec, g, &info) == cudaSuccess;
-    if (!ready) {
+    if (!ready) {  // different kernels under the same key: re-instantiate
       cudaGetLastError();
-      cudaEventSynchronize(it->second.done);
-      cudaGraphExecDestroy(it->second.exec);
-      cudaEventDestroy(it->second.done);
+      retire(it->second);
       g_graphs.erase(it);
       it = g_graphs.end();
     }
@@ -458,9 +485,7 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
       auto lru = g_graphs.begin();
       for (auto j = g_graphs.begin(); j != g_graphs.end(); ++j)
         if (j->second.last_use < lru->second.last_use) lru = j;
-      cudaEventSynchronize(lru->second.done);
-      cudaGraphExecDestroy(lru->second.exec);
-      cudaEventDestroy(lru->second.done);
+      retire(lru->second);
       g_graphs.erase(lru);
     }
     GraphEntry e;
