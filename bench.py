@@ -504,6 +504,26 @@ def main():
     for j in jobs["host"]:
         j.prestage = False
 
+    # isolated requests: one job on an idle GPU, wall clock from the host call
+    # to the first token on the host, with a prompt length the runner has not
+    # seen (n - 1): includes GEMM-plan / graph-update host work and launch
+    # latency, i.e. what a lone request waits (HBM-resident KV)
+    iso = []
+    for j in jobs["hbm"][:8]:
+        if j.n_new < 3:
+            continue
+        for cut, timed_run in ((2, False), (1, True)):   # warm server, then an unseen length
+            jj = Job(j.session_id + "/iso", j.token_ids[:-cut], kept=j.kept, source="hbm",
+                     block_ids=j.block_ids, save=False, dev_block_off=j.dev_block_off)
+            torch.cuda.synchronize()
+            w0 = time.perf_counter()
+            r = runner.run([jj])
+            r[0].first_token.numpy()
+            torch.cuda.synchronize()
+            if timed_run:
+                iso.append(time.perf_counter() - w0)
+            Runner.finalize(r)
+
     decode = None
     if dec_steps:
         from paper_2403_19708_b200.runner import ResidentKv
@@ -652,6 +672,11 @@ def main():
                        "reuse_hbm": ttft_hbm, "recompute": ttft_re,
                        "speedup_prestaged": ttft_re / ttft_pre if ttft_pre else None,
                        "speedup_saturated": ttft_re / ttft_host if ttft_host else None},
+        "ttft_isolated_hbm_s": {"p50": percentile(iso, 0.5) if iso else None,
+                                "turns": len(iso),
+                                "note": "one request on an idle, warm server (GPU idle), host "
+                                        "wall time from the call to the first token on the "
+                                        "host, prompt length not seen before"},
         "exposed_transfer_frac": {"host_saturated": stall_host / span_host,
                                   "host_prestaged": stall_pre / span_pre},
         "link_gbs_per_gpu": {"h2d": h2d_bytes / load_busy / 1e9 if load_busy else None,
