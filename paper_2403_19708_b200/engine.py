@@ -183,7 +183,9 @@ class Engine:
                              block_tokens=block_tokens, host_arena=self.arena,
                              hbm_arena=self.hbm.arena if self.hbm else None,
                              read_buffer_bytes=read_buffer_bytes, max_new=max_new,
-                             max_ctx=self.window + self.chunk, tp_reduce=tp_reduce)
+                             max_ctx=self.window + self.chunk, tp_reduce=tp_reduce,
+                             # tune the GEMMs over full prompts too (misses recompute them)
+                             autotune=self.window + self.chunk + max_new)
         self.context: dict[str, int] = {}
         self.tokens: dict[str, torch.Tensor] = {}   # conversation token ids (for misses)
 
