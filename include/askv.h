@@ -221,17 +221,19 @@ typedef struct askv_prefill_plan {
   const int64_t* promote_block_ids; /* host array */
   int32_t promote_nblocks;
   int64_t block_bytes, chunk_bytes, row_bytes;
-  /* Optional device timestamps (globaltimer ns, written by 1-thread stamp
-   * kernels on `stream`; CUDA timing events cost ~24 us each while the host
-   * link is saturated, see profiles/r01d_summary.md).  Layout:
-   *   stamps[0]                 loop begin
-   *   stamps[1 + 7*l + 0]       layer l end
-   *   stamps[1 + 7*l + 1 / 2]   pre-load wait begin / end   (stamp_flags & 1, with ev_src_ready)
-   *   stamps[1 + 7*l + 3 / 4]   K2 re-embed begin / end     (stamp_flags & 2, kept > 0 and a source)
-   *   stamps[1 + 7*l + 5 / 6]   K3 attention begin / end    (stamp_flags & 2)
-   * K2 / K3 write their own pair (no extra launch): begin = start of CTA 0,
-   * end = latest CTA end (incl. the split-KV combine).  Entries whose stage
-   * does not run are left untouched. */
+  /* Optional device timestamps (globaltimer ns).  CUDA timing events cost
+   * ~24 us each on a stream while the host link is saturated
+   * (profiles/r01d_summary.md), so the kernels that bound each interval write
+   * them themselves (start of CTA 0 / atomicMax of CTA ends); one 1-thread
+   * stamp kernel marks the last layer's end.  Layout:
+   *   stamps[0]                 loop begin (start of layer 0's input rmsnorm)   (flags & 1)
+   *   stamps[1 + 7*l + 0]       layer l end (start of layer l+1's input rmsnorm) (flags & 1)
+   *   stamps[1 + 7*l + 1]       pre-load wait begin (end of rope_new)  (flags & 1, ev_src_ready)
+   *   stamps[1 + 7*l + 3 / 4]   K2 re-embed begin / end; the begin is also the
+   *                             pre-load wait end  (flags & 2, or flags & 1 with ev_src_ready)
+   *   stamps[1 + 7*l + 5 / 6]   K3 attention begin / end incl. the split-KV combine (flags & 2)
+   * stamps[1 + 7*l + 2] is unused.  Entries whose stage does not run are left
+   * untouched. */
   uint64_t* stamps;
   int32_t stamp_flags;
   void (*allreduce)(void* ptr, int64_t elems, void* stream, void* ctx);

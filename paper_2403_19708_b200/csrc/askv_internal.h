@@ -39,6 +39,12 @@ int prefill_attn_stamped(const void* q, const void* kv, int64_t kv_row_stride, i
                          int n_new, int n_heads, int n_kv_heads, int head_dim, float scale,
                          void* out, void* workspace, size_t workspace_bytes, int num_splits,
                          void* stream, unsigned long long* stamp);
+int rmsnorm_stamped(const void* x, const void* w, void* y, int rows, int cols, float eps,
+                    void* stream, unsigned long long* begin);
+int rope_new_stamped(const void* qkv, int64_t qkv_row_stride, int n_new, int n_heads,
+                     int n_kv_heads, int head_dim, const float* rope_table, int table_positions,
+                     int pos0, void* q_out, void* kv_out, int64_t kv_row_stride, void* save_out,
+                     void* stream, unsigned long long* end);
 int reembed_stamped(const void* src_base, const int64_t* src_block_off, int block_tokens,
                     int64_t src_row_stride, int64_t first_token, int kept, int n_kv_heads,
                     int head_dim, const float* rope_table, int table_positions,

@@ -28,8 +28,14 @@ __device__ __forceinline__ float warp_sum(float v) {
 template <int VPT>
 __global__ void __launch_bounds__(kNormThreads)
     rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
-                   __nv_bfloat16* __restrict__ y, int cols, float eps) {
+                   __nv_bfloat16* __restrict__ y, int cols, float eps,
+                   unsigned long long* __restrict__ begin) {
   const int row = blockIdx.x;
+  if (begin && row == 0 && threadIdx.x == 0) {  // timeline: start of CTA 0 (runtime.cu)
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *begin = t;
+  }
   const int nvec = cols / 8;
   const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)row * cols);
   uint4 v[VPT];
@@ -130,6 +136,11 @@ using namespace askv;
 extern "C" int askv_rmsnorm(const void* x, const void* w, void* y, int rows, int cols,
                             float eps, void* stream) {
   clear_error();
+  return askv::rmsnorm_stamped(x, w, y, rows, cols, eps, stream, nullptr);
+}
+
+int askv::rmsnorm_stamped(const void* x, const void* w, void* y, int rows, int cols, float eps,
+                          void* stream, unsigned long long* begin) {
   ASKV_REQUIRE(rows >= 0 && cols > 0 && cols % 8 == 0 && cols <= 8 * 8 * kNormThreads,
                "rmsnorm: cols %d must be a multiple of 8 and <= 16384", cols);
   if (rows == 0) return ASKV_OK;
@@ -141,11 +152,11 @@ extern "C" int askv_rmsnorm(const void* x, const void* w, void* y, int rows, int
   auto* yo = static_cast<__nv_bfloat16*>(y);
   cudaStream_t s = (cudaStream_t)stream;
   switch (vpt) {
-    case 1: rmsnorm_kernel<1><<<rows, kNormThreads, 0, s>>>(xi, wi, yo, cols, eps); break;
-    case 2: rmsnorm_kernel<2><<<rows, kNormThreads, 0, s>>>(xi, wi, yo, cols, eps); break;
-    case 3: rmsnorm_kernel<3><<<rows, kNormThreads, 0, s>>>(xi, wi, yo, cols, eps); break;
-    case 4: rmsnorm_kernel<4><<<rows, kNormThreads, 0, s>>>(xi, wi, yo, cols, eps); break;
-    default: rmsnorm_kernel<8><<<rows, kNormThreads, 0, s>>>(xi, wi, yo, cols, eps); break;
+    case 1: rmsnorm_kernel<1><<<rows, kNormThreads, 0, s>>>(xi, wi, yo, cols, eps, begin); break;
+    case 2: rmsnorm_kernel<2><<<rows, kNormThreads, 0, s>>>(xi, wi, yo, cols, eps, begin); break;
+    case 3: rmsnorm_kernel<3><<<rows, kNormThreads, 0, s>>>(xi, wi, yo, cols, eps, begin); break;
+    case 4: rmsnorm_kernel<4><<<rows, kNormThreads, 0, s>>>(xi, wi, yo, cols, eps, begin); break;
+    default: rmsnorm_kernel<8><<<rows, kNormThreads, 0, s>>>(xi, wi, yo, cols, eps, begin); break;
   }
   return launch_status("rmsnorm launch");
 }

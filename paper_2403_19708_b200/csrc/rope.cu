@@ -183,7 +183,8 @@ __global__ void __launch_bounds__(kThreads)
     rope_new_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t qkv_row_stride, int n_new,
                     int hq, int hkv, const float* __restrict__ table, int pos0,
                     __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ kv_out,
-                    int64_t kv_row_stride, __nv_bfloat16* __restrict__ save_out) {
+                    int64_t kv_row_stride, __nv_bfloat16* __restrict__ save_out,
+                    unsigned long long* __restrict__ end) {
   constexpr int kUnitsPerHead = HD / 8;
   const int q_units = hq * kUnitsPerHead;
   const int k_units = hkv * kUnitsPerHead;
@@ -212,6 +213,14 @@ __global__ void __launch_bounds__(kThreads)
         st16_keep(kv_out + (int64_t)i * kv_row_stride + ku * 8,
                   ku < k_units ? rotate8(x[k], cs) : x[k]);
       }
+    }
+  }
+  if (end) {  // timeline: latest CTA end (runtime.cu, the pre-load wait begins here)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(end, t);
     }
   }
 }
@@ -315,6 +324,16 @@ extern "C" int askv_rope_new(const void* qkv, int64_t qkv_row_stride, int n_new,
                              int table_positions, int pos0, void* q_out, void* kv_out,
                              int64_t kv_row_stride, void* save_out, void* stream) {
   clear_error();
+  return askv::rope_new_stamped(qkv, qkv_row_stride, n_new, n_heads, n_kv_heads, head_dim,
+                                rope_table, table_positions, pos0, q_out, kv_out, kv_row_stride,
+                                save_out, stream, nullptr);
+}
+
+int askv::rope_new_stamped(const void* qkv, int64_t qkv_row_stride, int n_new, int n_heads,
+                           int n_kv_heads, int head_dim, const float* rope_table,
+                           int table_positions, int pos0, void* q_out, void* kv_out,
+                           int64_t kv_row_stride, void* save_out, void* stream,
+                           unsigned long long* end) {
   ASKV_REQUIRE(n_new >= 0 && n_heads > 0 && n_kv_heads > 0 && n_heads % n_kv_heads == 0,
                "rope_new: bad n_new=%d hq=%d hkv=%d", n_new, n_heads, n_kv_heads);
   ASKV_REQUIRE(head_dim == 64 || head_dim == 128, "rope_new: head_dim %d unsupported",
@@ -336,11 +355,11 @@ extern "C" int askv_rope_new(const void* qkv, int64_t qkv_row_stride, int n_new,
   if (head_dim == 128)
     rope_new_kernel<128><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
         x, qkv_row_stride, n_new, n_heads, n_kv_heads, rope_table, pos0, qo, kvo,
-        kv_row_stride, so);
+        kv_row_stride, so, end);
   else
     rope_new_kernel<64><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
         x, qkv_row_stride, n_new, n_heads, n_kv_heads, rope_table, pos0, qo, kvo,
-        kv_row_stride, so);
+        kv_row_stride, so, end);
   return launch_status("rope_new launch");
 }
 

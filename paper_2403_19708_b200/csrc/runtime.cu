@@ -519,26 +519,34 @@ static int issue_layers(const askv_prefill_plan* p, cudaStream_t s) {
             hd = p->head_dim, f = p->ffn;
   const int qkv_cols = (hq + 2 * hkv) * hd;
   const int64_t row = 2LL * hkv * hd;
-  stamp(p, 1, 0, s);
+  // Timeline stamps ride on the kernels that bound each interval (no extra
+  // launches): loop begin / previous layer end = start of the layer's input
+  // rmsnorm, pre-load wait begin = end of rope_new, wait end = start of K2;
+  // one stamp kernel marks the end of the last layer.
+  const bool tl = p->stamps && (p->stamp_flags & 1);
+  auto ts = [&](int idx) -> unsigned long long* {
+    return reinterpret_cast<unsigned long long*>(p->stamps + idx);
+  };
   for (int l = 0; l < p->layers; ++l) {
     auto* kv = static_cast<__nv_bfloat16*>(p->kv_layers ? p->kv_layers[l] : p->kv);
     const int st = 1 + 7 * l;
-    ASKV_TRY(askv_rmsnorm(p->x, p->w_in[l], p->h, n, d, p->rms_eps, s));
+    ASKV_TRY(rmsnorm_stamped(p->x, p->w_in[l], p->h, n, d, p->rms_eps, s,
+                             tl ? ts(l == 0 ? 0 : st - 7) : nullptr));
     ASKV_TRY(gemm(p->h, p->w_qkv[l], p->qkv, n, qkv_cols, d, false, p->gemm_ws,
                   p->gemm_ws_bytes, s));
     void* save_rows = p->save_rows ? p->save_rows[l] : nullptr;
     if (save_rows) wait(p->ev_save_free, l, s);
-    ASKV_TRY(askv_rope_new(p->qkv, qkv_cols, n, hq, hkv, hd, p->rope_table, p->rope_positions,
-                           p->kept, p->q_rot, kv + (int64_t)p->kept * row, row, save_rows, s));
+    const bool waits = tl && p->kept > 0 && p->src_kind != 0 && p->ev_src_ready;
+    ASKV_TRY(rope_new_stamped(p->qkv, qkv_cols, n, hq, hkv, hd, p->rope_table,
+                              p->rope_positions, p->kept, p->q_rot, kv + (int64_t)p->kept * row,
+                              row, save_rows, s, waits ? ts(st + 1) : nullptr));
     if (save_rows) rec(p->ev_save_ready, l, s);
     if (p->kept > 0 && p->src_kind != 0) {
-      if (p->ev_src_ready) stamp(p, 1, st + 1, s);
       wait(p->ev_src_ready, l, s);
-      if (p->ev_src_ready) stamp(p, 1, st + 2, s);
-      // probes: K2's own {first CTA begin, last CTA end} into stamps[st + 3 .. 4]
-      unsigned long long* k2_st = (p->stamps && (p->stamp_flags & 2))
-                                      ? reinterpret_cast<unsigned long long*>(p->stamps + st + 3)
-                                      : nullptr;
+      // K2's own {first CTA begin, last CTA end} into stamps[st + 3 .. 4]:
+      // the probes' K2 interval, and its begin is the pre-load wait's end
+      unsigned long long* k2_st =
+          (p->stamps && ((p->stamp_flags & 2) || waits)) ? ts(st + 3) : nullptr;
       if (p->src_kind == 1) {
         ASKV_TRY(reembed_stamped(p->src_layer[l], nullptr, 0, p->src_row_stride, p->head,
                                  p->kept, hkv, hd, p->rope_table, p->rope_positions, nullptr, 0,
@@ -587,7 +595,7 @@ static int issue_layers(const askv_prefill_plan* p, cudaStream_t s) {
     } else {
       ASKV_TRY(gemm(p->act, p->w_down[l], p->x, n, d, f, true, p->gemm_ws, p->gemm_ws_bytes, s));
     }
-    stamp(p, 1, st, s);
+    if (l == p->layers - 1) stamp(p, 1, st, s);
   }
   return launch_status("prefill_layers");
 }

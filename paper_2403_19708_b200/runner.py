@@ -712,8 +712,8 @@ class Runner:
             if self._cb_error is not None:
                 raise RuntimeError("tensor-parallel all-reduce failed") from self._cb_error
             n_stamps = 0
-            if lease:
-                n_stamps += L * (1 + (2 if rec.get("waited") else 0)) + 3   # + job begin/end, loop begin
+            if lease:   # job begin / end + the last layer's end (the rest ride on kernels)
+                n_stamps += 3
             self.launches += L * (4 + (1 if kept and job.source != "resident" else 0)
                                   + (2 if splits > 1 else 1)
                                   + (2 if self.tp_reduce is not None else 0)) + n_stamps
@@ -793,7 +793,7 @@ class Runner:
                 b = 3 + 7 * l
                 end_l = g(b)
                 if rec.get("waited"):
-                    wa, wb = g(b + 1), g(b + 2)
+                    wa, wb = g(b + 1), g(b + 3)   # rope_new end -> K2 begin
                     waits.append((wa, wb))
                     comp.extend([(begin, wa), (wb, end_l)])
                 else:
