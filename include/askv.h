@@ -245,8 +245,23 @@ typedef struct askv_prefill_plan {
   void* const* kv_layers;
   /* 1: capture the loop into a CUDA graph (cached per shape, updated in
    * place) and launch that; 0: issue every kernel on `stream`.  Ignored
-   * (stream issue) with `allreduce` or `promote_base` set. */
+   * (stream issue) with `allreduce` set. */
   int32_t graph;
+  /* Optional second attention KV buffer (same size as `kv`).  When set, with a
+   * pre-load source (src_kind 1/2), kv_layers NULL and neither allreduce nor
+   * promote_base, layers alternate between kv and kv_alt and K2 of layer l+1
+   * runs on a second stream alongside K3 of layer l, on the SMs K3 leaves idle
+   * (the pre-load wait of layer l is then observed before K3, stamps[1+7l+5]
+   * marks its end). */
+  void* kv_alt;
+  /* Optional HBM-tier write-through: right after rope_new,
+   * copy the layer's new pre-RoPE rows (save_rows) into rows
+   * [head + kept, head + kept + n_new) of these HBM-arena blocks, on `stream`,
+   * so every access to the tier (this copy, promote_base, K2 reads) is in one
+   * stream order. */
+  void* mirror_base;
+  const int64_t* mirror_block_ids; /* host array */
+  int32_t mirror_nblocks;
 } askv_prefill_plan;
 
 int askv_prefill_layers(const askv_prefill_plan* plan, void* stream);

@@ -81,7 +81,9 @@ class PrefillPlan(C.Structure):
         ("block_bytes", C.c_int64), ("chunk_bytes", C.c_int64), ("row_bytes", C.c_int64),
         ("stamps", C.c_void_p), ("stamp_flags", C.c_int32),
         ("allreduce", ALLREDUCE_FN), ("allreduce_ctx", C.c_void_p),
-        ("kv_layers", _pp), ("graph", C.c_int32),
+        ("kv_layers", _pp), ("graph", C.c_int32), ("kv_alt", C.c_void_p),
+        ("mirror_base", C.c_void_p), ("mirror_block_ids", C.POINTER(C.c_int64)),
+        ("mirror_nblocks", C.c_int32),
     ]
 
 

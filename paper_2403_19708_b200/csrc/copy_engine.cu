@@ -55,6 +55,16 @@ unsigned copy_flags() {
 int issue_batch(std::vector<void*>& dsts, std::vector<void*>& srcs, std::vector<size_t>& sizes,
                 cudaStream_t stream) {
   if (dsts.empty()) return ASKV_OK;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone) {
+    // inside a graph capture (the layer loop's HBM-tier copies): one memcpy
+    // node per segment; the batch API is not capturable
+    for (size_t i = 0; i < dsts.size(); ++i) {
+      cudaError_t e = cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDefault, stream);
+      if (e != cudaSuccess) return cuda_status(e, "cudaMemcpyAsync (captured)");
+    }
+    return ASKV_OK;
+  }
   cudaMemcpyAttributes attr = {};
   attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
   attr.flags = copy_flags();

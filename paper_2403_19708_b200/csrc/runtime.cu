@@ -240,6 +240,7 @@ std::vector<int64_t> graph_key(const askv_prefill_plan* p, cudaStream_t s) {
           n_bucket(p->n_new), p->kept > 0, p->attn_splits, p->src_kind, p->block_tokens,
           has(p->save_rows), has(p->ev_src_ready), has(p->ev_src_free), has(p->ev_save_free),
           has(p->ev_save_ready), p->stamps ? p->stamp_flags : -1, has(p->kv_layers),
+          has(p->kv_alt), has(p->mirror_base), p->mirror_nblocks, p->promote_nblocks,
           (int64_t)(intptr_t)s};
 }
 
@@ -444,7 +445,7 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
   // on the stream instead (same kernels, same order).  The tensor-parallel
   // host callback and the HBM-tier promotion (batched D2D copies) issue as
   // streams.
-  if (!p->graph || p->allreduce || p->promote_base) return issue_layers(p, s);
+  if (!p->graph || p->allreduce) return issue_layers(p, s);
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
     return issue_layers(p, s);  // caller is capturing already: record into its graph
@@ -507,6 +508,35 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
   return rc;
 }
 
+namespace askv {
+namespace {
+// Per-device side stream and internal events of the K2 || K3 overlap.  Inside
+// a capture the events become plain graph dependencies (a fork / join with the
+// main stream), outside they order the two streams.
+struct SideCtx {
+  cudaStream_t s2 = nullptr;
+  std::vector<cudaEvent_t> ev;  // [0] fork, [1] join, then (k2_done, k3_start) per layer
+};
+std::mutex g_side_mu;
+std::map<int, SideCtx> g_side;
+
+SideCtx* side_ctx(int layers) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_side_mu);
+  SideCtx& c = g_side[dev];
+  if (!c.s2 && cudaStreamCreateWithFlags(&c.s2, cudaStreamNonBlocking) != cudaSuccess)
+    return nullptr;
+  while ((int)c.ev.size() < 2 + 2 * layers) {
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    c.ev.push_back(e);
+  }
+  return &c;
+}
+}  // namespace
+}  // namespace askv
+
 static int issue_layers(const askv_prefill_plan* p, cudaStream_t s) {
   ASKV_REQUIRE(p->layers > 0 && p->n_new > 0 && p->kept >= 0 && p->head >= 0,
                "prefill_layers: bad layers=%d n_new=%d kept=%d", p->layers, p->n_new, p->kept);
@@ -527,8 +557,40 @@ static int issue_layers(const askv_prefill_plan* p, cudaStream_t s) {
   auto ts = [&](int idx) -> unsigned long long* {
     return reinterpret_cast<unsigned long long*>(p->stamps + idx);
   };
+  const bool reemb = p->kept > 0 && p->src_kind != 0;
+  const bool ovl = p->kv_alt && !p->kv_layers && reemb && !p->promote_base && !p->allreduce;
+  SideCtx* sc = ovl ? side_ctx(p->layers) : nullptr;
+  if (ovl && !sc) {
+    set_error("prefill_layers: side stream / events for the K2 overlap");
+    return ASKV_ECUDA;
+  }
+  auto kv_of = [&](int l) {
+    return static_cast<__nv_bfloat16*>(p->kv_layers ? p->kv_layers[l]
+                                       : (ovl && (l & 1)) ? p->kv_alt : p->kv);
+  };
+  // K2 of layer l on stream `ks`: wait for its pre-load, re-embed, release the slot
+  auto issue_k2 = [&](int l, cudaStream_t ks, unsigned long long* k2_st) -> int {
+    wait(p->ev_src_ready, l, ks);
+    if (p->src_kind == 1) {
+      ASKV_TRY(reembed_stamped(p->src_layer[l], nullptr, 0, p->src_row_stride, p->head,
+                               p->kept, hkv, hd, p->rope_table, p->rope_positions, nullptr, 0,
+                               kv_of(l), row, ks, k2_st));
+    } else {
+      ASKV_TRY(reembed_stamped(p->src_layer[l], p->src_block_off, p->block_tokens,
+                               p->src_row_stride, p->head, p->kept, hkv, hd, p->rope_table,
+                               p->rope_positions, nullptr, 0, kv_of(l), row, ks, k2_st));
+    }
+    return ASKV_OK;
+  };
+  if (ovl) {  // fork the side stream; layer 0's K2 starts right away
+    cudaEventRecord(sc->ev[0], s);
+    cudaStreamWaitEvent(sc->s2, sc->ev[0], 0);
+    ASKV_TRY(issue_k2(0, sc->s2, (p->stamp_flags & 2) && p->stamps ? ts(1 + 3) : nullptr));
+    rec(p->ev_src_free, 0, sc->s2);
+    cudaEventRecord(sc->ev[2], sc->s2);  // k2_done[0]
+  }
   for (int l = 0; l < p->layers; ++l) {
-    auto* kv = static_cast<__nv_bfloat16*>(p->kv_layers ? p->kv_layers[l] : p->kv);
+    auto* kv = kv_of(l);
     const int st = 1 + 7 * l;
     ASKV_TRY(rmsnorm_stamped(p->x, p->w_in[l], p->h, n, d, p->rms_eps, s,
                              tl ? ts(l == 0 ? 0 : st - 7) : nullptr));
@@ -536,26 +598,34 @@ static int issue_layers(const askv_prefill_plan* p, cudaStream_t s) {
                   p->gemm_ws_bytes, s));
     void* save_rows = p->save_rows ? p->save_rows[l] : nullptr;
     if (save_rows) wait(p->ev_save_free, l, s);
-    const bool waits = tl && p->kept > 0 && p->src_kind != 0 && p->ev_src_ready;
+    const bool waits = tl && reemb && p->ev_src_ready;
     ASKV_TRY(rope_new_stamped(p->qkv, qkv_cols, n, hq, hkv, hd, p->rope_table,
                               p->rope_positions, p->kept, p->q_rot, kv + (int64_t)p->kept * row,
                               row, save_rows, s, waits ? ts(st + 1) : nullptr));
     if (save_rows) rec(p->ev_save_ready, l, s);
-    if (p->kept > 0 && p->src_kind != 0) {
-      wait(p->ev_src_ready, l, s);
+    if (save_rows && p->mirror_base) {  // HBM tier write-through, in stream order
+      ASKV_TRY(askv_save_layer(p->mirror_base, p->mirror_block_ids, p->mirror_nblocks,
+                               p->block_bytes, (int64_t)l * p->chunk_bytes, p->block_tokens,
+                               p->row_bytes, p->head + p->kept, n, save_rows, s, nullptr));
+    }
+    if (ovl) {
+      // K2(l) ran on the side stream; K2(l+1) starts alongside K3(l) (its KV
+      // buffer was last read by K3(l-1), which precedes k3_start[l])
+      cudaStreamWaitEvent(s, sc->ev[2 + 2 * l], 0);
+      cudaEventRecord(sc->ev[3 + 2 * l], s);
+      if (l + 1 < p->layers) {
+        cudaStreamWaitEvent(sc->s2, sc->ev[3 + 2 * l], 0);
+        ASKV_TRY(issue_k2(l + 1, sc->s2,
+                          (p->stamp_flags & 2) && p->stamps ? ts(st + 7 + 3) : nullptr));
+        rec(p->ev_src_free, l + 1, sc->s2);
+        cudaEventRecord(sc->ev[2 + 2 * (l + 1)], sc->s2);
+      }
+    } else if (reemb) {
       // K2's own {first CTA begin, last CTA end} into stamps[st + 3 .. 4]:
       // the probes' K2 interval, and its begin is the pre-load wait's end
       unsigned long long* k2_st =
           (p->stamps && ((p->stamp_flags & 2) || waits)) ? ts(st + 3) : nullptr;
-      if (p->src_kind == 1) {
-        ASKV_TRY(reembed_stamped(p->src_layer[l], nullptr, 0, p->src_row_stride, p->head,
-                                 p->kept, hkv, hd, p->rope_table, p->rope_positions, nullptr, 0,
-                                 kv, row, s, k2_st));
-      } else {
-        ASKV_TRY(reembed_stamped(p->src_layer[l], p->src_block_off, p->block_tokens,
-                                 p->src_row_stride, p->head, p->kept, hkv, hd, p->rope_table,
-                                 p->rope_positions, nullptr, 0, kv, row, s, k2_st));
-      }
+      ASKV_TRY(issue_k2(l, s, k2_st));
       if (p->promote_base) {  // HBM tier: keep the pre-loaded rows resident
         const auto* src = static_cast<const char*>(p->src_layer[l]) +
                           (int64_t)p->head * p->row_bytes;
@@ -568,9 +638,7 @@ static int issue_layers(const askv_prefill_plan* p, cudaStream_t s) {
     ASKV_TRY(prefill_attn_stamped(
         p->q_rot, kv, row, p->kept, n, hq, hkv, hd, p->attn_scale, p->attn_out, p->attn_ws,
         p->attn_ws_bytes, p->attn_splits, s,
-        (p->stamps && (p->stamp_flags & 2))
-            ? reinterpret_cast<unsigned long long*>(p->stamps + st + 5)
-            : nullptr));
+        (p->stamps && ((p->stamp_flags & 2) || (ovl && waits))) ? ts(st + 5) : nullptr));
     if (p->allreduce) {  // tensor parallel: row-parallel W_o partial -> all-reduce -> residual
       ASKV_TRY(gemm(p->attn_out, p->w_o[l], p->h, n, d, hq * hd, false, p->gemm_ws,
                     p->gemm_ws_bytes, s));
@@ -596,6 +664,10 @@ static int issue_layers(const askv_prefill_plan* p, cudaStream_t s) {
       ASKV_TRY(gemm(p->act, p->w_down[l], p->x, n, d, f, true, p->gemm_ws, p->gemm_ws_bytes, s));
     }
     if (l == p->layers - 1) stamp(p, 1, st, s);
+  }
+  if (ovl) {  // join the side stream back into the main one
+    cudaEventRecord(sc->ev[1], sc->s2);
+    cudaStreamWaitEvent(s, sc->ev[1], 0);
   }
   return launch_status("prefill_layers");
 }

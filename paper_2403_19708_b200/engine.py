@@ -92,6 +92,10 @@ class HbmTier:
         self.arena = torch.empty(n_blocks * self.block_elems, dtype=torch.bfloat16,
                                  device=device)
         self.free = deque(range(n_blocks))
+        # block -> session that held it last; a session that gets such a block
+        # must order its writes after that session's in-flight saves (fence)
+        self.prev_owner: dict[int, str] = {}
+        self.fence: dict[str, set] = {}
         self.tab: dict[str, list[int]] = {}
         self.dropped: dict[str, int] = {}
         self.valid: set[str] = set()          # mirror holds every row the host holds
@@ -100,10 +104,22 @@ class HbmTier:
         self.hits = 0
         self.promotions = 0
 
+    def _release(self, sid: str, ids) -> None:
+        for b in ids:
+            self.prev_owner[b] = sid
+        self.free.extend(ids)
+
+    def _take(self, sid: str) -> int:
+        b = self.free.popleft()
+        prev = self.prev_owner.pop(b, None)
+        if prev is not None and prev != sid:
+            self.fence.setdefault(sid, set()).add(prev)
+        return b
+
     def drop(self, sid: str) -> None:
         ids = self.tab.pop(sid, None)
         if ids:
-            self.free.extend(ids)
+            self._release(sid, ids)
         self.dropped.pop(sid, None)
         self.valid.discard(sid)
         self.lru.pop(sid, None)
@@ -117,17 +133,17 @@ class HbmTier:
         self.dropped.setdefault(sid, host_dropped)
         k = host_dropped - self.dropped[sid]
         if k > 0:
-            self.free.extend(ids[:k])
+            self._release(sid, ids[:k])
             del ids[:k]
             self.dropped[sid] = host_dropped
         if len(ids) > len(host_tab):
-            self.free.extend(ids[len(host_tab):])
+            self._release(sid, ids[len(host_tab):])
             del ids[len(host_tab):]
         while len(ids) < len(host_tab):
             if not self.free and not self._evict(exclude=pinned | {sid}):
                 self.drop(sid)
                 return False
-            ids.append(self.free.popleft())
+            ids.append(self._take(sid))
         self.lru[sid] = None
         self.lru.move_to_end(sid)
         return True
@@ -333,6 +349,7 @@ class Engine:
                 if self._hbm_sync(sid):
                     hids = list(self.hbm.tab[sid])
                     job.mirror_block_ids = hids
+                    job.fence_sessions = self.hbm.fence.pop(sid, set())
                     if job.source == "resident":
                         pass
                     elif kept and resident:

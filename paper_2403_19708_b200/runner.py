@@ -138,6 +138,9 @@ class Job:
     mirror_block_ids: list | None = None
     promote_block_ids: list | None = None
     head: int = 0   # row of session token 0 inside block_ids[0] (store.head_row)
+    # sessions whose HBM-tier blocks this job's mirror / promotion reuses: their
+    # last saves (write-through on the save stream) must land first
+    fence_sessions: set = field(default_factory=set)
     prestage: bool = False  # start the job only once all its layers are pre-loaded
     # resident rotated KV (decode): the job writes all its
     # layers' rows into kv_cache; source "resident" = kept rows already there
@@ -280,9 +283,11 @@ class Runner:
                  read_buffer_bytes: int = 4 << 30, write_buffer_bytes: int = 2 << 30,
                  max_new: int = 1024, max_ctx: int | None = None, timeline: bool = True,
                  tp_reduce=None, gemm_workspace_bytes: int = 32 << 20, graph: bool = True,
-                 autotune: bool | int = True):
+                 autotune: bool | int = True, overlap: bool = False):
         self.shape = s = shape
         self.graph = graph   # issue each job's layer loop as one CUDA graph launch
+        # K2 of layer l+1 alongside K3 of layer l (second stream, two KV buffers)
+        self.overlap = overlap
         self.device = torch.device(device)
         self.w = weights or LlamaWeights(shape, seed=seed, device=device)
         self.block_tokens = block_tokens
@@ -506,11 +511,6 @@ class Runner:
                 ops.save_layer(arena, job.block_ids, self.block_bytes,
                                layer * self.chunk_bytes, self.block_tokens, self.row_bytes,
                                job.head + kept, n, self.wbuf[wslot], stream=ss)
-                if job.mirror_block_ids is not None:   # HBM tier, write-through
-                    ops.save_layer(self.hbm_arena, job.mirror_block_ids, self.block_bytes,
-                                   layer * self.chunk_bytes, self.block_tokens,
-                                   self.row_bytes, job.head + kept, n, self.wbuf[wslot],
-                                   stream=ss)
                 self._wdone[wslot].record(ss)
                 if sess_ev is not None:
                     sess_ev.record(ss)
@@ -579,7 +579,12 @@ class Runner:
             raise ValueError("hbm job needs dev_block_off")
         arena = None
         if job.save:
-            arena = self.hbm_arena if job.source == "hbm" else (
+            # an "hbm" job whose session lives in the HBM arena (bench value
+            # mode) saves there; an HBM-tier hit (mirror_block_ids set) keeps
+            # host DRAM as the backing store -- its block ids are host blocks --
+            # and the tier copy is the in-loop write-through
+            in_hbm = job.source == "hbm" and job.mirror_block_ids is None
+            arena = self.hbm_arena if in_hbm else (
                 self.host_arena.buffer if self.host_arena is not None else None)
             if arena is None:
                 raise RuntimeError("save requested but no arena for it")
@@ -601,13 +606,30 @@ class Runner:
         first = torch.empty(1, dtype=torch.int64, pin_memory=True)
         logits_out = None
         rec = {"saves": [], "loads": []}
+        # device inputs the caller made on its own stream (token ids, the HBM
+        # tier's block offsets) must land before the job reads them: torch
+        # streams are non-blocking, nothing else orders them
+        caller = torch.cuda.current_stream(self.device)
         with torch.cuda.stream(cs):
+            if caller.cuda_stream != cs.cuda_stream:
+                cs.wait_stream(caller)
+            # ... and stay allocated until the job's kernels have read them: the
+            # caching allocator only knows the stream they were made on, so a
+            # freed offsets tensor could otherwise be handed out (and
+            # overwritten) while K2 is still queued on the compute stream
+            for t in (job.dev_block_off, job.token_ids):
+                if t is not None and t.is_cuda:
+                    t.record_stream(cs)
             if job.source == "hbm" or job.mirror_block_ids is not None:
-                # HBM-tier rows written by this session's previous saves (save stream)
-                dep = self._last_save.get(job.session_id)
-                if dep is not None:
-                    dep[1].wait()
-                    dep[0].wait(cs)
+                # HBM-tier rows written by this session's previous saves (save
+                # stream), and blocks reassigned from other sessions whose
+                # write-through saves may still be in flight
+                for sid in {job.session_id, *job.fence_sessions}:
+                    dep = self._last_save.get(sid)
+                    if dep is not None:
+                        dep[1].wait()
+                        dep[0].wait(cs)
+
             units = None
             if kept and job.source == "host":
                 units = [self._acquire(jid, l) for l in range(L)]
@@ -648,6 +670,10 @@ class Runner:
                 p.kv_layers = arr(job.kv_cache.layer_ptrs())
             else:
                 p.kv = self._buf("kv", kept + n, self.row_elems).data_ptr()
+                if (self.overlap and kept and job.source in ("host", "hbm")
+                        and job.promote_block_ids is None and self.tp_reduce is None):
+                    p.kv_alt = self._buf("kv2", kept + n, self.row_elems).data_ptr()
+                    rec["overlap"] = True
             p.attn_out = self._buf("ao", n, hq * hd).data_ptr()
             p.gu = self._buf("gu", n, 2 * s.ffn).data_ptr()
             p.act = self._buf("act", n, s.ffn).data_ptr()
@@ -679,6 +705,14 @@ class Runner:
                 base = self.hbm_arena.data_ptr()
                 p.src_layer = arr([base + l * self.chunk_bytes for l in range(L)])
                 p.src_block_off = job.dev_block_off.data_ptr()
+            if job.save and job.mirror_block_ids is not None:
+                # HBM tier write-through inside the layer loop (compute-stream
+                # order with promotions and K2 reads of the tier)
+                mids = (C.c_int64 * len(job.mirror_block_ids))(*job.mirror_block_ids)
+                keep.append(mids)
+                p.mirror_base = self.hbm_arena.data_ptr()
+                p.mirror_block_ids = mids
+                p.mirror_nblocks = len(job.mirror_block_ids)
             wslots = []
             if job.save:
                 for _ in range(L):
@@ -792,8 +826,8 @@ class Runner:
             for l in range(L):
                 b = 3 + 7 * l
                 end_l = g(b)
-                if rec.get("waited"):
-                    wa, wb = g(b + 1), g(b + 3)   # rope_new end -> K2 begin
+                if rec.get("waited"):   # rope_new end -> K2 begin (K3 begin when overlapped)
+                    wa, wb = g(b + 1), g(b + (5 if rec.get("overlap") else 3))
                     waits.append((wa, wb))
                     comp.extend([(begin, wa), (wb, end_l)])
                 else:

@@ -429,3 +429,72 @@ def test_graph_issue_is_bit_identical_to_stream_issue():
         for blk in ta:
             assert torch.equal(engs[0].arena.buffer[blk * bb:(blk + 1) * bb],
                                engs[1].arena.buffer[blk * bb:(blk + 1) * bb]), (sid, blk)
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_k2_overlap_is_bit_identical(graph):
+    """K2 of layer l+1 issued on a second stream alongside K3 of layer l (two
+    alternating KV buffers) gives bit-identical logits and saved bytes to the
+    single-stream loop, graph-captured or not, host and HBM-tier sources."""
+    engine, model, runner = _mods()
+    from dataclasses import replace
+    shape = replace(model.shape("tiny"), context_window=64, layers=3)
+    w = runner.LlamaWeights(shape, seed=13)
+    engs = []
+    for ovl in (False, True):
+        e = engine.Engine(shape, host_blocks=64, block_tokens=16, weights=w, max_new=64,
+                          read_buffer_bytes=16 << 20, hbm_blocks=8)
+        e.runner.graph = graph
+        e.runner.overlap = ovl
+        e.arena.buffer.zero_()
+        engs.append(e)
+    rng = np.random.default_rng(13)
+    for k in range(5):
+        for sid in ("a", "b", "c"):
+            new_ids = torch.as_tensor(rng.integers(0, shape.vocab, 9 + k))
+            out_ids = torch.as_tensor(rng.integers(0, shape.vocab, 6))
+            a, b = (e.turn(sid, k, new_ids, out_ids, want_logits=True) for e in engs)
+            torch.cuda.synchronize()
+            assert (a.kept, a.drop, a.hit) == (b.kept, b.drop, b.hit)
+            assert torch.equal(a.result.logits, b.result.logits), (sid, k)
+    bb = engs[0].runner.block_bytes
+    for sid in ("a", "b", "c"):
+        for blk in engs[0].store.block_table(sid):
+            assert torch.equal(engs[0].arena.buffer[blk * bb:(blk + 1) * bb],
+                               engs[1].arena.buffer[blk * bb:(blk + 1) * bb]), (sid, blk)
+
+
+def test_hbm_tier_with_evictions_is_bit_identical_to_host_path():
+    """Three sessions over an 8-block HBM tier: sessions get evicted, their
+    blocks reassigned, and promoted again from host DRAM.  Every turn's logits
+    and every saved host row equal the host-only engine's (a tier hit keeps
+    host DRAM as the backing store: its saves go there, the tier copy is the
+    in-loop write-through)."""
+    engine, model, runner = _mods()
+    from dataclasses import replace
+    shape = replace(model.shape("tiny"), context_window=64, layers=3)
+    w = runner.LlamaWeights(shape, seed=13)
+    engs = []
+    for hb in (0, 8):
+        e = engine.Engine(shape, host_blocks=64, block_tokens=16, weights=w, max_new=64,
+                          read_buffer_bytes=16 << 20, hbm_blocks=hb)
+        e.arena.buffer.zero_()
+        engs.append(e)
+    rng = np.random.default_rng(16)
+    for k in range(5):
+        for sid in ("a", "b", "c"):
+            new_ids = torch.as_tensor(rng.integers(0, shape.vocab, 9 + k))
+            out_ids = torch.as_tensor(rng.integers(0, shape.vocab, 6))
+            a, b = (e.turn(sid, k, new_ids, out_ids, want_logits=True) for e in engs)
+            torch.cuda.synchronize()
+            assert (a.kept, a.drop, a.hit) == (b.kept, b.drop, b.hit)
+            assert torch.equal(a.result.logits, b.result.logits), (sid, k)
+    for e in engs:
+        e.runner.join()
+    torch.cuda.synchronize()
+    assert engs[1].hbm.hits > 0 and engs[1].hbm.promotions > 0
+    bb = engs[0].runner.block_bytes
+    for sid in ("a", "b", "c"):
+        for blk in engs[0].store.block_table(sid):
+            assert torch.equal(engs[0].arena.buffer[blk * bb:(blk + 1) * bb],
+                               engs[1].arena.buffer[blk * bb:(blk + 1) * bb]), (sid, blk)

@@ -24,6 +24,7 @@ def main():
                     help="stream a background pinned H2D copy during the profiled step")
     ap.add_argument("--no-save", action="store_true", help="jobs without the K4 save")
     ap.add_argument("--no-graph", action="store_true", help="stream-issue the layer loop")
+    ap.add_argument("--overlap", action="store_true", help="K2(l+1) alongside K3(l)")
     a = ap.parse_args()
     import bench
     from paper_2403_19708_b200 import model
@@ -39,7 +40,7 @@ def main():
     hbm = torch.zeros(sum(nbs) * bb // 2, dtype=torch.bfloat16, device="cuda")
     runner = Runner(shape, host_arena=arena, hbm_arena=hbm, read_buffer_bytes=4 << 30,
                     write_buffer_bytes=1 << 30, max_new=max(n for *_, n in turns),
-                    max_ctx=4096, timeline=True, graph=not a.no_graph)
+                    max_ctx=4096, timeline=True, graph=not a.no_graph, overlap=a.overlap)
     jobs, pos = [], 0
     rng = np.random.default_rng(0)
     for (sid, k, kept, new), nb in zip(turns, nbs):
