@@ -63,6 +63,8 @@ def parse():
                     help="directory for the disk-tier probe ('none' = skip)")
     ap.add_argument("--decode-steps", type=int, default=32,
                     help="greedy decode steps measured after the prefill legs (0 = skip)")
+    ap.add_argument("--k2-overlap", type=int, default=0,
+                    help="1: K2 of layer l+1 on a side stream alongside K3 of layer l")
     ap.add_argument("--profile-attn", action="store_true",
                     help="run only a few hbm steps (for ncu captures)")
     return ap.parse_args()
@@ -412,7 +414,8 @@ def main():
                     hbm_arena=hbm, read_buffer_bytes=4 << 30, write_buffer_bytes=1 << 30,
                     max_new=max(max_new, 1), max_ctx=max(shape.context_window, max_kept + 1),
                     # tune the GEMMs over the recompute baseline's prompt lengths too
-                    autotune=max(shape.context_window, max_kept + 1) + max(max_new, 1))
+                    autotune=max(shape.context_window, max_kept + 1) + max(max_new, 1),
+                    overlap=bool(args.k2_overlap))
     ids_perm = np.random.default_rng(99 + rank).permutation(n_blocks)
     jobs = {"host": [], "hbm": [], "recompute": []}
     pos = 0
