@@ -221,3 +221,27 @@ def test_disk_tier_truncation_and_remove(tmp_path):
     stor.remove("t")
     assert not Path(path).exists() and "t" not in disk.meta
     stor.check_invariants()
+
+
+def test_hbm_tier_block_reuse_is_fenced():
+    """HBM session tier bookkeeping (engine.HbmTier, host-side only): a block
+    that moves from one session to another records the previous owner, so the
+    new owner's next job orders its tier writes after that session's saves; a
+    session re-taking its own freed blocks needs no fence; the mirror tracks
+    the host table's front drops and growth one-to-one."""
+    from paper_2403_19708_b200.engine import HbmTier
+    tier = HbmTier(4, 64, "cpu")
+    assert tier.sync("a", [10, 11], 0, set()) and tier.tab["a"] == [0, 1]
+    assert tier.sync("b", [20, 21], 0, set()) and tier.tab["b"] == [2, 3]
+    assert tier.fence == {}
+    # c needs a block: the LRU session (a) is evicted, its blocks go to c
+    assert tier.sync("c", [30], 0, set()) and tier.tab["c"] == [0]
+    assert "a" not in tier.tab and tier.fence == {"c": {"a"}}
+    # front drop of b's first block, then growth: b takes back its own block
+    # first (no fence) and a's remaining one (fenced on a)
+    assert tier.sync("b", [21, 22, 23], 1, set())
+    assert tier.tab["b"] == [3, 1, 2] and tier.fence["b"] == {"a"}
+    # pinned sessions are never evicted; with nothing evictable the sync fails
+    # and the session is dropped from the tier
+    assert not tier.sync("d", [40, 41], 0, {"b", "c"})
+    assert "d" not in tier.tab
