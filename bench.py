@@ -63,6 +63,9 @@ def parse():
                     help="directory for the disk-tier probe ('none' = skip)")
     ap.add_argument("--decode-steps", type=int, default=32,
                     help="greedy decode steps measured after the prefill legs (0 = skip)")
+    ap.add_argument("--tp-rank-of", type=int, default=0,
+                    help="c5 on one GPU: run one rank of a TP-K shard (weights, heads and KV "
+                         "slice of rank 0), collective excluded -- a per-rank compute probe")
     ap.add_argument("--k2-overlap", type=int, default=0,
                     help="1: K2 of layer l+1 on a side stream alongside K3 of layer l")
     ap.add_argument("--profile-attn", action="store_true",
@@ -343,6 +346,9 @@ def main():
 
     shape = model.shape(CONFIGS[args.config][0])
     tp = world if args.config == "c5" else 1
+    rank_probe = args.config == "c5" and world == 1 and args.tp_rank_of > 1
+    if rank_probe:   # one TP rank's shard on this GPU, no all-reduce partner
+        shape = shape.tp_shard(args.tp_rank_of)
     if tp > 1:
         # C5: one model replica tensor-parallel over all ranks (head-parallel
         # attention + KV store slice per rank, NCCL all-reduce after W_o / W_down)
@@ -659,6 +665,9 @@ def main():
             "l2": "inputs larger than L2 (per-step KV " f"{h2d_bytes / 1e9:.1f} GB)",
             "parallelism": (f"tensor-parallel tp{tp} (NCCL all-reduce of W_o / W_down "
                             f"partials over NVLink)" if tp > 1 else
+                            f"one rank of a tp{args.tp_rank_of} shard, all-reduce excluded "
+                            f"(per-rank compute probe; outputs are partial sums)"
+                            if rank_probe else
                             f"sessions sharded, no collective ({world} independent ranks)")},
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d_step,
                 "d2h_bytes_per_step": d2h_step, "ms_per_step": ms_host / args.steps},
