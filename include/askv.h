@@ -115,6 +115,9 @@ size_t askv_attn_workspace_bytes(int n_cached, int n_new, int n_heads, int head_
                                  int num_splits);
 /* Split count the auto policy would use (for reporting / tests). */
 int askv_attn_num_splits(int n_cached, int n_new, int n_heads, int sm_count);
+/* Same with GQA: n_heads q-heads over n_kv_heads kv heads (the launch packs a
+ * kv head's (token, q-head) rows into shared tiles). */
+int askv_attn_num_splits_gqa(int n_cached, int n_new, int n_heads, int n_kv_heads, int sms);
 
 /*
  * K1 — layer-wise pre-loader: H2D of one layer's kept blocks of one session

@@ -36,6 +36,7 @@ SIGNATURES = {
                                  _sz, _i32, _vp]),
     "askv_attn_workspace_bytes": (_sz, [_i32, _i32, _i32, _i32, _i32]),
     "askv_attn_num_splits": (_i32, [_i32, _i32, _i32, _i32]),
+    "askv_attn_num_splits_gqa": (_i32, [_i32, _i32, _i32, _i32, _i32]),
     "askv_preload_layer": (_i32, [_vp, _vp, _pi64, _i32, _i64, _i64, _i64, _i64, _vp, _vp]),
     "askv_save_layer": (_i32, [_vp, _pi64, _i32, _i64, _i64, _i32, _i64, _i64, _i32, _vp, _vp,
                                _vp]),

@@ -71,6 +71,7 @@ struct AttnParams {
   int n_cached;
   int hq;
   int group;
+  int pack;  // > 1: GQA packing -- a CTA's 128 rows are (token, q-head) pairs of one kv head
   int num_splits;
   int tiles_per_split;
   float scale_log2;
@@ -154,19 +155,29 @@ __global__ void __launch_bounds__(352, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int h = blockIdx.y;
+  const int h = blockIdx.y;  // q-head; the kv head when packed
   const int split = blockIdx.z;
-  const int kh = h / p.group;
+  const int pack = p.pack;
+  const int kh = pack > 1 ? h : h / p.group;
   if (threadIdx.x == 0) ATTN_TRACE(0);
   launch_stamp_begin(p.stamp);
+  // Query rows of this CTA's row space: tokens of q-head h, or -- GQA packing --
+  // the (token, q-head) pairs of kv head h, row = token * pack + head-in-group,
+  // so one K/V tile serves 128 rows of every q-head sharing it.
+  const int q_rows = pack > 1 ? p.n_new * pack : p.n_new;
+  auto tok = [&](int row) { return pack > 1 ? row / pack : row; };
+  auto out_row = [&](int row) -> int64_t {  // (token, q-head) index into [n_new][hq]
+    return pack > 1 ? (int64_t)(row / pack) * p.hq + h * pack + row % pack
+                    : (int64_t)row * p.hq + h;
+  };
   // query tiles of this CTA: A at q0, B at q0 + 128 (paired only)
   const int q0 = blockIdx.x * kBM * C::kQTiles;
-  const int rows_a = min(kBM, p.n_new - q0);
-  const int rows_b = kAllowPair ? max(0, min(kBM, p.n_new - q0 - kBM)) : 0;
+  const int rows_a = min(kBM, q_rows - q0);
+  const int rows_b = kAllowPair ? max(0, min(kBM, q_rows - q0 - kBM)) : 0;
   // CTA-uniform mode: paired when this CTA really has two query tiles
   const bool paired = rows_b > 0;
   const int last_row = q0 + (rows_b > 0 ? kBM + rows_b : rows_a) - 1;
-  const int kv_end = p.n_cached + last_row + 1;
+  const int kv_end = p.n_cached + tok(last_row) + 1;
   const int tiles_total = (kv_end + kBN - 1) / kBN;
   const int t_begin = split * p.tiles_per_split;
   const int t_end = min(tiles_total, t_begin + p.tiles_per_split);
@@ -176,7 +187,7 @@ __global__ void __launch_bounds__(352, 1)
   // n_cached + q0 + rows_a - 1, so A uses a prefix of the split's tiles
   int nt_a = n_tiles, nt_b = 0;
   if (paired) {
-    const int last_a = (p.n_cached + q0 + rows_a - 1) / kBN;
+    const int last_a = (p.n_cached + tok(q0 + rows_a - 1)) / kBN;
     nt_a = max(0, min(n_tiles, last_a + 1 - t_begin));
     nt_b = rows_b > 0 ? n_tiles : 0;
   }
@@ -187,7 +198,7 @@ __global__ void __launch_bounds__(352, 1)
       const int g = paired ? (warp >> 2) : 0;
       const int rows = g ? rows_b : rows_a;
       if ((paired || warp < 4) && r < rows) {
-        const int64_t row = ((int64_t)split * p.n_new + q0 + g * kBM + r) * p.hq + h;
+        const int64_t row = (int64_t)split * p.n_new * p.hq + out_row(q0 + g * kBM + r);
         p.part_lse[row] = -INFINITY;
         float4* po = reinterpret_cast<float4*>(p.part_o + row * HD);
 #pragma unroll
@@ -236,8 +247,8 @@ __global__ void __launch_bounds__(352, 1)
       for (int t = 0; t < qt; ++t)
 #pragma unroll
         for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d_hint(sQ + t * C::kTileBytes + c * (kBM * 128), &tm_q, q_full, c * 64, h,
-                           q0 + t * kBM, pol_q);
+          tma_load_3d_hint(sQ + t * C::kTileBytes + c * (kBM * 128), &tm_q, q_full, c * 64,
+                           pack > 1 ? h * pack : h, tok(q0 + t * kBM), pol_q);
       // K tiles: as far ahead as the K ring allows (S(j) needs K(j) well before
       // PV(j) needs V(j)); V tiles come from warp 10, so a V slot still held by
       // a PV in flight never delays the next K (in-kernel trace: with one
@@ -362,7 +373,7 @@ __global__ void __launch_bounds__(352, 1)
     const uint32_t t_s = tmem + lane_off + C::col_s(w);
     const uint32_t t_o = tmem + lane_off + C::col_o(w);
     const int qt0 = q0 + (paired ? w * kBM : 0);  // first query of this group's tile
-    const int row_limit = p.n_cached + qt0 + r;
+    const int row_limit = p.n_cached + tok(qt0 + r);
     const float sl2 = p.scale_log2;
     const int my_tiles = paired ? (w ? nt_b : nt_a) : (n_tiles - w + 1) / 2;
     float m_acc = -INFINITY, l_acc = 0.f;
@@ -454,7 +465,7 @@ __global__ void __launch_bounds__(352, 1)
       tc_fence_after();
       const int kbase = (t_begin + j) * kBN;
       // group-uniform: does any row of this tile see a masked column here?
-      if (kbase + kBN - 1 > p.n_cached + qt0)
+      if (kbase + kBN - 1 > p.n_cached + tok(qt0))
         tile(std::true_type{}, t, row_limit - kbase);
       else
         tile(std::false_type{}, t, 0);
@@ -505,7 +516,7 @@ __global__ void __launch_bounds__(352, 1)
       }
       if (r < rows_g) {
         if (!partial) {
-          __nv_bfloat16* dst = p.out + ((int64_t)qi * p.hq + h) * HD + col;
+          __nv_bfloat16* dst = p.out + out_row(qi) * HD + col;
 #pragma unroll
           for (int e = 0; e < 32; e += 8) {
             uint4 v;
@@ -516,7 +527,7 @@ __global__ void __launch_bounds__(352, 1)
             *reinterpret_cast<uint4*>(dst + e) = v;
           }
         } else {
-          const int64_t row = ((int64_t)split * p.n_new + qi) * p.hq + h;
+          const int64_t row = (int64_t)split * p.n_new * p.hq + out_row(qi);
           float4* po = reinterpret_cast<float4*>(p.part_o + row * HD + col);
 #pragma unroll
           for (int e = 0; e < 32; e += 4)
@@ -593,7 +604,7 @@ EncodeTiledFn get_encode_fn() {
 
 // 3-D bf16 map {d, heads, rows} with a {64, 1, 128} SWIZZLE_128B box.
 int make_map(CUtensorMap* m, const void* base, int head_dim, int heads, int64_t head_stride,
-             int64_t rows, int64_t row_stride) {
+             int64_t rows, int64_t row_stride, int box_heads = 1) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -601,7 +612,9 @@ int make_map(CUtensorMap* m, const void* base, int head_dim, int heads, int64_t 
   }
   cuuint64_t dims[3] = {(cuuint64_t)head_dim, (cuuint64_t)heads, (cuuint64_t)rows};
   cuuint64_t strides[2] = {(cuuint64_t)head_stride * 2, (cuuint64_t)row_stride * 2};
-  cuuint32_t box[3] = {64, 1, 128};
+  // box_heads > 1 (GQA packing): 128 / box_heads tokens x box_heads heads land as
+  // 128 rows ordered (token, head), the same smem tile layout
+  cuuint32_t box[3] = {64, (cuuint32_t)box_heads, (cuuint32_t)(128 / box_heads)};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -641,15 +654,34 @@ bool use_pairs(int q_tiles, int hq, int sms) {
   return q_tiles * hq > sms;
 }
 
+// GQA packing: when q-heads share a kv head, one CTA's
+// 128 query rows are (token, q-head) pairs of a kv head, so each K/V tile
+// feeds rows of every head of the group and a skinny prefill pads less (a
+// 301-token tile set of 8 heads is 19 full tiles instead of 8 x 3 with a
+// 45-row tail).  The group must divide the 128-row tile.  ASKV_ATTN_PACK=0
+// turns it off.
+int gqa_pack(int hq, int hkv) {
+  static int knob = -1;
+  if (knob < 0) {
+    const char* e = getenv("ASKV_ATTN_PACK");
+    knob = (e && e[0] == '0') ? 0 : 1;
+  }
+  const int g = hq / hkv;
+  return (knob && g > 1 && g <= 16 && 128 % g == 0) ? g : 1;
+}
+
 // Split count minimising waves x (tiles per split + fixed per-CTA overhead).
 // Split-KV policy, fitted to a B200 sweep (tools/kbench.py sweep): one CTA per
 // SM at most (one wave), and at least 4 KV tiles per split so the per-CTA
 // prologue / epilogue and the combine pass stay amortised.
-int choose_splits(int n_cached, int n_new, int hq, int sms) {
-  const int q_tiles = (n_new + kBM - 1) / kBM;
-  const int q_groups = use_pairs(q_tiles, hq, sms) ? (q_tiles + 1) / 2 : q_tiles;
+int choose_splits(int n_cached, int n_new, int hq, int sms, int hkv = 0) {
+  if (hkv <= 0) hkv = hq;
+  const int pack = gqa_pack(hq, hkv);
+  const int q_tiles = (n_new * pack + kBM - 1) / kBM;
+  const int q_groups =
+      pack == 1 && use_pairs(q_tiles, hq, sms) ? (q_tiles + 1) / 2 : q_tiles;
   const int kv_tiles = (n_cached + n_new + kBN - 1) / kBN;
-  const int ctas = q_groups * hq;
+  const int ctas = q_groups * (pack > 1 ? hkv : hq);
   int best = 1;
   for (int s = 2; s <= kMaxSplits; ++s) {
     const int tps = (kv_tiles + s - 1) / s;
@@ -664,16 +696,17 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
                 int hq, int hkv, float scale, void* out, void* ws, size_t ws_bytes,
                 int splits, cudaStream_t stream, unsigned long long* stamp) {
   const int rows = n_cached + n_new;
+  const int pack = gqa_pack(hq, hkv);
   CUtensorMap mq, mk, mv;
-  int rc = make_map(&mq, q, HD, hq, HD, n_new, (int64_t)hq * HD);
+  int rc = make_map(&mq, q, HD, hq, HD, n_new, (int64_t)hq * HD, pack);
   if (!rc) rc = make_map(&mk, kv, HD, hkv, HD, rows, kv_row_stride);
   if (!rc)
     rc = make_map(&mv, static_cast<const __nv_bfloat16*>(kv) + (int64_t)hkv * HD, HD, hkv, HD,
                   rows, kv_row_stride);
   if (rc) return rc;
 
-  const int q_tiles = (n_new + kBM - 1) / kBM;
-  const bool paired = use_pairs(q_tiles, hq, sm_count());
+  const int q_tiles = (n_new * pack + kBM - 1) / kBM;
+  const bool paired = pack == 1 && use_pairs(q_tiles, hq, sm_count());
   const int q_groups = paired ? (q_tiles + 1) / 2 : q_tiles;
   const int kv_tiles = (rows + kBN - 1) / kBN;
   const int tps = (kv_tiles + splits - 1) / splits;
@@ -683,6 +716,7 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
   prm.n_cached = n_cached;
   prm.hq = hq;
   prm.group = hq / hkv;
+  prm.pack = pack;
   prm.num_splits = splits;
   prm.tiles_per_split = tps;
   prm.scale_log2 = scale * 1.4426950408889634f;
@@ -699,7 +733,7 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
     prm.part_o = static_cast<float*>(ws);
     prm.part_lse = prm.part_o + (size_t)splits * rows_qh * HD;
   }
-  dim3 grid(q_groups, hq, splits);
+  dim3 grid(q_groups, pack > 1 ? hkv : hq, splits);
   if (paired) {
     auto kern = attn_fwd_kernel<HD, true>;
     static bool attr = false;
@@ -739,6 +773,14 @@ extern "C" int askv_attn_num_splits(int n_cached, int n_new, int n_heads, int sm
   return choose_splits(n_cached, n_new, n_heads, sms > 0 ? sms : sm_count());
 }
 
+extern "C" int askv_attn_num_splits_gqa(int n_cached, int n_new, int n_heads, int n_kv_heads,
+                                        int sms) {
+  if (n_new <= 0 || n_heads <= 0 || n_cached < 0 || n_kv_heads <= 0 ||
+      n_heads % n_kv_heads)
+    return 1;
+  return choose_splits(n_cached, n_new, n_heads, sms > 0 ? sms : sm_count(), n_kv_heads);
+}
+
 extern "C" size_t askv_attn_workspace_bytes(int n_cached, int n_new, int n_heads,
                                             int head_dim, int num_splits) {
   if (n_new <= 0 || n_heads <= 0) return 0;
@@ -775,7 +817,8 @@ int askv::prefill_attn_stamped(const void* q, const void* kv, int64_t kv_row_str
                "prefill_attn: q/kv must be 16-byte aligned with row stride %% 8 == 0");
   ASKV_REQUIRE(kv_row_stride >= 2LL * n_kv_heads * head_dim,
                "prefill_attn: kv_row_stride %lld < 2*Hkv*d", (long long)kv_row_stride);
-  int splits = num_splits > 0 ? num_splits : choose_splits(n_cached, n_new, n_heads, sm_count());
+  int splits = num_splits > 0 ? num_splits
+                              : choose_splits(n_cached, n_new, n_heads, sm_count(), n_kv_heads);
   if (head_dim == 128)
     return launch_attn<128>(q, kv, kv_row_stride, n_cached, n_new, n_heads, n_kv_heads, scale,
                             out, workspace, workspace_bytes, splits, (cudaStream_t)stream, stamp);

@@ -100,8 +100,11 @@ def attn_workspace_bytes(n_cached: int, n_new: int, n_heads: int, head_dim: int,
     return int(lib().askv_attn_workspace_bytes(n_cached, n_new, n_heads, head_dim, num_splits))
 
 
-def attn_num_splits(n_cached: int, n_new: int, n_heads: int, sm_count: int = 0) -> int:
-    return int(lib().askv_attn_num_splits(n_cached, n_new, n_heads, sm_count))
+def attn_num_splits(n_cached: int, n_new: int, n_heads: int, sm_count: int = 0,
+                    n_kv_heads: int | None = None) -> int:
+    if n_kv_heads is None or n_kv_heads == n_heads:
+        return int(lib().askv_attn_num_splits(n_cached, n_new, n_heads, sm_count))
+    return int(lib().askv_attn_num_splits_gqa(n_cached, n_new, n_heads, n_kv_heads, sm_count))
 
 
 def prefill_attn(q: torch.Tensor, kv: torch.Tensor, n_cached: int, n_new: int, n_heads: int,

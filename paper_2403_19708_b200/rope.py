@@ -170,7 +170,7 @@ def attention_with_decoupled_cache(record: KvRecord, new_q, new_k, new_v, positi
     q_rot = torch.empty((n, hq, d), dtype=torch.bfloat16, device=dev)
     ops.rope_new(qkv, n, hq, hkv, d, table, next_pos, q_rot, kv[s:])
     out = torch.empty((n, hq, d), dtype=torch.bfloat16, device=dev)
-    splits = num_splits or ops.attn_num_splits(s, n, hq)
+    splits = num_splits or ops.attn_num_splits(s, n, hq, n_kv_heads=hkv)
     ws = None
     nbytes = ops.attn_workspace_bytes(s, n, hq, d, splits)
     if nbytes:

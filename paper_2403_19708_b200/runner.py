@@ -649,7 +649,7 @@ class Runner:
                 self.launches += 1
             x = F.embedding(ids, self.w.embed)
             self._buf("h", n, s.d_model)
-            splits = ops.attn_num_splits(kept, n, hq)
+            splits = ops.attn_num_splits(kept, n, hq, n_kv_heads=hkv)
             wsb = ops.attn_workspace_bytes(kept, n, hq, hd, splits)
             ws = self._workspace(wsb) if wsb else None
 

@@ -48,7 +48,7 @@ def attn(args):
         q = torch.randn(n, hq, d, device="cuda").to(torch.bfloat16)
         kv = torch.randn(kept + n, 2, hkv, d, device="cuda").to(torch.bfloat16)
         o = torch.empty(n, hq, d, device="cuda", dtype=torch.bfloat16)
-        s = args.splits or ops.attn_num_splits(kept, n, hq)
+        s = args.splits or ops.attn_num_splits(kept, n, hq, n_kv_heads=hkv)
         ws = torch.empty(max(1, ops.attn_workspace_bytes(kept, n, hq, d, s)), dtype=torch.uint8,
                          device="cuda")
         t = timeit(lambda: ops.prefill_attn(q, kv, kept, n, hq, hkv, d, o, ws, num_splits=s),
