@@ -12,12 +12,14 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "../paper_2403_19708_b200/csrc/askv_ptx.cuh"
 using namespace askv;
 
-template <int MODE>
+template <int MODE_>
 __global__ void probe(long long* out, int iters, int writers) {
+  constexpr int MODE = MODE_ >= 10 ? MODE_ - 10 : MODE_;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -65,6 +67,20 @@ __global__ void probe(long long* out, int iters, int writers) {
     long long t1 = clock64();
     out[blockIdx.x] = t1 - t0;
     done = 1;
+  } else if (warp >= 1 && warp <= writers && MODE_ >= 10) {
+    // TMEM reader: tcgen05.ld 32 lanes x 32 columns in a loop over columns
+    // [384, 512) (the softmax's S reads), 4 warps cover the 128 lanes
+    const uint32_t lane_off = (uint32_t)(((warp - 1) & 3) * 32) << 16;
+    float acc = 0.f;
+    while (!done) {
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        float v[32];
+        tmem_ld32(tmem + lane_off + 384 + c * 32, v);
+        acc += v[0];
+      }
+    }
+    if (acc == 12345.f) out[0] = 0;
   } else if (warp >= 1 && warp <= writers) {
     // smem writer: 16-byte stores over a 32 KB region (a TMA fill stand-in)
     uint4* w = reinterpret_cast<uint4*>(smem + 131072);
@@ -90,6 +106,7 @@ int main() {
   const char* names[] = {"SS N=128 (S, kernel 1)", "SS N=64 (S, kernel 2)", "TS N=128 (PV)",
                          "SS N=256", "TS N=128 A=Q in TMEM (S)"};
   auto run = [&](auto kern, int mode) {
+    if (mode > 9) mode -= 10;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     for (int writers : {0, 4}) {
       for (int grid : {1, 148}) {
@@ -111,10 +128,15 @@ int main() {
       }
     }
   };
-  run(probe<0>, 0);
-  run(probe<1>, 1);
-  run(probe<2>, 2);
-  run(probe<3>, 3);
-  run(probe<4>, 4);
+  if (!getenv("TMEM_ONLY")) {
+    run(probe<0>, 0);
+    run(probe<1>, 1);
+    run(probe<2>, 2);
+    run(probe<3>, 3);
+    run(probe<4>, 4);
+  }
+  printf("-- with 4 warps streaming tcgen05.ld (32x32b.x32) from other TMEM columns --\n");
+  run(probe<10>, 0);
+  run(probe<12>, 2);
   return 0;
 }

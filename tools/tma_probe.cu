@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <vector>
 
@@ -51,8 +52,11 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
 }
 
 // grid.x = heads * per_head; CTA (head, q) streams n_tiles K tiles and V tiles.
-template <int C, int kStages, int kPieceRows>
-__global__ void __launch_bounds__(64, 1)
+// kMma: warp 2 keeps the tensor core busy with SS MMAs (M=128 N=128 K=16, both
+// operands from a separate 64 KB shared region, like S = Q K^T) while the
+// stream runs -- does operand traffic slow the TMA fill?
+template <int C, int kStages, int kPieceRows, bool kMma = false>
+__global__ void __launch_bounds__(96, 1)
     stream_kernel(const __grid_constant__ CUtensorMap tm, int per_head, int hkv, int n_tiles,
                   int kv_rows) {
   extern __shared__ uint8_t raw[];
@@ -70,7 +74,20 @@ __global__ void __launch_bounds__(64, 1)
     }
     fence_mbar_init();
   }
+  __shared__ uint32_t tslot;
+  __shared__ volatile int stream_done;
+  __shared__ uint64_t mma_bar;
+  if (kMma) {
+    if (threadIdx.x == 0) {
+      stream_done = 0;
+      mbar_init(&mma_bar, 1);
+      fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(&tslot, 128);
+    tc_fence_before();
+  }
   if (C > 1) cluster_sync_all(); else __syncthreads();
+  if (kMma) tc_fence_after();
   const int steps = 2 * n_tiles;  // K tile, V tile, K tile, ...
   if (warp == 0 && lane == 0) {
     const uint64_t pol = l2_policy_evict_last();
@@ -103,8 +120,38 @@ __global__ void __launch_bounds__(64, 1)
         for (int c = 0; c < C; ++c) mbar_arrive_remote(&empty[s], c);
       }
     }
+    if (kMma) stream_done = 1;
+  } else if (kMma && warp == 2 && lane == 0) {
+    const uint32_t sa = smem_u32(smem + kStages * kTile + 2 * kStages * 8 + 1024 - 1024 + 0);
+    const uint32_t base = (sa + 1023) & ~1023u;
+    const uint32_t sq = base, sk = base + 32768;
+    constexpr uint32_t idesc = idesc_bf16_f32(128, 128, 0, 0);
+    const uint32_t tmem = tslot;
+    int iters = 0;
+    while (!stream_done) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
+        umma_bf16(tmem, sdesc_sw128(sq + off, 16, 1024), sdesc_sw128(sk + off, 16, 1024), idesc,
+                  k > 0);
+      }
+      umma_commit(&mma_bar);
+      mbar_wait(&mma_bar, iters & 1);
+      ++iters;
+    }
+  }
+  if (kMma) {
+    tc_fence_before();
+    __syncwarp();
   }
   if (C > 1) cluster_sync_all();
+  if (kMma) {
+    __syncthreads();
+    if (warp == 2) {
+      tc_fence_after();
+      tmem_dealloc(tslot, 128);
+    }
+  }
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -146,11 +193,11 @@ int main() {
   cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
   auto run = [&](auto kern, int stages, int piece_rows, int heads, int per_head, int C,
                  bool flush_l2) {
-    const int smem = stages * kTile + 2 * stages * 8 + 1024;
+    const int smem = stages * kTile + 2 * stages * 8 + 1024 + 65536 + 1024;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(heads * per_head);
-    cfg.blockDim = dim3(64);
+    cfg.blockDim = dim3(96);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -183,6 +230,13 @@ int main() {
            stages, piece_rows, C, heads, per_head, ctas, flush_l2 ? "cold" : "warm", best * 1e3,
            per_cta / cyc, per_cta * ctas / best / 1e9);
   };
+  printf("-- with / without concurrent SS MMAs (M128 N128 K16) on the same SM --\n");
+  for (int fl = 1; fl >= 0; --fl) {
+    run(stream_kernel<1, 4, 128, false>, 4, 128, 40, 3, 1, fl);
+    printf("   + MMA: ");
+    run(stream_kernel<1, 4, 128, true>, 4, 128, 40, 3, 1, fl);
+  }
+  if (getenv("TMA_PROBE_MMA_ONLY")) return 0;
   for (int fl = 1; fl >= 0; --fl) {
     run(stream_kernel<1, 4, 64>, 4, 64, 40, 3, 1, fl);
     run(stream_kernel<1, 4, 128>, 4, 128, 40, 3, 1, fl);
