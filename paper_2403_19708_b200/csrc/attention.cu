@@ -550,390 +550,6 @@ __global__ void __launch_bounds__(352, 1)
   if (p.num_splits == 1) launch_stamp_end(p.stamp);
 }
 
-// ============================================================================
-// Kernel 4: one 128-row query tile, 64-key sub-tiles alternating between the
-// two softmax warpgroups, each with a double-buffered S.
-//
-// In kernel 1 each warpgroup has one S buffer, so S(j+2) can be issued only
-// after PV(j) has read P(j) out of it: per warpgroup the chain
-// softmax -> PV -> S -> softmax leaves the tensor core ~40 % busy and the MMA
-// warp waiting (in-kernel trace, r01_attn_experiments.md).  Here warpgroup g
-// owns sub-tiles s = 2i + g (64 keys) and two S buffers, so S_g(i+1) is
-// computed while softmax_g(i) runs.  TMEM: O_0 [0,128), O_1 [128,256),
-// S_g[b] at 256 + 128 g + 64 b (P over its first 32 columns).  An N=64 MMA
-// costs about as much as N=128 (tools/mma_probe2.cu), so S costs 2x the
-// tensor time of kernel 1 -- the bet is that hiding the chain wins more.
-// Warps: 0-3 group 0, 4-7 group 1, 8 TMA Q + K (+ TMEM alloc), 9 MMA, 10 TMA V.
-// ============================================================================
-template <int HD>
-struct SubCfg {
-  static constexpr int kKStages = 3;
-  static constexpr int kVStages = 3;
-  static constexpr int kChunks = HD / 64;
-  static constexpr int kTileBytes = kBM * HD * 2;
-  static constexpr int kQOff = 0;
-  static constexpr int kKOff = kTileBytes;
-  static constexpr int kVOff = kKOff + kKStages * kTileBytes;
-  static constexpr int kBarOff = kVOff + kVStages * kTileBytes;
-  // q_full, k_full[SK], k_empty[SK], v_full[SV], v_empty[SV],
-  // s_full[2][2], p_full[2][2], o_full[2][2]
-  static constexpr int kNumBars = 1 + 2 * kKStages + 2 * kVStages + 12;
-  static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
-  static constexpr int kSmemBytes = kTmemSlotOff + 16 + 1024;
-  static constexpr uint32_t kTmemCols = 512;
-  __host__ __device__ static constexpr uint32_t col_o(int g) { return 128u * (uint32_t)g; }
-  __host__ __device__ static constexpr uint32_t col_s(int g, int b) {
-    return 256u + 128u * (uint32_t)g + 64u * (uint32_t)b;
-  }
-  static constexpr int kThreads = 352;
-  static constexpr int kSub = 64;
-  static constexpr float kRescaleLog2 = 8.0f;
-  static_assert(kSmemBytes <= 232448, "smem budget");
-};
-
-template <int HD>
-__global__ void __launch_bounds__(352, 1)
-    attn_sub_kernel(const __grid_constant__ CUtensorMap tm_q,
-                    const __grid_constant__ CUtensorMap tm_k,
-                    const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
-  using C = SubCfg<HD>;
-  constexpr int kSub = C::kSub;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem + C::kQOff;
-  uint8_t* sK = smem + C::kKOff;
-  uint8_t* sV = smem + C::kVOff;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = q_full + 1;
-  uint64_t* k_empty = k_full + C::kKStages;
-  uint64_t* v_full = k_empty + C::kKStages;
-  uint64_t* v_empty = v_full + C::kVStages;
-  uint64_t* s_full = v_empty + C::kVStages;  // [g * 2 + b]
-  uint64_t* p_full = s_full + 4;             // [g * 2 + b]
-  uint64_t* o_full = p_full + 4;             // [g * 2 + b]: PV_g(i) with i & 1 == b
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kTmemSlotOff);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int h = blockIdx.y;
-  const int split = blockIdx.z;
-  const int pack = p.pack;
-  const int kh = pack > 1 ? h : h / p.group;
-  launch_stamp_begin(p.stamp);
-  const int q_rows = pack > 1 ? p.n_new * pack : p.n_new;
-  auto tok = [&](int row) { return pack > 1 ? row / pack : row; };
-  auto out_row = [&](int row) -> int64_t {
-    return pack > 1 ? (int64_t)(row / pack) * p.hq + h * pack + row % pack
-                    : (int64_t)row * p.hq + h;
-  };
-  const int q0 = blockIdx.x * kBM;
-  const int rows = min(kBM, q_rows - q0);
-  const int kv_end = p.n_cached + tok(q0 + rows - 1) + 1;
-  const int tiles_total = (kv_end + kBN - 1) / kBN;
-  const int t_begin = split * p.tiles_per_split;
-  const int t_end = min(tiles_total, t_begin + p.tiles_per_split);
-  const int key0 = t_begin * kBN;
-  const int key_end = min(t_end * kBN, kv_end);
-  const int nsub = key_end > key0 ? (key_end - key0 + kSub - 1) / kSub : 0;
-  const int n_tiles = (nsub + 1) / 2;
-  const bool partial = p.num_splits > 1;
-
-  if (nsub == 0) {  // empty split: neutral partials
-    if (warp < 4) {
-      const int r = threadIdx.x & 127;
-      if (r < rows) {
-        const int64_t row = (int64_t)split * p.n_new * p.hq + out_row(q0 + r);
-        p.part_lse[row] = -INFINITY;
-        float4* po = reinterpret_cast<float4*>(p.part_o + row * HD);
-#pragma unroll
-        for (int c = 0; c < HD / 4; ++c) po[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    }
-    return;
-  }
-
-  if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    for (int i = 0; i < C::kKStages; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
-    }
-    for (int i = 0; i < C::kVStages; ++i) {
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
-    }
-    for (int i = 0; i < 4; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 128);
-      mbar_init(&o_full[i], 1);
-    }
-    fence_mbar_init();
-  }
-  if (warp == 8) tmem_alloc(tmem_slot, C::kTmemCols);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 8) {
-    // ------------------------------------------------------------ TMA: Q + K
-    if (lane == 0) {
-      tma_prefetch_desc(&tm_q);
-      tma_prefetch_desc(&tm_k);
-      const uint64_t pol_kv = l2_policy_evict_last();
-      const uint64_t pol_q = l2_policy_evict_first();
-      mbar_expect_tx(q_full, C::kTileBytes);
-#pragma unroll
-      for (int c = 0; c < C::kChunks; ++c)
-        tma_load_3d_hint(sQ + c * (kBM * 128), &tm_q, q_full, c * 64, pack > 1 ? h * pack : h,
-                         tok(q0), pol_q);
-      for (int jk = 0; jk < n_tiles; ++jk) {
-        const int st = jk % C::kKStages;
-        if (jk >= C::kKStages) mbar_wait(&k_empty[st], ((jk / C::kKStages) - 1) & 1);
-        mbar_expect_tx(&k_full[st], C::kTileBytes);
-#pragma unroll
-        for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d_hint(sK + st * C::kTileBytes + c * (kBN * 128), &tm_k, &k_full[st],
-                           c * 64, kh, (t_begin + jk) * kBN, pol_kv);
-      }
-    }
-  } else if (warp == 10) {
-    // ------------------------------------------------------------ TMA: V
-    if (lane == 0) {
-      tma_prefetch_desc(&tm_v);
-      const uint64_t pol_kv = l2_policy_evict_last();
-      for (int jv = 0; jv < n_tiles; ++jv) {
-        const int st = jv % C::kVStages;
-        if (jv >= C::kVStages) mbar_wait(&v_empty[st], ((jv / C::kVStages) - 1) & 1);
-        mbar_expect_tx(&v_full[st], C::kTileBytes);
-#pragma unroll
-        for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d_hint(sV + st * C::kTileBytes + c * (kBN * 128), &tm_v, &v_full[st],
-                           c * 64, kh, (t_begin + jv) * kBN, pol_kv);
-      }
-    }
-  } else if (warp == 9) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc_s = idesc_bf16_f32(kBM, kSub, 0, 0);
-      constexpr uint32_t idesc_o = idesc_bf16_f32(kBM, HD, 0, 1);
-      const uint32_t sk = smem_u32(sK), sv = smem_u32(sV), sq = smem_u32(sQ);
-      // S(s): group s & 1, its sub-tile i = s >> 1 into buffer i & 1
-      auto issue_s = [&](int s) {
-        const int g = s & 1, b = (s >> 1) & 1;
-        const uint32_t kb =
-            sk + ((s >> 1) % C::kKStages) * C::kTileBytes + (s & 1) * (kSub * 128);
-#pragma unroll
-        for (int k = 0; k < HD / 16; ++k) {
-          const uint32_t kk = (k & 3) * 32;
-          umma_bf16(tmem + C::col_s(g, b), sdesc_sw128(sq + (k >> 2) * (kBM * 128) + kk, 16, 1024),
-                    sdesc_sw128(kb + (k >> 2) * (kBN * 128) + kk, 16, 1024), idesc_s, k > 0);
-        }
-        umma_commit(&s_full[g * 2 + b]);
-      };
-      auto issue_pv = [&](int s) {
-        const int g = s & 1, i = s >> 1, b = i & 1;
-        const uint32_t vb = sv + ((s >> 1) % C::kVStages) * C::kTileBytes;
-#pragma unroll
-        for (int kk = 0; kk < kSub / 16; ++kk) {
-          const int k = (s & 1) * (kSub / 16) + kk;
-          umma_bf16_tmem_a(tmem + C::col_o(g), tmem + C::col_s(g, b) + kk * 8,
-                           sdesc_sw128(vb + k * (16 * 128), kBN * 128, 1024), idesc_o,
-                           (i > 0) || (kk > 0));
-        }
-        umma_commit(&o_full[g * 2 + b]);
-      };
-      auto wait_k = [&](int j) {
-        mbar_wait(&k_full[j % C::kKStages], (j / C::kKStages) & 1);
-        tc_fence_after();
-      };
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      // prologue: both groups' first two sub-tiles (K tiles 0 and 1)
-      for (int s = 0; s < 4 && s < nsub; ++s) {
-        if ((s & 1) == 0) wait_k(s >> 1);
-        issue_s(s);
-        if ((s & 1) == 1 || s == nsub - 1) umma_commit(&k_empty[(s >> 1) % C::kKStages]);
-      }
-      for (int s = 0; s < nsub; ++s) {
-        const int g = s & 1, i = s >> 1;
-        mbar_wait(&p_full[g * 2 + (i & 1)], (i >> 1) & 1);
-        if ((s & 1) == 0) {
-          mbar_wait(&v_full[(s >> 1) % C::kVStages], ((s >> 1) / C::kVStages) & 1);
-        }
-        tc_fence_after();
-        issue_pv(s);
-        if ((s & 1) == 1 || s == nsub - 1) umma_commit(&v_empty[(s >> 1) % C::kVStages]);
-        const int nx = s + 4;  // the same group's sub-tile i + 2, same S buffer
-        if (nx < nsub) {
-          if ((nx & 1) == 0) wait_k(nx >> 1);
-          issue_s(nx);
-          if ((nx & 1) == 1 || nx == nsub - 1) umma_commit(&k_empty[(nx >> 1) % C::kKStages]);
-        }
-      }
-    }
-  } else if (warp < 8) {
-    // ------------------------------------------------------------ softmax groups
-    const int g = warp >> 2;
-    const int r = (warp & 3) * 32 + lane;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t t_o = tmem + lane_off + C::col_o(g);
-    const int row_limit = p.n_cached + tok(q0 + r);
-    const float sl2 = p.scale_log2;
-    const int my_sub = (nsub - g + 1) / 2;   // sub-tiles s = 2 i + g
-    float m_acc = -INFINITY, l_acc = 0.f;
-    auto tile = [&](auto mask_tag, int i, int lim) {
-      constexpr bool kMask = decltype(mask_tag)::value;
-      const uint32_t t_s = tmem + lane_off + C::col_s(g, i & 1);
-      uint32_t sr[kSub];
-#pragma unroll
-      for (int c = 0; c < kSub / 32; ++c)
-        tmem_ld32_nowait(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
-      tmem_wait_ld();
-      if (kMask) {
-#pragma unroll
-        for (int e = 0; e < kSub; ++e) sr[e] = (e <= lim) ? sr[e] : 0xff800000u;  // -inf
-      }
-      float a0 = fmaxf(__uint_as_float(sr[0]), __uint_as_float(sr[1]));
-      float a1 = fmaxf(__uint_as_float(sr[2]), __uint_as_float(sr[3]));
-      float a2 = fmaxf(__uint_as_float(sr[4]), __uint_as_float(sr[5]));
-      float a3 = fmaxf(__uint_as_float(sr[6]), __uint_as_float(sr[7]));
-#pragma unroll
-      for (int e = 8; e < kSub; e += 8) {
-        a0 = fmax3(a0, __uint_as_float(sr[e + 0]), __uint_as_float(sr[e + 1]));
-        a1 = fmax3(a1, __uint_as_float(sr[e + 2]), __uint_as_float(sr[e + 3]));
-        a2 = fmax3(a2, __uint_as_float(sr[e + 4]), __uint_as_float(sr[e + 5]));
-        a3 = fmax3(a3, __uint_as_float(sr[e + 6]), __uint_as_float(sr[e + 7]));
-      }
-      const float m_tile = fmax3(fmax3(a0, a1, a2), a3, -INFINITY) * sl2;
-      const bool need = m_tile > m_acc + C::kRescaleLog2;
-      if (i == 0) {
-        if (need) m_acc = m_tile;
-      } else if (__any_sync(0xffffffffu, need)) {
-        // O_g holds sub-tiles < i: PV_g(i-2) finished before S_g(i) reused its
-        // buffer, so only PV_g(i-1) can be in flight
-        mbar_wait(&o_full[g * 2 + ((i - 1) & 1)], ((i - 1) >> 1) & 1);
-        tc_fence_after();
-        const float f = need ? ex2(m_acc - m_tile) : 1.f;
-#pragma unroll 1
-        for (int c = 0; c < HD / 32; ++c) {
-          float ov[32];
-          tmem_ld32(t_o + c * 32, ov);
-#pragma unroll
-          for (int e = 0; e < 32; ++e) ov[e] *= f;
-          tmem_st32(t_o + c * 32, ov);
-        }
-        tmem_wait_st();
-        if (need) {
-          l_acc *= f;
-          m_acc = m_tile;
-        }
-      }
-      const float neg_m = (m_acc == -INFINITY) ? 0.f : -m_acc;
-      const float2 sl2v = make_float2(sl2, sl2), negm2 = make_float2(neg_m, neg_m);
-      float2 ls0 = make_float2(0.f, 0.f), ls1 = ls0, ls2 = ls0, ls3 = ls0;
-#pragma unroll
-      for (int c = 0; c < kSub / 32; ++c) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const int k = c * 32 + e;
-          const float2 x = ffma2(make_float2(__uint_as_float(sr[k]), __uint_as_float(sr[k + 1])),
-                                 sl2v, negm2);
-          const float2 pp = (!kMask && ((e >> 1) & 3) == 3) ? ex2_poly2(x)
-                                                             : make_float2(ex2(x.x), ex2(x.y));
-          switch ((e >> 1) & 3) {
-            case 0: ls0 = fadd2(ls0, pp); break;
-            case 1: ls1 = fadd2(ls1, pp); break;
-            case 2: ls2 = fadd2(ls2, pp); break;
-            default: ls3 = fadd2(ls3, pp); break;
-          }
-          pk[e >> 1] = pack_bf16x2(pp.x, pp.y);
-        }
-        tmem_st16(t_s + c * 16, pk);
-      }
-      const float2 la = fadd2(ls0, ls1), lb = fadd2(ls2, ls3);
-      l_acc += (la.x + la.y) + (lb.x + lb.y);
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&p_full[g * 2 + (i & 1)]);
-    };
-    for (int i = 0; i < my_sub; ++i) {
-      mbar_wait(&s_full[g * 2 + (i & 1)], (i >> 1) & 1);
-      tc_fence_after();
-      const int kbase = key0 + (2 * i + g) * kSub;
-      if (kbase + kSub - 1 > p.n_cached + tok(q0))
-        tile(std::true_type{}, i, row_limit - kbase);
-      else
-        tile(std::false_type{}, i, 0);
-    }
-    // the group's last two PVs may both be in flight (one per o_full buffer)
-    if (my_sub > 1) mbar_wait(&o_full[g * 2 + ((my_sub - 2) & 1)], ((my_sub - 2) >> 1) & 1);
-    if (my_sub > 0) mbar_wait(&o_full[g * 2 + ((my_sub - 1) & 1)], ((my_sub - 1) >> 1) & 1);
-    tc_fence_after();
-    // ---- merge the groups' (m, l, O) through TMEM, each writes half the dims
-    const uint32_t t_ml = tmem + lane_off + C::col_s(g, 0);  // free after the last PV
-    tmem_st2(t_ml, m_acc, l_acc);
-    tmem_wait_st();
-    tc_fence_before();
-    named_bar_sync(1, 256);
-    tc_fence_after();
-    float m0, l0, m1, l1;
-    tmem_ld2(tmem + lane_off + C::col_s(0, 0), m0, l0);
-    tmem_ld2(tmem + lane_off + C::col_s(1, 0), m1, l1);
-    const float m_fin = fmaxf(m0, m1);
-    const float f0 = l0 > 0.f ? ex2(m0 - m_fin) : 0.f;
-    const float f1 = l1 > 0.f ? ex2(m1 - m_fin) : 0.f;
-    const float l_fin = l0 * f0 + l1 * f1;
-    const float inv_l = l_fin > 0.f ? 1.f / l_fin : 0.f;
-    const int qi = q0 + r;
-    const int col0 = g * (HD / 2);
-    for (int c = 0; c < HD / 64; ++c) {
-      const int col = col0 + c * 32;
-      float a[32], b[32];
-      tmem_ld32(tmem + lane_off + C::col_o(0) + col, a);
-      tmem_ld32(tmem + lane_off + C::col_o(1) + col, b);
-      float o[32];
-#pragma unroll
-      for (int e = 0; e < 32; ++e) {
-        const float x = f0 > 0.f ? a[e] * f0 : 0.f;
-        const float y = f1 > 0.f ? b[e] * f1 : 0.f;
-        o[e] = (x + y) * inv_l;
-      }
-      if (r >= rows) continue;
-      if (!partial) {
-        __nv_bfloat16* dst = p.out + out_row(qi) * HD + col;
-#pragma unroll
-        for (int e = 0; e < 32; e += 8) {
-          uint4 v;
-          v.x = pack_bf16x2(o[e + 0], o[e + 1]);
-          v.y = pack_bf16x2(o[e + 2], o[e + 3]);
-          v.z = pack_bf16x2(o[e + 4], o[e + 5]);
-          v.w = pack_bf16x2(o[e + 6], o[e + 7]);
-          *reinterpret_cast<uint4*>(dst + e) = v;
-        }
-      } else {
-        const int64_t row = (int64_t)split * p.n_new * p.hq + out_row(qi);
-        float4* po = reinterpret_cast<float4*>(p.part_o + row * HD + col);
-#pragma unroll
-        for (int e = 0; e < 32; e += 4) po[e / 4] = make_float4(o[e], o[e + 1], o[e + 2], o[e + 3]);
-        if (c == 0 && g == 0)
-          p.part_lse[row] = l_fin > 0.f ? m_fin + __log2f(l_fin) : -INFINITY;
-      }
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 8) {
-    tc_fence_after();
-    tmem_dealloc(tmem, C::kTmemCols);
-  }
-  if (p.num_splits == 1) launch_stamp_end(p.stamp);
-}
-
 // Deterministic split-KV combine: one warp per (query, head), splits in order.
 template <int HD>
 __global__ void __launch_bounds__(128)
@@ -1039,17 +655,6 @@ bool use_pairs(int q_tiles, int hq, int sms) {
   return q_tiles * hq > sms;
 }
 
-// Kernel 4 (64-key sub-tiles, double-buffered S per warpgroup) for unpaired
-// launches: ASKV_ATTN_KERNEL=4 (measurement knob).
-bool use_sub_kernel() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("ASKV_ATTN_KERNEL");
-    v = (e && e[0] == '4') ? 1 : 0;
-  }
-  return v == 1;
-}
-
 // GQA packing: when q-heads share a kv head, one CTA's
 // 128 query rows are (token, q-head) pairs of a kv head, so each K/V tile
 // feeds rows of every head of the group and a skinny prefill pads less (a
@@ -1130,17 +735,7 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
     prm.part_lse = prm.part_o + (size_t)splits * rows_qh * HD;
   }
   dim3 grid(q_groups, pack > 1 ? hkv : hq, splits);
-  if (!paired && use_sub_kernel()) {
-    auto kern = attn_sub_kernel<HD>;
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           SubCfg<HD>::kSmemBytes);
-      if (e != cudaSuccess) return cuda_status(e, "attn smem attribute");
-      attr = true;
-    }
-    kern<<<grid, SubCfg<HD>::kThreads, SubCfg<HD>::kSmemBytes, stream>>>(mq, mk, mv, prm);
-  } else if (paired) {
+  if (paired) {
     auto kern = attn_fwd_kernel<HD, true>;
     static bool attr = false;
     if (!attr) {
