@@ -93,13 +93,15 @@ int main(int argc, char** argv) {
          "tmem->first S %.2f | WG0 tile loop %.2f | last tile->epilogue %.2f | epilogue->exit %.2f\n",
          cnt, s_entry / cnt * 1e-3, s_tmem / cnt * 1e-3, s_q / cnt * 1e-3, s_first / cnt * 1e-3,
          s_loop / cnt * 1e-3, s_epi / cnt * 1e-3, s_exit / cnt * 1e-3);
-  for (int c : {0, ran / 2, ran - 1}) {
+  for (int c : {0, 1, ran / 2, ran - 1}) {
     const unsigned long long* r = &h[c * 192];
     printf("cta %d: entry %.2f tmem %.2f q %.2f |", c, (r[0] - t0) * 1e-3, (r[1] - t0) * 1e-3,
            (r[2] - t0) * 1e-3);
     for (int t = 0; t < 28 && r[8 + 2 * t]; ++t)
       printf(" [%.2f %.2f]", (r[8 + 2 * t] - t0) * 1e-3, (r[9 + 2 * t] - t0) * 1e-3);
-    printf(" | epi %.2f exit %.2f\n", (r[3] - t0) * 1e-3, (r[4] - t0) * 1e-3);
+    printf(" | epi %.2f merged %.2f stored %.2f synced %.2f exit %.2f\n", (r[3] - t0) * 1e-3,
+           r[5] ? (r[5] - t0) * 1e-3 : 0.0, r[6] ? (r[6] - t0) * 1e-3 : 0.0,
+           r[7] ? (r[7] - t0) * 1e-3 : 0.0, (r[4] - t0) * 1e-3);
     printf("   mma: P(j) seen / V(j) ready / PV(j) issued / K(j+2) ready:");
     for (int t = 0; t < 28 && r[64 + t]; ++t)
       printf(" [%.2f %.2f %.2f %.2f]", (r[64 + t] - t0) * 1e-3, (r[96 + t] - t0) * 1e-3,
