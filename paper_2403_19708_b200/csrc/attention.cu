@@ -104,20 +104,6 @@ struct AttnParams {
 // Warps: 0-3 WG0, 4-7 WG1, 8 TMA Q + K (+ TMEM alloc), 9 MMA, 10 TMA V.
 // ============================================================================
 
-// Which exponential pairs take the FMA-pipe polynomial instead of MUFU:
-// ASKV_POLY_EVERY = 4 -> one pair in four (default), 2 -> half, 0 -> none
-// (build-time measurement knob).
-#ifndef ASKV_POLY_EVERY
-#define ASKV_POLY_EVERY 4
-#endif
-__device__ __forceinline__ constexpr bool poly_pair(int pair) {
-#if ASKV_POLY_EVERY > 0
-  return pair % ASKV_POLY_EVERY == ASKV_POLY_EVERY - 1;
-#else
-  return false;
-#endif
-}
-
 template <int HD, bool kAllowPair>
 struct Cfg {
   // K is consumed early (S) and V late (PV), so K gets the deeper ring when
@@ -222,46 +208,39 @@ __global__ void __launch_bounds__(352, 1)
     return;
   }
 
-  // Warp 8 lane 0 initialises the barriers and starts the Q, first K and first
-  // V loads before the TMEM allocation and the CTA-wide barrier, so the
-  // load latency overlaps the set-up (in-kernel trace: alloc + barrier
-  // ~0.6 us, then Q landed ~0.9 us later).
-  const uint64_t pol_kv = l2_policy_evict_last();  // K/V re-read by every q tile of the head
-  const int k_pre = min(n_tiles, C::kKStages), v_pre = min(n_tiles, C::kVStages);
-  auto load_k = [&](int jk) {
-    const int st = jk % C::kKStages;
-    mbar_expect_tx(&k_full[st], C::kTileBytes);
-#pragma unroll
-    for (int c = 0; c < C::kChunks; ++c)
-      tma_load_3d_hint(sK + st * C::kTileBytes + c * (kBN * 128), &tm_k, &k_full[st], c * 64, kh,
-                       (t_begin + jk) * kBN, pol_kv);
-  };
-  auto load_v = [&](int jv) {
-    const int st = jv % C::kVStages;
-    mbar_expect_tx(&v_full[st], C::kTileBytes);
-#pragma unroll
-    for (int c = 0; c < C::kChunks; ++c)
-      tma_load_3d_hint(sV + st * C::kTileBytes + c * (kBN * 128), &tm_v, &v_full[st], c * 64, kh,
-                       (t_begin + jv) * kBN, pol_kv);
-  };
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < C::kKStages; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < C::kVStages; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int w = 0; w < 2; ++w) {
+      mbar_init(&s_full[w], 1);
+      mbar_init(&p_full[w], 128);
+      mbar_init(&o_full[w], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 8) tmem_alloc(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) ATTN_TRACE(1);
+
   if (warp == 8) {
+    // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      mbar_init(q_full, 1);
-      for (int s = 0; s < C::kKStages; ++s) {
-        mbar_init(&k_full[s], 1);
-        mbar_init(&k_empty[s], 1);
-      }
-      for (int s = 0; s < C::kVStages; ++s) {
-        mbar_init(&v_full[s], 1);
-        mbar_init(&v_empty[s], 1);
-      }
-      for (int w = 0; w < 2; ++w) {
-        mbar_init(&s_full[w], 1);
-        mbar_init(&p_full[w], 128);
-        mbar_init(&o_full[w], 1);
-      }
-      fence_mbar_init();
-      // Q is read once: evict first
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      // K/V tiles are re-read by every query tile of the head: keep them in L2
+      // against streaming traffic (the pre-loader's DMA writes); Q is read once.
+      const uint64_t pol_kv = l2_policy_evict_last();
       const uint64_t pol_q = l2_policy_evict_first();
       const int qt = paired ? 2 : 1;
       mbar_expect_tx(q_full, qt * C::kTileBytes);
@@ -270,36 +249,32 @@ __global__ void __launch_bounds__(352, 1)
         for (int c = 0; c < C::kChunks; ++c)
           tma_load_3d_hint(sQ + t * C::kTileBytes + c * (kBM * 128), &tm_q, q_full, c * 64,
                            pack > 1 ? h * pack : h, tok(q0 + t * kBM), pol_q);
-      for (int j = 0; j < k_pre; ++j) load_k(j);
-      for (int j = 0; j < v_pre; ++j) load_v(j);
-    }
-    __syncwarp();
-    tmem_alloc(tmem_slot, C::kTmemCols);
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) ATTN_TRACE(1);
-
-  if (warp == 8) {
-    // ------------------------------------------------------------ TMA producer (K)
-    // K tiles: as far ahead as the K ring allows (S(j) needs K(j) well before
-    // PV(j) needs V(j)); V tiles come from warp 10, so a V slot still held by
-    // a PV in flight never delays the next K (in-kernel trace: with one
-    // ordered producer the MMA warp waited ~0.55 us per tile for K(j+2)).
-    if (lane == 0) {
-      for (int jk = k_pre; jk < n_tiles; ++jk) {
-        mbar_wait(&k_empty[jk % C::kKStages], ((jk / C::kKStages) - 1) & 1);
-        load_k(jk);
+      // K tiles: as far ahead as the K ring allows (S(j) needs K(j) well before
+      // PV(j) needs V(j)); V tiles come from warp 10, so a V slot still held by
+      // a PV in flight never delays the next K (in-kernel trace: with one
+      // ordered producer the MMA warp waited ~0.55 us per tile for K(j+2)).
+      for (int jk = 0; jk < n_tiles; ++jk) {
+        const int st = jk % C::kKStages;
+        if (jk >= C::kKStages) mbar_wait(&k_empty[st], ((jk / C::kKStages) - 1) & 1);
+        mbar_expect_tx(&k_full[st], C::kTileBytes);
+#pragma unroll
+        for (int c = 0; c < C::kChunks; ++c)
+          tma_load_3d_hint(sK + st * C::kTileBytes + c * (kBN * 128), &tm_k, &k_full[st],
+                           c * 64, kh, (t_begin + jk) * kBN, pol_kv);
       }
     }
   } else if (warp == 10) {
     // ------------------------------------------------------------ TMA producer (V)
     if (lane == 0) {
-      for (int jv = v_pre; jv < n_tiles; ++jv) {
-        mbar_wait(&v_empty[jv % C::kVStages], ((jv / C::kVStages) - 1) & 1);
-        load_v(jv);
+      const uint64_t pol_kv = l2_policy_evict_last();
+      for (int jv = 0; jv < n_tiles; ++jv) {
+        const int st = jv % C::kVStages;
+        if (jv >= C::kVStages) mbar_wait(&v_empty[st], ((jv / C::kVStages) - 1) & 1);
+        mbar_expect_tx(&v_full[st], C::kTileBytes);
+#pragma unroll
+        for (int c = 0; c < C::kChunks; ++c)
+          tma_load_3d_hint(sV + st * C::kTileBytes + c * (kBN * 128), &tm_v, &v_full[st],
+                           c * 64, kh, (t_begin + jv) * kBN, pol_kv);
       }
     }
   } else if (warp == 9) {
@@ -466,7 +441,7 @@ __global__ void __launch_bounds__(352, 1)
                                  sl2v, negm2);
           // a quarter of the exponentials go to the FMA pipe (packed cubic) so
           // MUFU and FMA share the load; masked tiles keep MUFU (exact zeros)
-          const float2 pp = (!kMask && poly_pair(e >> 1)) ? ex2_poly2(x)
+          const float2 pp = (!kMask && ((e >> 1) & 3) == 3) ? ex2_poly2(x)
                                                              : make_float2(ex2(x.x), ex2(x.y));
           switch ((e >> 1) & 3) {
             case 0: ls0 = fadd2(ls0, pp); break;
@@ -512,7 +487,6 @@ __global__ void __launch_bounds__(352, 1)
       tc_fence_before();
       named_bar_sync(1, 256);
       tc_fence_after();
-      if (threadIdx.x == 0) ATTN_TRACE(5);
       float m0, l0, m1, l1;
       tmem_ld2(tmem + lane_off + C::col_s(0) + 64, m0, l0);
       tmem_ld2(tmem + lane_off + C::col_s(1) + 64, m1, l1);
@@ -528,29 +502,12 @@ __global__ void __launch_bounds__(352, 1)
     const float inv_l = l_fin > 0.f ? 1.f / l_fin : 0.f;
     const int rows_g = paired ? (w ? rows_b : rows_a) : rows_a;
     const int qi = qt0 + r;
-    if (partial && r < rows_g && (paired || w == 0))
-      p.part_lse[(int64_t)split * p.n_new * p.hq + out_row(qi)] =
-          l_fin > 0.f ? m_fin + __log2f(l_fin) : -INFINITY;
-    // Normalised rows go through shared memory (free: every MMA has completed
-    // once both groups pass the barrier below) so the global stores are
-    // row-contiguous -- a thread-per-row store touches 32 rows per warp
-    // instruction and cost 2-4 us per CTA (tools/attn_trace.cu).  16-byte
-    // chunks are XOR-swizzled by (row & 7) against bank conflicts.
-    if (paired) {
-      tc_fence_before();
-      named_bar_sync(1, 256);
-      tc_fence_after();
-    }
-    const int ebytes = partial ? 4 : 2;
-    const int cpr = HD * ebytes / 16;  // 16-byte chunks per row
-    uint8_t* stage = smem + (paired ? w * (kBM * HD * 4) : 0);
     const uint32_t t_o_other = tmem + lane_off + C::col_o(w ^ 1);
     for (int c = 0; c < ncols / 32; ++c) {
       const int col = col0 + c * 32;
       float a[32], b[32];
-      tmem_ld32_nowait(t_o + col, *reinterpret_cast<uint32_t(*)[32]>(a));
-      if (!paired) tmem_ld32_nowait(t_o_other + col, *reinterpret_cast<uint32_t(*)[32]>(b));
-      tmem_wait_ld();
+      tmem_ld32(t_o + col, a);
+      if (!paired) tmem_ld32(t_o_other + col, b);
       float o[32];
 #pragma unroll
       for (int e = 0; e < 32; ++e) {
@@ -558,58 +515,33 @@ __global__ void __launch_bounds__(352, 1)
         const float y = (!paired && f_other > 0.f) ? b[e] * f_other : 0.f;
         o[e] = (x + y) * inv_l;
       }
-      uint8_t* srow = stage + r * (cpr * 16);
-      if (!partial) {
+      if (r < rows_g) {
+        if (!partial) {
+          __nv_bfloat16* dst = p.out + out_row(qi) * HD + col;
 #pragma unroll
-        for (int e = 0; e < 32; e += 8) {
-          const int ch = (col + e) / 8;
-          uint4 v;
-          v.x = pack_bf16x2(o[e + 0], o[e + 1]);
-          v.y = pack_bf16x2(o[e + 2], o[e + 3]);
-          v.z = pack_bf16x2(o[e + 4], o[e + 5]);
-          v.w = pack_bf16x2(o[e + 6], o[e + 7]);
-          *reinterpret_cast<uint4*>(srow + ((ch ^ (r & 7)) * 16)) = v;
-        }
-      } else {
+          for (int e = 0; e < 32; e += 8) {
+            uint4 v;
+            v.x = pack_bf16x2(o[e + 0], o[e + 1]);
+            v.y = pack_bf16x2(o[e + 2], o[e + 3]);
+            v.z = pack_bf16x2(o[e + 4], o[e + 5]);
+            v.w = pack_bf16x2(o[e + 6], o[e + 7]);
+            *reinterpret_cast<uint4*>(dst + e) = v;
+          }
+        } else {
+          const int64_t row = (int64_t)split * p.n_new * p.hq + out_row(qi);
+          float4* po = reinterpret_cast<float4*>(p.part_o + row * HD + col);
 #pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          const int ch = (col + e) / 4;
-          *reinterpret_cast<float4*>(srow + ((ch ^ (r & 7)) * 16)) =
-              make_float4(o[e], o[e + 1], o[e + 2], o[e + 3]);
+          for (int e = 0; e < 32; e += 4)
+            po[e / 4] = make_float4(o[e], o[e + 1], o[e + 2], o[e + 3]);
+          if (c == 0 && (paired || w == 0))
+            p.part_lse[row] = l_fin > 0.f ? m_fin + __log2f(l_fin) : -INFINITY;
         }
       }
     }
-    named_bar_sync(1, 256);
-    if (threadIdx.x == 0) ATTN_TRACE(6);
-    // cooperative row-contiguous stores: 256 threads, one 16-byte chunk each
-    auto store_tiles = [&](auto cpr_tag) {
-      constexpr int kCpr = decltype(cpr_tag)::value;
-      for (int g = 0; g < (paired ? 2 : 1); ++g) {
-        const int rows_t = g ? rows_b : rows_a;
-        const int q_t = q0 + g * kBM;
-        const uint8_t* st = smem + g * (kBM * HD * 4);
-        for (int i = threadIdx.x; i < rows_t * kCpr; i += 256) {  // warps 0-7
-          const int row = i / kCpr, ch = i % kCpr;
-          const uint4 v = *reinterpret_cast<const uint4*>(st + row * (kCpr * 16) +
-                                                          ((ch ^ (row & 7)) * 16));
-          const int64_t orow = out_row(q_t + row);
-          uint8_t* dst = partial
-              ? reinterpret_cast<uint8_t*>(p.part_o +
-                                           ((int64_t)split * p.n_new * p.hq + orow) * HD)
-              : reinterpret_cast<uint8_t*>(p.out + orow * HD);
-          *reinterpret_cast<uint4*>(dst + ch * 16) = v;
-        }
-      }
-    };
-    if (partial)
-      store_tiles(std::integral_constant<int, HD / 4>{});
-    else
-      store_tiles(std::integral_constant<int, HD / 8>{});
   }
 
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) ATTN_TRACE(7);
   if (warp == 8) {
     tc_fence_after();
     tmem_dealloc(tmem, C::kTmemCols);

@@ -14,7 +14,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 
-def timeit(fn, reps=20, flush=True):
+def timeit(fn, reps=20, flush=True, batch=1):
     buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(3):
         fn()
@@ -27,10 +27,11 @@ def timeit(fn, reps=20, flush=True):
             torch.cuda._sleep(200000)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        fn()
+        for _ in range(batch):
+            fn()
         e1.record()
         torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1) * 1e-3)
+        ts.append(e0.elapsed_time(e1) * 1e-3 / batch)
     ts.sort()
     return ts[len(ts) // 2]
 
@@ -52,7 +53,7 @@ def attn(args):
         ws = torch.empty(max(1, ops.attn_workspace_bytes(kept, n, hq, d, s)), dtype=torch.uint8,
                          device="cuda")
         t = timeit(lambda: ops.prefill_attn(q, kv, kept, n, hq, hkv, d, o, ws, num_splits=s),
-                   reps=args.reps, flush=not args.warm)
+                   reps=args.reps, flush=not args.warm, batch=args.batch)
         fl = attention_flops(kept, n, hq, d)
         row = dict(kept=kept, n=n, hq=hq, hkv=hkv, splits=s, us=t * 1e6, tflops=fl / t / 1e12,
                    l2="warm" if args.warm else "flushed")
@@ -107,6 +108,7 @@ if __name__ == "__main__":
     ap.add_argument("--shape", default="", help="kept,n,hq,hkv")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--warm", action="store_true", help="no L2 flush between reps")
+    ap.add_argument("--batch", type=int, default=1, help="launches per timed rep (averaged)")
     a = ap.parse_args()
     os.environ["ASKV_ATTN_KERNEL"] = a.kernel
     {"attn": attn, "reembed": reembed, "sweep": sweep}[a.what](a)
