@@ -125,13 +125,22 @@ struct Cfg {
   // TMEM columns: S of group w at 128*w, O of group w at 256 + 128*w
   __host__ __device__ static constexpr uint32_t col_s(int w) { return 128u * (uint32_t)w; }
   __host__ __device__ static constexpr uint32_t col_o(int w) { return 256u + 128u * (uint32_t)w; }
-  static constexpr int kThreads = 352;
+#ifndef ASKV_ATTN_SOFTMAX_REGS
+#define ASKV_ATTN_SOFTMAX_REGS 224
+#endif
+  // > 0: a 12th (idle) warp completes warpgroup 2 so the producer / MMA
+  // warps (56 registers each) hand their registers to the softmax
+  // warpgroups (setmaxnreg).  The launch-bound cap for 11-12 warps is 168
+  // registers, which spilled in the softmax (96 B/thread); with 224: no
+  // spills, paired shapes -12 %, C3 -1 % (tools/kbench.py --batch 50)
+  static constexpr int kSoftmaxRegs = ASKV_ATTN_SOFTMAX_REGS;
+  static constexpr int kThreads = kSoftmaxRegs > 0 ? 384 : 352;
   static constexpr float kRescaleLog2 = 8.0f;
   static_assert(kSmemBytes <= 232448, "smem budget");
 };
 
 template <int HD, bool kAllowPair>
-__global__ void __launch_bounds__(352, 1)
+__global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
@@ -231,9 +240,15 @@ __global__ void __launch_bounds__(352, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) ATTN_TRACE(1);
+  // kSoftmaxRegs > 0: each role branch resizes its registers first
+  // (4 x 32 x 56 + 8 x 32 x kSoftmaxRegs <= 64 K)
+  auto shrink = [] {
+    if constexpr (C::kSoftmaxRegs > 0) setmaxnreg_dec<56>();
+  };
 
   if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
+    shrink();
     if (lane == 0) {
       tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_k);
@@ -265,6 +280,7 @@ __global__ void __launch_bounds__(352, 1)
     }
   } else if (warp == 10) {
     // ------------------------------------------------------------ TMA producer (V)
+    shrink();
     if (lane == 0) {
       const uint64_t pol_kv = l2_policy_evict_last();
       for (int jv = 0; jv < n_tiles; ++jv) {
@@ -279,6 +295,7 @@ __global__ void __launch_bounds__(352, 1)
     }
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
+    shrink();
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(kBM, kBN, 0, 0);
       constexpr uint32_t idesc_o = idesc_bf16_f32(kBM, HD, 0, 1);
@@ -368,6 +385,7 @@ __global__ void __launch_bounds__(352, 1)
     }
   } else if (warp < 8) {
     // ------------------------------------------------------------ softmax groups
+    if constexpr (C::kSoftmaxRegs > 0) setmaxnreg_inc<C::kSoftmaxRegs>();
     const int w = warp >> 2;
     const int r = (warp & 3) * 32 + lane;  // row in tile == TMEM lane
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
@@ -538,6 +556,8 @@ __global__ void __launch_bounds__(352, 1)
         }
       }
     }
+  } else {
+    shrink();  // warp 11: completes warpgroup 2 for setmaxnreg
   }
 
   tc_fence_before();
