@@ -52,8 +52,10 @@ def test_split_policy_without_gpu(built):
     assert lib.askv_attn_num_splits(2142, 100, 40, 148) == 3
     # 13B p50 turn (2 query tiles x 40 heads = 80 CTAs) already fills a wave
     assert lib.askv_attn_num_splits(2142, 237, 40, 148) == 1
-    # 70B TP8 rank (8 q-heads): split up to >= 4 KV tiles per split
-    assert lib.askv_attn_num_splits(2048, 256, 8, 148) == 5
+    # 70B TP8 rank (8 q-heads): split while >= 6 KV tiles per split remain
+    assert lib.askv_attn_num_splits(2048, 256, 8, 148) == 3
+    # short history: 9 KV tiles would leave 5 per split -- not worth a combine
+    assert lib.askv_attn_num_splits(1000, 100, 40, 148) == 1
     # full recompute of 2379 tokens fills the machine without splitting
     assert lib.askv_attn_num_splits(0, 2379, 40, 148) == 1
     assert lib.askv_attn_workspace_bytes(2142, 237, 40, 128, 4) == 4 * 237 * 40 * 129 * 4
