@@ -38,8 +38,16 @@ __global__ void __launch_bounds__(kNormThreads)
   }
   const int nvec = cols / 8;
   const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)row * cols);
-  uint4 v[VPT];
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  uint4 v[VPT], wv[VPT];
   float ss = 0.f;
+  // the weight vectors are loaded up front with x, so the scaled write does
+  // not wait a second memory latency after the reduction
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int idx = threadIdx.x + i * kNormThreads;
+    wv[i] = idx < nvec ? __ldg(wr + idx) : make_uint4(0, 0, 0, 0);
+  }
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
     const int idx = threadIdx.x + i * kNormThreads;
@@ -62,15 +70,13 @@ __global__ void __launch_bounds__(kNormThreads)
   }
   __syncthreads();
   const float scale = rsqrtf(red[0] / (float)cols + eps);
-  const uint4* wr = reinterpret_cast<const uint4*>(w);
   uint4* yr = reinterpret_cast<uint4*>(y + (int64_t)row * cols);
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
     const int idx = threadIdx.x + i * kNormThreads;
     if (idx >= nvec) break;
-    const uint4 wv = wr[idx];
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[i]);
-    const __nv_bfloat162* g = reinterpret_cast<const __nv_bfloat162*>(&wv);
+    const __nv_bfloat162* g = reinterpret_cast<const __nv_bfloat162*>(&wv[i]);
     uint4 o;
     uint32_t* op = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
