@@ -70,3 +70,28 @@ def test_argument_errors_without_gpu(built):
     assert b"multiple" in lib.askv_last_error()
     rc = lib.askv_save_layer(None, None, 1, 100, 0, 16, 8, 0, 40, None, None, None)
     assert rc == _lib.ASKV_EINVAL
+
+
+def test_attention_kernel_does_not_spill(built):
+    """K3's softmax warpgroups run with 224 registers (setmaxnreg); before the
+    register split the 168-register cap spilled ~100 B per thread inside the
+    tile loop.  Guard the split: the fused kernels keep (almost) no stack."""
+    import shutil
+    import subprocess
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not Path(tool).exists():
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([tool, "-res-usage", str(built)], capture_output=True, text=True,
+                         check=True).stdout
+    stacks = {}
+    name = None
+    for line in out.splitlines():
+        m = re.search(r"Function (\S+):", line)
+        if m:
+            name = m.group(1)
+            continue
+        m = re.search(r"STACK:(\d+)", line)
+        if m and name and "attn_fwd_kernel" in name:
+            stacks[name] = int(m.group(1))
+    assert len(stacks) == 4, stacks  # HD 64 / 128 x unpaired / paired
+    assert max(stacks.values()) <= 16, stacks
