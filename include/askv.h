@@ -65,6 +65,9 @@ int askv_rope_table(float* table, int max_pos, int head_dim, double theta_base, 
  * Replaces: rope.py:63-74 (rotate_matrix) at rope.py:138, KvRecord.truncated
  * rope.py:48-52, and the kept range of sim.py:468-483.
  * src/dst: device bf16.  Strides in elements.
+ * Precondition: every positions[i] lies in [0, table_positions) -- the kernel
+ * does not bound-check explicit positions (the pos0 form is checked; the
+ * Python numeric API checks explicit ones, ops._check_positions).
  */
 int askv_reembed(const void* src_base, const int64_t* src_block_off, int block_tokens,
                  int64_t src_row_stride, int64_t first_token, int kept, int n_kv_heads,
@@ -76,6 +79,7 @@ int askv_reembed(const void* src_base, const int64_t* src_block_off, int block_t
  * Rotate every head of n_rows rows x[i] = [heads][hd] at positions[i]
  * (device int32, or pos0 + i when NULL) into out[i].
  * Replaces: rope.py:63-74 (rotate_matrix) / rope.py:77-85 (rope_rotate).
+ * Precondition as askv_reembed: explicit positions within [0, table_positions).
  */
 int askv_rotate_rows(const void* x, int64_t x_row_stride, int n_rows, int n_heads,
                      int head_dim, const float* rope_table, int table_positions,
@@ -172,6 +176,9 @@ int askv_event_destroy(void* ev);
 int askv_event_record(void* ev, void* stream);
 int askv_stream_wait_event(void* stream, void* ev);
 int askv_event_elapsed_ms(void* start, void* end, float* ms);
+/* Block the calling host thread until the event's recorded work is done (the
+ * disk tier fences arena blocks on a session's in-flight copies with it). */
+int askv_event_synchronize(void* ev);
 
 /*
  * One job's full layer loop (the reuse prefill of N new tokens over `kept`

@@ -47,6 +47,7 @@ SIGNATURES = {
     "askv_event_record": (_i32, [_vp, _vp]),
     "askv_stream_wait_event": (_i32, [_vp, _vp]),
     "askv_event_elapsed_ms": (_i32, [_vp, _vp, C.POINTER(C.c_float)]),
+    "askv_event_synchronize": (_i32, [_vp]),
     "askv_prefill_layers": (_i32, [_vp, _vp]),
     "askv_prefill_plan_size": (_sz, []),
     "askv_stamp": (_i32, [_vp, _vp]),

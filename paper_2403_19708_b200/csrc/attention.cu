@@ -425,11 +425,17 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
       }
       const float m_tile = fmax3(fmax3(a0, a1, a2), a3, -INFINITY) * sl2;
       const bool need = m_tile > m_acc + C::kRescaleLog2;
+      if (t > 0) {
+        // Every PV's completion phase is consumed here (compute-sanitizer
+        // synccheck flags a phase nobody waits for).  Free: s_full of S(t) was
+        // committed after PV(t-1) was issued, and a commit tracks every earlier
+        // tcgen05 op of the issuing thread, so PV(t-1) is already complete.
+        mbar_wait(&o_full[w], (t - 1) & 1);
+      }
       if (t == 0) {
         if (need) m_acc = m_tile;
       } else if (__any_sync(0xffffffffu, need)) {
-        // O_w holds this group's tiles < t: wait for its last PV, rescale in place
-        mbar_wait(&o_full[w], (t - 1) & 1);
+        // O_w holds this group's tiles < t (their last PV waited above): rescale in place
         tc_fence_after();
         const float f = need ? ex2(m_acc - m_tile) : 1.f;
 #pragma unroll 1

@@ -236,12 +236,21 @@ std::vector<int64_t> graph_key(const askv_prefill_plan* p, cudaStream_t s) {
   // instantiating a graph each (~7 ms of host time for a 13B job); the split
   // count shapes the topology and stays in the key.  An update that fails
   // (different kernels) re-instantiates.
+  // The HBM-tier write-through / promotion copies are one memcpy node per
+  // block segment their rows touch; that count depends on where head + kept
+  // falls against the block boundaries, so it is part of the topology.
+  auto segs = [&](int64_t first, int64_t rows) -> int64_t {
+    if (rows <= 0 || p->block_tokens <= 0) return 0;
+    return (first + rows - 1) / p->block_tokens - first / p->block_tokens + 1;
+  };
+  const int64_t mirror_segs = p->mirror_base ? segs(p->head + p->kept, p->n_new) : 0;
+  const int64_t promote_segs = p->promote_base ? segs(p->head, p->kept) : 0;
   return {dev, p->layers, p->d_model, p->n_heads, p->n_kv_heads, p->head_dim, p->ffn,
           n_bucket(p->n_new), p->kept > 0, p->attn_splits, p->src_kind, p->block_tokens,
           has(p->save_rows), has(p->ev_src_ready), has(p->ev_src_free), has(p->ev_save_free),
           has(p->ev_save_ready), p->stamps ? p->stamp_flags : -1, has(p->kv_layers),
           has(p->kv_alt), has(p->mirror_base), p->mirror_nblocks, p->promote_nblocks,
-          (int64_t)(intptr_t)s};
+          mirror_segs, promote_segs, (int64_t)(intptr_t)s};
 }
 
 #define ASKV_TRY(expr)          \
@@ -287,6 +296,12 @@ extern "C" int askv_event_elapsed_ms(void* start, void* end, float* ms) {
   ASKV_REQUIRE(start && end && ms, "event_elapsed_ms: null pointer");
   return cuda_status(cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)end),
                      "cudaEventElapsedTime");
+}
+
+extern "C" int askv_event_synchronize(void* ev) {
+  clear_error();
+  ASKV_REQUIRE(ev != nullptr, "event_synchronize: null event");
+  return cuda_status(cudaEventSynchronize((cudaEvent_t)ev), "cudaEventSynchronize");
 }
 
 extern "C" int askv_stamp(uint64_t* dst, void* stream) {
@@ -442,9 +457,9 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
   // queues behind the H2D DMA and the GPU idles between kernels
   // (profiles/r01d_summary.md); a graph's nodes are resident on the device.
   // If the driver refuses the capture or the instantiation, the job is issued
-  // on the stream instead (same kernels, same order).  The tensor-parallel
-  // host callback and the HBM-tier promotion (batched D2D copies) issue as
-  // streams.
+  // on the stream instead (same kernels, same order).  A tensor-parallel
+  // host callback issues on the stream (a host function cannot be captured);
+  // the HBM-tier copies are captured (graph_key counts their segments).
   if (!p->graph || p->allreduce) return issue_layers(p, s);
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)

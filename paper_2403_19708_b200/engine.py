@@ -46,8 +46,10 @@ def save_truncate(tokens: int, window: int, cut: int) -> int:
 def rolling_kept(kept: int, sizes, window: int, cut: int) -> int:
     """Context after appending chunks with a rolling window: before each chunk
     that would overflow, drop `cut`-sized front chunks (sim.py:468-483).  For
-    chunk sizes <= cut this ends exactly at save_truncate(kept + sum(sizes))
-    (sim.py:576-581), which tests/test_store_cpu.py checks."""
+    chunk sizes <= min(cut, W - cut) this ends exactly at
+    save_truncate(kept + sum(sizes)) (sim.py:576-581), which
+    tests/test_store_cpu.py checks over ratios 0.1-0.9; a larger chunk can
+    overflow by more than the save-time rule drops (ratio 0.75, chunk > W/4)."""
     for c in sizes:
         if kept + c > window:
             kept = overflow_kept(kept, c, window, cut)
@@ -162,7 +164,7 @@ class HbmTier:
 
 class Engine:
     """One GPU's serving loop for the reuse path.  Prefills are processed in
-    chunks of at most `chunk` = min(max_new, cut) tokens (chunked prefill: a
+    chunks of at most `chunk` = min(max_new, cut, W - cut) tokens (chunked prefill: a
     chunk after the first reuses the rows its predecessor just saved), with the
     reference's window truncation applied before any chunk that would overflow,
     so positions never exceed the window."""
@@ -172,7 +174,7 @@ class Engine:
                  read_buffer_bytes: int = 1 << 30, max_new: int = 1024,
                  truncation_ratio: float = 0.5, ttl: float = math.inf, pin: bool = True,
                  tp_reduce=None, hbm_blocks: int = 0, disk_dir: str | None = None,
-                 disk_blocks: int = 0):
+                 disk_blocks: int = 0, autotune: bool | int = True):
         self.shape = shape
         self.profile = profile_for(shape, truncation_ratio=truncation_ratio)
         self.block_tokens = block_tokens
@@ -193,7 +195,9 @@ class Engine:
         self.prefetched: set[str] = set()
         self.window = shape.context_window
         self.cut = self.profile.cut_tokens
-        self.chunk = max(1, min(max_new, self.cut))
+        # chunks <= min(cut, W - cut) keep the rolling window equal to the
+        # reference's save-time truncation for every ratio (rolling_kept)
+        self.chunk = max(1, min(max_new, self.cut, self.window - self.cut))
         self.hbm = HbmTier(hbm_blocks, block_bytes, device) if hbm_blocks > 0 else None
         self.runner = Runner(shape, weights=weights, device=device, seed=seed,
                              block_tokens=block_tokens, host_arena=self.arena,
@@ -201,7 +205,9 @@ class Engine:
                              read_buffer_bytes=read_buffer_bytes, max_new=max_new,
                              max_ctx=self.window + self.chunk, tp_reduce=tp_reduce,
                              # tune the GEMMs over full prompts too (misses recompute them)
-                             autotune=self.window + self.chunk + max_new)
+                             autotune=(self.window + self.chunk + max_new
+                                       if autotune is True else autotune))
+        self.store.io_fence = self.runner.fence
         self.context: dict[str, int] = {}
         self.tokens: dict[str, torch.Tensor] = {}   # conversation token ids (for misses)
 
@@ -309,6 +315,8 @@ class Engine:
         n = int(ids.numel())
         if self.store.peek(sid) is not None:
             self.store.remove(sid)
+        if self.hbm is not None:
+            self.hbm.drop(sid)        # the rows are rewritten: a mirror would be stale
         tab = self.store.reserve_rows(sid, n)
         res = self.runner.run([Job(sid, ids, kept=0, source="none", block_ids=tab, save=True,
                                    head=self.store.head_row(sid))])[0]

@@ -25,6 +25,18 @@ def _ptr(t):
     return None if t is None else t.data_ptr()
 
 
+def _check_positions(positions, table: "RopeTable") -> None:
+    """Explicit positions index the cos/sin table, which the kernels do not
+    bound-check: every entry must lie in [0, table.max_pos) (a host sync; this
+    is the numeric API, the layer loop uses pos0 + i and is checked natively)."""
+    if positions is None or positions.numel() == 0:
+        return
+    lo, hi = int(positions.min()), int(positions.max())
+    if lo < 0 or hi >= table.max_pos:
+        raise ValueError(f"positions [{lo}, {hi}] outside the RoPE table's "
+                         f"[0, {table.max_pos})")
+
+
 def _require_cuda(*ts):
     for t in ts:
         if t is not None and not t.is_cuda:
@@ -63,6 +75,7 @@ def reembed(src: torch.Tensor, kept: int, n_kv_heads: int, head_dim: int, table:
             stream=None) -> None:
     """K2: dst[i] = [rope(K, pos), V] of source row first_token+i (see askv.h)."""
     _require_cuda(src, dst, block_off, positions)
+    _check_positions(positions, table)
     row = 2 * n_kv_heads * head_dim
     check(lib().askv_reembed(
         src.data_ptr(), _ptr(block_off), int(block_tokens),
@@ -75,6 +88,7 @@ def reembed(src: torch.Tensor, kept: int, n_kv_heads: int, head_dim: int, table:
 def rotate_rows(x: torch.Tensor, n_heads: int, head_dim: int, table: RopeTable,
                 out: torch.Tensor, *, positions=None, pos0: int = 0, stream=None) -> None:
     _require_cuda(x, out, positions)
+    _check_positions(positions, table)
     n = x.shape[0]
     check(lib().askv_rotate_rows(x.data_ptr(), int(x.stride(0)), int(n), int(n_heads),
                                  int(head_dim), table.table.data_ptr(), table.max_pos,
@@ -202,6 +216,10 @@ class NativeEvent:
     def wait(self, stream) -> None:
         """Make `stream` wait for this event."""
         check(lib().askv_stream_wait_event(stream.cuda_stream, self.handle), "stream_wait_event")
+
+    def synchronize(self) -> None:
+        """Block the host until the work recorded before this event is done."""
+        check(lib().askv_event_synchronize(self.handle), "event_synchronize")
 
     def elapsed_ms(self, end: "NativeEvent") -> float:
         ms = C.c_float()

@@ -332,6 +332,8 @@ class Runner:
         self._wflag: list = [None] * self.n_wslots   # host flag: slot's last save submitted
         self._sess_ev: dict = {}                     # session -> event of its last save
         self._last_save: dict = {}                   # session -> (event, host flag)
+        self._sess_load_ev: dict = {}                # session -> event of its last pre-load
+        self._last_load: dict = {}                   # session -> (event, host flag)
         self._pool = _EventPool()
         self._leases: dict = {}
         # device timestamp ring (globaltimer ns) for the compute-stream timeline:
@@ -450,7 +452,11 @@ class Runner:
         ids = list(job.block_ids[:nb])
         dep = self._last_save.get(job.session_id)
         lease = self._lease(jid)
-        for layer in range(self.shape.layers):
+        load_ev = self._sess_load_ev.get(job.session_id)
+        if load_ev is None:
+            load_ev = self._sess_load_ev[job.session_id] = ops.NativeEvent()
+        L = self.shape.layers
+        for layer in range(L):
             u = _Unit()
             u.seq = self._seq
             u.slot = u.seq % self.n_slots
@@ -476,12 +482,16 @@ class Runner:
                                       self.block_bytes, layer * self.chunk_bytes,
                                       self.chunk_bytes, tail, stream=sl)
                     self._slot_ready[u.slot].record(sl)
+                    if layer == L - 1:
+                        load_ev.record(sl)
                     if u.times:
                         u.times[1].record(sl)
                 finally:
                     u.issued.set()
 
             self._io_load.submit(submit)
+            if layer == L - 1:
+                self._last_load[job.session_id] = (load_ev, u.issued)
 
     def _acquire(self, jid, layer) -> _Unit:
         u = self._units.pop((jid, layer), None)
@@ -520,6 +530,23 @@ class Runner:
                 flag.set()
 
         self._io_save.submit(submit)
+
+    def fence(self, session_id: str | None = None) -> None:
+        """Block the host until the GPU copies touching the host arena are done:
+        the session's last pre-load (K1) and save (K4), or with None every
+        pre-load and save queued so far.  Host-side accesses to arena blocks
+        (the disk tier's pwrite / pread) call this first: the copy streams run
+        asynchronously to the host, and a freed block may still be the source of
+        an H2D or the target of a D2H in flight."""
+        if session_id is None:
+            self.drain_io()
+            self.s_load.synchronize()
+            self.s_save.synchronize()
+            return
+        for dep in (self._last_save.get(session_id), self._last_load.get(session_id)):
+            if dep is not None:
+                dep[1].wait()
+                dep[0].synchronize()
 
     def close(self) -> None:
         for t in (self._io_load, self._io_save):

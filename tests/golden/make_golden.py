@@ -18,6 +18,9 @@ Writes into tests/golden/:
   workload_c{1,2,3}.json generate_poisson sessions (trace.py:326-356) plus the
                          reference simulator's per-turn records in reuse mode
                          with unbounded tiers (sim.py:408-466)
+  sim_c2.json            full event logs + turn records of capacity-constrained
+                         C2 runs (evict_to_disk / evict_out / prefetch order,
+                         sim.py:298-366; policy.py)
 """
 
 from __future__ import annotations
@@ -223,12 +226,55 @@ def workloads():
             sessions=sessions, records=records)))
 
 
+# capacity-constrained C2 runs of the reference simulator: the event log pins
+# the scheduler-aware eviction / prefetch order (policy.py, sim.py:298-366)
+SIM_CASES = {
+    "sa_disk": dict(dram=12e9, disk=40e9, policy="scheduler-aware"),
+    "sa_nodisk": dict(dram=16e9, disk=0, policy="scheduler-aware"),
+    "lru_disk": dict(dram=12e9, disk=40e9, policy="lru"),
+    "sa_disk_window": dict(dram=10e9, disk=30e9, policy="scheduler-aware",
+                           prefetch_window=4, eviction_window=6),
+}
+
+
+def sim_golden():
+    from kvsim import policy
+    wl = trace.generate_poisson(64, 1.0, seed=7)
+    out = {}
+    for name, c in SIM_CASES.items():
+        prof = model.ModelProfile(name="7b", kv_bytes_per_token=float(kvb("7b")),
+                                  prefill_seconds_per_token=6e-5, decode_seconds_per_step=6e-3,
+                                  context_window=4096, layers=32)
+        tiers = model.TierConfig(hbm_read_buffer=int(4e9), hbm_write_buffer=int(2e9),
+                                 dram_capacity=int(c["dram"]), disk_capacity=int(c["disk"]),
+                                 pcie_bandwidth=55e9, disk_bandwidth=3.2e9)
+        pol = policy.PolicyConfig(kind=policy.PolicyKind(c["policy"]),
+                                  prefetch_window=c.get("prefetch_window"),
+                                  eviction_window=c.get("eviction_window"))
+        cfg = sim.SimConfig(profile=prof, tiers=tiers, policy=pol, mode=sim.Mode.REUSE,
+                            block_bytes=128 * kvb("7b"))
+        log = sim.run(wl, cfg)
+        out[name] = dict(
+            case=c, block_bytes=128 * kvb("7b"), kv_bytes_per_token=kvb("7b"),
+            events=[e.to_dict() for e in log.events],
+            turns=[dict(session=t.session_id, turn=t.turn_index, hit=t.hit_class,
+                        ttft=t.ttft_s, prefill=t.prefill_s, stall=t.stall_s,
+                        prompt=t.prompt_tokens, done=t.done, evicted=t.bytes_evicted)
+                   for t in log.turns],
+            meta=log.meta)
+    (OUT / "sim_c2.json").write_text(json.dumps(out))
+
+
 if __name__ == "__main__":
     np.seterr(all="ignore")
+    if sys.argv[1:] == ["sim"]:
+        sim_golden()
+        sys.exit(0)
     rope_golden()
     equivalence()
     truncation()
     store_golden()
     overlap_golden()
     workloads()
+    sim_golden()
     print("golden fixtures written to", OUT, file=sys.stderr)

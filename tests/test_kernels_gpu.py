@@ -280,19 +280,24 @@ def test_silu_mul_vs_torch_fp32(rows, ffn):
     assert torch.allclose(got, want, rtol=8e-3, atol=1e-2)
 
 
-@pytest.mark.parametrize("emu", ["0", "3", "5"])
-def test_attention_exp2_emulation_split(emu, monkeypatch):
-    """The FMA-pipe exp2 (ex2_poly) share is a tuning knob; every setting must
-    meet the same parity bar (checked in a subprocess: the knob is read once)."""
+@pytest.mark.parametrize("knob", ["ASKV_ATTN_PAIR=0", "ASKV_ATTN_PAIR=1", "ASKV_ATTN_PACK=0"])
+def test_attention_mode_knobs(knob):
+    """K3's measurement knobs (read once per process in csrc/attention.cu:
+    use_pairs / gqa_pack) force the paired / unpaired instances and turn GQA
+    packing off; every setting must meet the same parity bar (run in a
+    subprocess so the knob is read fresh)."""
+    import os
     import subprocess
     import sys
     code = (
         "import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
         "from test_kernels_gpu import *;"
         "test_prefill_attention_vs_oracle(2142, 237, 8, 8, 128, 0);"
-        "test_prefill_attention_vs_oracle(0, 300, 4, 4, 64, 1)")
-    env = dict(__import__("os").environ, ASKV_ATTN_EMU=emu)
-    root = __import__("os").path.dirname(__import__("os").path.dirname(__file__))
+        "test_prefill_attention_vs_oracle(0, 300, 4, 4, 64, 1);"
+        "test_prefill_attention_vs_oracle(700, 90, 8, 1, 128, 0)")
+    name, val = knob.split("=")
+    env = dict(os.environ, **{name: val})
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                        text=True)
     assert r.returncode == 0, r.stderr[-2000:]

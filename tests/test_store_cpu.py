@@ -152,6 +152,27 @@ def test_rolling_window_chunks_equal_save_truncation(kept, sizes, w):
                                                                           0.5)
 
 
+@pytest.mark.parametrize("ratio", [0.1, 0.25, 0.5, 0.75, 0.9])
+@pytest.mark.parametrize("w", [64, 100, 4096])
+def test_rolling_window_engine_chunk_any_ratio(ratio, w):
+    """The engine's chunk bound min(max_new, cut, W - cut) keeps the rolling
+    window equal to the reference's save-time truncation (sim.py:576-581) for
+    every truncation ratio, not only 0.5 (ratio 0.75 with chunks
+    > W - cut overflowed).  Exhaustive over kept / turn length on a grid."""
+    from paper_2403_19708_b200.engine import rolling_kept
+    cut = max(1, int(ratio * w))
+    chunk = max(1, min(2048, cut, w - cut))
+    for kept in range(0, w + 1, max(1, w // 32)):
+        for total in range(1, 3 * w, max(1, w // 40)):
+            sizes = [chunk] * (total // chunk) + ([total % chunk] if total % chunk else [])
+            assert rolling_kept(kept, sizes, w, cut) == \
+                layout_ref.save_truncate(kept + total, w, ratio), (kept, total)
+    # the bound is what makes it hold: ratio 0.75 with a chunk of W/2 breaks it
+    if ratio == 0.75 and w == 4096:
+        assert rolling_kept(2000, [3072], w, cut) != \
+            layout_ref.save_truncate(2000 + 3072, w, ratio)
+
+
 def _disk_store(tmp_path, blocks=16, tb=16, kvb=1024, disk_blocks=64):
     from paper_2403_19708_b200.disk import DiskTier
     prof = model.ModelProfile(name="p", kv_bytes_per_token=float(kvb),

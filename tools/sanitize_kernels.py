@@ -1,0 +1,135 @@
+"""Small launches of every libaskv kernel family for compute-sanitizer.
+
+    compute-sanitizer --tool racecheck python tools/sanitize_kernels.py [--only attn]
+
+K3 instances covered: split (one query tile, both softmax groups on one
+tile set), paired (two query tiles per CTA), GQA-packed, split-KV (combine
+kernel), masked diagonal tiles; K2 reembed (contiguous and block-table
+sources), rope_new (with and without the pre-RoPE save copy).  Sizes are tiny
+so racecheck / synccheck (which serialise and instrument every shared-memory
+access) finish in minutes.  Outputs are checked for NaN only; numerics are the
+parity tests' job.
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+
+def attn_cases():
+    from paper_2403_19708_b200 import ops
+    d = 128
+    # (kept, new, hq, hkv, splits, pair)
+    cases = [(300, 100, 2, 2, 1, "0"),      # split mode: one query tile, 4 KV tiles
+             (200, 300, 2, 2, 1, "1"),      # paired mode: two query tiles per CTA
+             (256, 64, 8, 1, 1, "0"),       # GQA packing (8 q-heads per kv head)
+             (1000, 60, 2, 2, 3, "0"),      # split-KV + combine
+             (0, 130, 1, 1, 1, "1")]        # no cache, paired with a 2-row tail
+    for kept, n, hq, hkv, s, pair in cases:
+        os.environ["ASKV_ATTN_PAIR"] = pair
+        q = torch.randn(n, hq, d, device="cuda").to(torch.bfloat16)
+        kv = torch.randn(kept + n, 2, hkv, d, device="cuda").to(torch.bfloat16)
+        o = torch.empty(n, hq, d, device="cuda", dtype=torch.bfloat16)
+        ws = torch.empty(max(1, ops.attn_workspace_bytes(kept, n, hq, d, s)),
+                         dtype=torch.uint8, device="cuda")
+        ops.prefill_attn(q, kv, kept, n, hq, hkv, d, o, ws, num_splits=s)
+        torch.cuda.synchronize()
+        assert torch.isfinite(o.float()).all(), (kept, n, hq, hkv, s)
+        print(f"attn kept={kept} n={n} hq={hq} hkv={hkv} splits={s} pair={pair} ok",
+              flush=True)
+
+
+def rope_cases():
+    from paper_2403_19708_b200 import ops
+    hkv, d, bt = 2, 128, 16
+    row = 2 * hkv * d
+    table = ops.rope_table(4096, d)
+    kept = 70
+    src = torch.randn(kept + 10, row, device="cuda").to(torch.bfloat16)
+    dst = torch.empty(kept, row, device="cuda", dtype=torch.bfloat16)
+    ops.reembed(src, kept, hkv, d, table, dst, first_token=3)
+    # block-table source: 6 blocks of bt rows scattered in an arena
+    arena = torch.randn(16 * bt, row, device="cuda").to(torch.bfloat16)
+    bids = torch.tensor([5, 2, 9, 0, 14, 7], device="cuda", dtype=torch.int64)
+    ops.reembed(arena, kept, hkv, d, table, dst, block_off=bids * bt * row, block_tokens=bt)
+    n, hq = 33, 4
+    qkv = torch.randn(n, (hq + 2 * hkv) * d, device="cuda").to(torch.bfloat16)
+    q_out = torch.empty(n, hq * d, device="cuda", dtype=torch.bfloat16)
+    kv_out = torch.empty(n, row, device="cuda", dtype=torch.bfloat16)
+    save = torch.empty(n, row, device="cuda", dtype=torch.bfloat16)
+    ops.rope_new(qkv, n, hq, hkv, d, table, kept, q_out, kv_out, save)
+    ops.rope_new(qkv, n, hq, hkv, d, table, kept, q_out, kv_out, None)
+    torch.cuda.synchronize()
+    print("rope/reembed ok", flush=True)
+
+
+def provenance_cases():
+    """The round-1 initcheck reports (rope_new<64> / reembed<64> reading
+    "uninitialized" rows inside the layer loop) came from inputs written by
+    engines the tool may not track: a cuBLASLt GEMM output (TMA stores) feeding
+    rope_new, and a read-buffer slot written by cudaMemcpyBatchAsync (the
+    pre-loader) feeding K2.  Reproduce each provenance in isolation: the same
+    kernels on SM-written inputs report nothing (rope_cases)."""
+    import torch.nn.functional as F
+    from paper_2403_19708_b200 import ops
+    from paper_2403_19708_b200.store import HostArena
+    hq, hkv, d, n = 4, 4, 64, 24
+    table = ops.rope_table(4096, d)
+    x = torch.randn(n, 256, device="cuda").to(torch.bfloat16)
+    w = torch.randn((hq + 2 * hkv) * d, 256, device="cuda").to(torch.bfloat16)
+    qkv = F.linear(x, w)                       # cuBLASLt (TMA-store epilogue)
+    q_out = torch.empty(n, hq * d, device="cuda", dtype=torch.bfloat16)
+    kv_out = torch.empty(n, 2 * hkv * d, device="cuda", dtype=torch.bfloat16)
+    ops.rope_new(qkv, n, hq, hkv, d, table, 0, q_out, kv_out, None)
+    torch.cuda.synchronize()
+    print("provenance: gemm -> rope_new done", flush=True)
+    row = 2 * hkv * d
+    bt, layers = 16, 2
+    block_bytes = layers * bt * row * 2
+    arena = HostArena(4, block_bytes, pin=True)
+    arena.buffer.view(torch.bfloat16).normal_()
+    slot = torch.empty(4 * bt, row, device="cuda", dtype=torch.bfloat16)
+    kept = 40
+    ops.preload_layer(slot, arena.buffer, [2, 0, 3], block_bytes, 0, bt * row * 2,
+                      (kept - 2 * bt) * row * 2)      # cudaMemcpyBatchAsync
+    dst = torch.empty(kept, row, device="cuda", dtype=torch.bfloat16)
+    ops.reembed(slot, kept, hkv, d, table, dst)
+    torch.cuda.synchronize()
+    print("provenance: memcpy batch -> reembed done", flush=True)
+
+
+def engine_turns(graph: bool):
+    """Two turns of the tiny model through the native layer loop (a miss, then
+    a reuse hit with pre-load + K2 + K3 + save), issued as a CUDA graph or on
+    the stream: isolates whether initcheck's reports depend on graph issue."""
+    from paper_2403_19708_b200 import engine, model
+    shape = model.shape("tiny")
+    eng = engine.Engine(shape, host_blocks=32, block_tokens=16, seed=0, max_new=64,
+                        read_buffer_bytes=32 << 20, autotune=False)
+    eng.runner.graph = graph
+    g = torch.Generator().manual_seed(0)
+    eng.turn("s", 0, torch.randint(0, shape.vocab, (24,), generator=g),
+             torch.randint(0, shape.vocab, (8,), generator=g))
+    eng.turn("s", 1, torch.randint(0, shape.vocab, (24,), generator=g))
+    torch.cuda.synchronize()
+    print(f"engine turns graph={graph} done", flush=True)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="", choices=["", "attn", "rope", "provenance", "engine_graph",
+                                                   "engine_stream"])
+    a = ap.parse_args()
+    from paper_2403_19708_b200 import build
+    build.build()
+    if a.only in ("", "attn"):
+        attn_cases()
+    if a.only in ("", "rope"):
+        rope_cases()
+    if a.only == "provenance":
+        provenance_cases()
+    if a.only.startswith("engine_"):
+        engine_turns(a.only == "engine_graph")
