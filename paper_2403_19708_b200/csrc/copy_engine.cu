@@ -2,11 +2,13 @@
 // the host link), plus the ABI bookkeeping (version, last error).
 //
 // Each call turns one (session, layer) into a list of contiguous
-// pinned-host <-> HBM segments and issues them as ONE cudaMemcpyBatchAsync on
-// the caller's dedicated copy stream (one DMA descriptor list instead of one
-// runtime call per block), then records the caller's event so the compute
-// stream can wait on exactly that layer (overlap.py:69-123 / :126-200 model
-// this schedule analytically; here it is real).
+// pinned-host <-> HBM segments and issues them on the caller's dedicated copy
+// stream: a run of consecutive arena blocks (same stride on both sides) is
+// ONE strided cudaMemcpy2DAsync, an isolated segment one cudaMemcpyAsync, so a
+// (session, layer) costs a handful of runtime calls, not one per block.  The
+// caller's event is then recorded so the compute stream can wait on exactly
+// that layer (overlap.py:69-123 / :126-200 model this schedule analytically;
+// here it is real).
 #include <cuda_runtime.h>
 
 #include <cstdarg>
@@ -37,47 +39,65 @@ void clear_error() { g_last_error.clear(); }
 
 namespace {
 
-// cudaMemcpyFlagPreferOverlapWithCompute is a tuning knob (ASKV_COPY_OVERLAP=1);
-// default 0 keeps the DMAs on the copy engines.
-unsigned copy_flags() {
+// ASKV_COPY_2D=0 disables the strided (2-D) form: every segment is its own
+// cudaMemcpyAsync (an A/B knob for the DMA efficiency of short chunks).
+bool use_2d() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("ASKV_COPY_OVERLAP");
-    v = (e && e[0] == '1') ? 1 : 0;
+    const char* e = getenv("ASKV_COPY_2D");
+    v = (e && e[0] == '0') ? 0 : 1;
   }
-  return v ? (unsigned)cudaMemcpyFlagPreferOverlapWithCompute : 0u;
+  return v == 1;
 }
 
-// Issue a list of same-direction copies in stream order.
-// Pointers are UVA-classified (cudaMemcpyDefault), so the same entry points
-// serve a pinned-host arena (H2D / D2H over the host link) and an
-// HBM-resident arena (D2D).
-int issue_batch(std::vector<void*>& dsts, std::vector<void*>& srcs, std::vector<size_t>& sizes,
-                cudaStream_t stream) {
-  if (dsts.empty()) return ASKV_OK;
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(stream, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone) {
-    // inside a graph capture (the layer loop's HBM-tier copies): one memcpy
-    // node per segment; the batch API is not capturable
-    for (size_t i = 0; i < dsts.size(); ++i) {
-      cudaError_t e = cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDefault, stream);
-      if (e != cudaSuccess) return cuda_status(e, "cudaMemcpyAsync (captured)");
+// One copy segment: `rows` equal pieces of `width` bytes, piece i at
+// dst + i*dpitch / src + i*spitch (rows == 1: a plain contiguous copy).
+struct Seg {
+  char* dst;
+  const char* src;
+  size_t width, rows, dpitch, spitch;
+};
+
+// Append a contiguous piece, merging it into the previous segment when it
+// continues it (contiguous on both sides, or one more row of the same stride).
+void push_piece(std::vector<Seg>& v, char* d, const char* s, size_t n) {
+  if (!v.empty()) {
+    Seg& p = v.back();
+    if (p.rows == 1 && p.dst + p.width == d && p.src + p.width == s) {
+      p.width += n;  // contiguous continuation
+      return;
     }
-    return ASKV_OK;
+    if (use_2d() && n == p.width) {
+      const char* plast_s = p.src + (p.rows - 1) * p.spitch;
+      char* plast_d = p.dst + (p.rows - 1) * p.dpitch;
+      if (p.rows == 1 && d > p.dst && s > p.src) {
+        p.dpitch = (size_t)(d - p.dst);
+        p.spitch = (size_t)(s - p.src);
+        p.rows = 2;
+        return;
+      }
+      if (p.rows > 1 && d == plast_d + p.dpitch && s == plast_s + p.spitch) {
+        ++p.rows;
+        return;
+      }
+    }
   }
-  cudaMemcpyAttributes attr = {};
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.flags = copy_flags();
-  size_t attr_idx = 0;
-  size_t fail_idx = 0;
-  cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(),
-                                       &attr, &attr_idx, 1, &fail_idx, stream);
-  if (e == cudaSuccess) return ASKV_OK;
-  // Batch API unavailable (older driver): same segments, one call each.
-  (void)cudaGetLastError();
-  for (size_t i = 0; i < dsts.size(); ++i) {
-    e = cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDefault, stream);
-    if (e != cudaSuccess) return cuda_status(e, "cudaMemcpyAsync");
+  v.push_back(Seg{d, s, n, 1, n, n});
+}
+
+// Issue the segments in stream order.  Pointers are UVA-classified
+// (cudaMemcpyDefault), so the same entry points serve a pinned-host arena
+// (H2D / D2H over the host link) and an HBM-resident arena (D2D); inside a
+// graph capture (the layer loop's HBM-tier copies) each becomes a memcpy node.
+int issue(const std::vector<Seg>& v, cudaStream_t stream) {
+  for (const Seg& g : v) {
+    cudaError_t e;
+    if (g.rows == 1)
+      e = cudaMemcpyAsync(g.dst, g.src, g.width, cudaMemcpyDefault, stream);
+    else
+      e = cudaMemcpy2DAsync(g.dst, g.dpitch, g.src, g.spitch, g.width, g.rows,
+                            cudaMemcpyDefault, stream);
+    if (e != cudaSuccess) return cuda_status(e, g.rows == 1 ? "cudaMemcpyAsync" : "cudaMemcpy2DAsync");
   }
   return ASKV_OK;
 }
@@ -124,17 +144,16 @@ extern "C" int askv_preload_layer(void* dst, const void* host_base, const int64_
   ASKV_REQUIRE(layer_off + chunk_bytes <= block_bytes, "preload: layer chunk outside block");
   ASKV_REQUIRE(tail_bytes >= 0 && tail_bytes <= chunk_bytes, "preload: bad tail_bytes");
   ASKV_REQUIRE(nblocks == 0 || (dst && host_base && block_ids), "preload: null pointer");
-  std::vector<void*> d(nblocks), s(nblocks);
-  std::vector<size_t> n(nblocks);
+  std::vector<Seg> segs;
+  segs.reserve(4);
   auto* hb = static_cast<const char*>(host_base);
   auto* db = static_cast<char*>(dst);
   for (int i = 0; i < nblocks; ++i) {
     ASKV_REQUIRE(block_ids[i] >= 0, "preload: negative block id");
-    d[i] = db + (int64_t)i * chunk_bytes;
-    s[i] = const_cast<char*>(hb + block_ids[i] * block_bytes + layer_off);
-    n[i] = (size_t)((i == nblocks - 1 && tail_bytes > 0) ? tail_bytes : chunk_bytes);
+    push_piece(segs, db + (int64_t)i * chunk_bytes, hb + block_ids[i] * block_bytes + layer_off,
+               (size_t)((i == nblocks - 1 && tail_bytes > 0) ? tail_bytes : chunk_bytes));
   }
-  int rc = issue_batch(d, s, n, (cudaStream_t)stream);
+  int rc = issue(segs, (cudaStream_t)stream);
   if (rc) return rc;
   if (done_event)
     return cuda_status(cudaEventRecord((cudaEvent_t)done_event, (cudaStream_t)stream),
@@ -157,8 +176,7 @@ extern "C" int askv_save_layer(void* host_base, const int64_t* block_ids, int nb
                "save: tokens [%lld,%lld) need more than %d blocks", (long long)first_token,
                (long long)last, nblocks);
   ASKV_REQUIRE(n_tokens == 0 || (host_base && block_ids && src), "save: null pointer");
-  std::vector<void*> d, s;
-  std::vector<size_t> n;
+  std::vector<Seg> segs;
   auto* hb = static_cast<char*>(host_base);
   auto* sb = static_cast<const char*>(src);
   int64_t t = first_token;
@@ -168,12 +186,11 @@ extern "C" int askv_save_layer(void* host_base, const int64_t* block_ids, int nb
     int64_t cnt = block_tokens - r;
     if (cnt > last - t) cnt = last - t;
     ASKV_REQUIRE(block_ids[b] >= 0, "save: negative block id");
-    d.push_back(hb + block_ids[b] * block_bytes + layer_off + r * row_bytes);
-    s.push_back(const_cast<char*>(sb + (t - first_token) * row_bytes));
-    n.push_back((size_t)(cnt * row_bytes));
+    push_piece(segs, hb + block_ids[b] * block_bytes + layer_off + r * row_bytes,
+               sb + (t - first_token) * row_bytes, (size_t)(cnt * row_bytes));
     t += cnt;
   }
-  int rc = issue_batch(d, s, n, (cudaStream_t)stream);
+  int rc = issue(segs, (cudaStream_t)stream);
   if (rc) return rc;
   if (done_event)
     return cuda_status(cudaEventRecord((cudaEvent_t)done_event, (cudaStream_t)stream),

@@ -23,6 +23,7 @@ from dataclasses import dataclass, field
 import torch
 
 from .model import LlamaShape, TierConfig, profile_for
+from .policy import JobQueue, PolicyConfig, make_room, plan_prefetch
 from .runner import Job, JobResult, LlamaWeights, ResidentKv, Runner
 from .store import CapacityError, HitClass, HostArena, KvStore, Tier
 
@@ -174,17 +175,28 @@ class Engine:
                  read_buffer_bytes: int = 1 << 30, max_new: int = 1024,
                  truncation_ratio: float = 0.5, ttl: float = math.inf, pin: bool = True,
                  tp_reduce=None, hbm_blocks: int = 0, disk_dir: str | None = None,
-                 disk_blocks: int = 0, autotune: bool | int = True):
+                 disk_blocks: int = 0, autotune: bool | int = True,
+                 policy: PolicyConfig | None = None, dram_bytes: int | None = None,
+                 numa_node: int | None = None):
         self.shape = shape
+        # placement policy (policy.py:92-204): the reference's scheduler-aware
+        # ranking over `queue` (the serving loop's JobQueue when one drives this
+        # engine, sim.Server; empty otherwise = coldest first)
+        self.policy = policy if policy is not None else PolicyConfig()
+        self.queue = JobQueue()
         self.profile = profile_for(shape, truncation_ratio=truncation_ratio)
         self.block_tokens = block_tokens
         block_bytes = block_tokens * shape.kv_bytes_per_token
-        self.arena = HostArena(host_blocks, block_bytes, pin=pin)
+        self.arena = HostArena(host_blocks, block_bytes, pin=pin, numa_node=numa_node)
         disk = None
         if disk_dir is not None and disk_blocks > 0:
             from .disk import DiskTier
             disk = DiskTier(disk_dir, block_bytes)
-        tiers = TierConfig(dram_capacity=host_blocks * block_bytes,
+        # accounting capacity: the arena, or less (`dram_bytes`) so the
+        # physical spare covers the rows of the jobs in flight
+        dram = host_blocks * block_bytes if dram_bytes is None else min(
+            int(dram_bytes), host_blocks * block_bytes)
+        tiers = TierConfig(dram_capacity=dram,
                            disk_capacity=disk_blocks * block_bytes if disk else 0)
         self.store = KvStore(self.profile, tiers, block_bytes=block_bytes, ttl=ttl,
                              evictor=self._make_room, arena=self.arena,
@@ -208,37 +220,23 @@ class Engine:
                              autotune=(self.window + self.chunk + max_new
                                        if autotune is True else autotune))
         self.store.io_fence = self.runner.fence
+        if self.hbm is not None:
+            # any physical release / demotion of a session's host rows ends
+            # its HBM mirror (the mirror is only valid against those rows)
+            self.store.on_release = self.hbm.drop
         self.context: dict[str, int] = {}
         self.tokens: dict[str, torch.Tensor] = {}   # conversation token ids (for misses)
 
     def _make_room(self, needed: float) -> None:
-        """Free DRAM by least-recently-used unpinned sessions: demoted to the
-        disk tier when there is one (making disk room by evicting its LRU items
-        out), else evicted out (sim.py:300-327 with the LRU baseline policy)."""
-        freed = 0.0
-        # sessions prefetched for upcoming jobs go last (scheduler-aware eviction,
-        # policy.py select_evict_to_disk avoids the queue window)
-        order = sorted(self.store.memory_items(),
-                       key=lambda i: (i.session_id in self.prefetched, i.last_access, i.seq))
-        for it in order:
-            if freed >= needed:
-                break
-            sid = it.session_id
-            if sid in self.store.pinned:
-                continue
-            blocks = self.store.charge(it.bytes)
-            freed += blocks
-            if self.hbm is not None:
-                self.hbm.drop(sid)
-            if self.store.disk is not None and blocks <= self.store.disk_capacity:
-                for old in sorted(self.store.disk_items(), key=lambda i: (i.last_access, i.seq)):
-                    if self.store.disk_free >= blocks:
-                        break
-                    self.store.remove(old.session_id)
-                self.store.move(sid, Tier.DISK)
+        """Free DRAM with the reference's placement policy (sim.py:298-327 via
+        policy.make_room): victims ranked by the scheduler-aware key over
+        `self.queue` (policy.py:159-172), demoted to the disk tier when there is
+        one (dropping disk victims while it is full), else evicted out."""
+        def count(action, sid, nbytes, counted):
+            if action == "evict_to_disk":
                 self.disk_evictions += 1
-            else:
-                self.store.remove(sid)
+
+        make_room(self.store, self.queue, self.policy, needed, on_evict=count)
 
     def _ensure_arena(self, sid: str, rows: int) -> None:
         """Physical room for the session's rows before the saver writes them
@@ -247,7 +245,9 @@ class Engine:
         need = -(-(st.head_row(sid) + rows) // self.block_tokens) - len(st.tables.get(sid, ()))
         while st.arena.free_blocks < need:
             before = st.arena.free_blocks
-            self._make_room((need - before) * st.block_bytes)
+            # the store's evictor: this engine's policy, or the serving loop's
+            # when one drives the engine (sim.Server installs its own)
+            (st.evictor or self._make_room)((need - before) * st.block_bytes)
             if st.arena.free_blocks == before:
                 raise CapacityError(f"host arena full: {need} blocks for {sid}")
 
@@ -276,14 +276,17 @@ class Engine:
         blocks = self.store.charge(it.bytes)
         target = blocks + self.store.mem_buffer_reserve
         if self.store.mem_free < target:
-            self._make_room(target - self.store.mem_free)
+            (self.store.evictor or self._make_room)(target - self.store.mem_free)
         self.store.move(sid, Tier.MEMORY, wait=wait)
         self.disk_promotions += 1
 
-    def prefetch(self, sids) -> list[str]:
+    def prefetch(self, sids=None) -> list[str]:
         """Scheduler-aware prefetch (policy.py:122-150, sim.py:329-366): start
         disk -> DRAM reads for the sessions of upcoming jobs; the reads run on
-        the disk IO threads while the current prefill proceeds."""
+        the disk IO threads while the current prefill proceeds.  `sids` None =
+        the reference's pick over `self.queue` (plan_prefetch)."""
+        if sids is None:
+            sids = plan_prefetch(self.queue, self.store, self.policy, exclude=self.prefetched)
         started = []
         for sid in sids:
             it = self.store.peek(sid)
@@ -327,7 +330,7 @@ class Engine:
         return res
 
     def _prefill(self, sid: str, ids: torch.Tensor, kept: int, want_logits: bool,
-                 kv_cache: ResidentKv | None = None):
+                 kv_cache: ResidentKv | None = None, prestage_layers: int = 0):
         """Chunked prefill of `ids` after `kept` stored rows, saving every chunk's
         K/V; rolling window truncation before a chunk that would overflow.
         With `kv_cache` the last chunk leaves every layer's rotated rows resident
@@ -337,6 +340,8 @@ class Engine:
         pos, n = 0, int(ids.numel())
         while pos < n:
             c = min(self.chunk, n - pos)
+            if kept + n - pos <= self.window and n - pos <= self.runner.max_new:
+                c = n - pos   # no overflow possible: one job (same rows as chunking)
             if kept + c > self.window:
                 k2 = overflow_kept(kept, c, self.window, self.cut)
                 self.store.drop_front_rows(sid, kept - k2)
@@ -347,7 +352,8 @@ class Engine:
             self._ensure_arena(sid, kept + c)
             tab = self.store.reserve_rows(sid, kept + c)
             job = Job(sid, ids[pos:pos + c], kept=kept, source="host" if kept else "none",
-                      block_ids=tab, save=True, head=self.store.head_row(sid))
+                      block_ids=tab, save=True, head=self.store.head_row(sid),
+                      prestage_layers=prestage_layers if pos == 0 else 0)
             if kv_cache is not None and pos + c == n:
                 job.kv_cache = kv_cache
                 if kept and kv_cache.rows == kept:

@@ -1,0 +1,81 @@
+"""Host memory on a chosen NUMA node (one process per GPU,
+each with its pinned KV arena on its own GPU's NUMA node, so the pre-loader's
+H2D DMAs never cross the socket interconnect).
+
+The arena is an anonymous mapping bound to the node with mbind(MPOL_BIND)
+before any page is touched; page-locking it with cudaHostRegister then
+faults every page in on that node and makes it DMA-able like cudaHostAlloc
+memory.  No libnuma is needed (raw syscall through libc)."""
+
+from __future__ import annotations
+
+import ctypes
+import mmap
+import os
+import platform
+
+_MPOL_BIND = 2
+_MPOL_MF_STRICT = 1
+_SYS_MBIND = {"x86_64": 237, "aarch64": 235}
+
+
+def node_count() -> int:
+    try:
+        return sum(1 for d in os.listdir("/sys/devices/system/node")
+                   if d.startswith("node") and d[4:].isdigit())
+    except OSError:
+        return 1
+
+
+def gpu_numa_node(device_index: int) -> int | None:
+    """NUMA node of a CUDA device from its PCI address (sysfs), None if the
+    platform does not report one (single-node hosts report -1)."""
+    import torch
+
+    p = torch.cuda.get_device_properties(device_index)
+    bus = "%04x:%02x:%02x.0" % (getattr(p, "pci_domain_id", 0), p.pci_bus_id, p.pci_device_id)
+    try:
+        with open(f"/sys/bus/pci/devices/{bus}/numa_node") as f:
+            node = int(f.read().strip())
+    except (OSError, ValueError):
+        return None
+    return node if node >= 0 else None
+
+
+def _mbind(addr: int, length: int, node: int) -> None:
+    nr = _SYS_MBIND.get(platform.machine())
+    if nr is None:
+        raise OSError(f"mbind: unsupported machine {platform.machine()}")
+    maxnode = max(64, node + 1)
+    mask = (ctypes.c_ulong * (maxnode // 64 + 1))()
+    mask[node // 64] = 1 << (node % 64)
+    libc = ctypes.CDLL(None, use_errno=True)
+    libc.syscall.restype = ctypes.c_long
+    rc = libc.syscall(ctypes.c_long(nr), ctypes.c_void_p(addr), ctypes.c_ulong(length),
+                      ctypes.c_int(_MPOL_BIND), mask, ctypes.c_ulong(maxnode + 1),
+                      ctypes.c_uint(_MPOL_MF_STRICT))
+    if rc != 0:
+        e = ctypes.get_errno()
+        raise OSError(e, f"mbind(node {node}): {os.strerror(e)}")
+
+
+def host_buffer(nbytes: int, node: int, *, pin: bool = True):
+    """(uint8 tensor of `nbytes` on NUMA node `node`, node).  pin=True
+    page-locks and registers it with CUDA (cudaHostRegister)."""
+    import torch
+
+    if node < 0 or node >= max(1, node_count()):
+        raise ValueError(f"no NUMA node {node} (host has {node_count()})")
+    mm = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+    addr = ctypes.addressof(ctypes.c_char.from_buffer(mm))
+    _mbind(addr, nbytes, node)
+    buf = torch.frombuffer(mm, dtype=torch.uint8)
+    if pin:
+        rt = torch.cuda.cudart()
+        err = rt.cudaHostRegister(addr, nbytes, 0)
+        if int(err) != 0:
+            raise RuntimeError(f"cudaHostRegister of {nbytes} B failed: {err}")
+        buf._askv_registered = (addr, mm)   # keep the mapping alive with the tensor
+    else:
+        buf._askv_registered = (None, mm)
+    return buf, node

@@ -63,3 +63,51 @@ class Timeline:
 
 def ms_to_s(x: float) -> float:
     return x * 1e-3
+
+
+# ---------------------------------------------------------------------------
+# The reference's planner entry points, measured.
+# overlap.py:69-72 / :126-128 signatures; bind() a measured.MeasuredExecutor
+# (an engine on this process's GPU) first -- there is no analytical fallback.
+
+_executor = None
+
+
+def bind(executor) -> None:
+    """Route plan_preload / plan_async_save to `executor`
+    (measured.MeasuredExecutor); None unbinds."""
+    global _executor
+    _executor = executor
+
+
+def _bound():
+    if _executor is None:
+        raise RuntimeError("overlap: no engine bound; call overlap.bind("
+                           "measured.MeasuredExecutor(engine)) first")
+    return _executor
+
+
+def plan_preload(hist_tokens: int, new_tokens: int, profile, tiers, read_buffer: float,
+                 prev_job_running: bool = True, *, bandwidth: float | None = None,
+                 job=None) -> Timeline:
+    """Run one job's layer-wise pre-load + prefill on the GPU and return its
+    measured Timeline (overlap.py:69-123 plans it analytically).  Same
+    argument checks as the reference (overlap.py:79-82)."""
+    if hist_tokens < 0 or new_tokens < 0:
+        raise ValueError("token counts must be >= 0")
+    if read_buffer < 0:
+        raise ValueError("read_buffer must be >= 0")
+    return _bound().plan_preload(hist_tokens, new_tokens, profile, tiers, read_buffer,
+                                 prev_job_running, bandwidth=bandwidth, job=job)
+
+
+def plan_async_save(prompt_tokens: int, decode_steps: int, profile, tiers,
+                    write_buffer: float, *, bandwidth: float | None = None,
+                    job=None) -> Timeline:
+    """Measured write-back Timeline of a job (overlap.py:126-200)."""
+    if prompt_tokens < 0 or decode_steps < 0:
+        raise ValueError("token counts must be >= 0")
+    if write_buffer < 0:
+        raise ValueError("write_buffer must be >= 0")
+    return _bound().plan_async_save(prompt_tokens, decode_steps, profile, tiers, write_buffer,
+                                    bandwidth=bandwidth, job=job)

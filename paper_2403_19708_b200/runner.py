@@ -142,6 +142,10 @@ class Job:
     # last saves (write-through on the save stream) must land first
     fence_sessions: set = field(default_factory=set)
     prestage: bool = False  # start the job only once all its layers are pre-loaded
+    # read-buffer head start (overlap.py:91-93, sim.py:439): start the job once
+    # its first `prestage_layers` layers are pre-loaded (the bytes the loader
+    # moved while the job waited in the queue); 0 = none, >= layers = all
+    prestage_layers: int = 0
     # resident rotated KV (decode): the job writes all its
     # layers' rows into kv_cache; source "resident" = kept rows already there
     kv_cache: "ResidentKv | None" = None
@@ -236,7 +240,7 @@ def _ptr_array(items) -> "C.Array":
 
 class _IOThread(threading.Thread):
     """Submits copy-engine work (pre-load / save DMA batches) from its own host
-    thread, FIFO.  A multi-GB pre-load queue can block cudaMemcpyBatchAsync on
+    thread, FIFO.  A multi-GB pre-load queue can block the copy calls on
     stream back-pressure; on the compute thread that would starve kernel
     issue (the paper's system likewise uses dedicated IO threads)."""
 
@@ -660,8 +664,9 @@ class Runner:
             units = None
             if kept and job.source == "host":
                 units = [self._acquire(jid, l) for l in range(L)]
-                if job.prestage:   # start only once the whole job is resident
-                    self._slot_ready[units[-1].slot].wait(cs)
+                k = L if job.prestage else min(L, max(0, int(job.prestage_layers)))
+                if k:   # head start: layers 0..k-1 resident before the job begins
+                    self._slot_ready[units[k - 1].slot].wait(cs)
             t0 = lease.get() if lease else None
             if t0:   # one timing event: the base of the copy streams' intervals
                 _lib.check(_lib.lib().askv_stamp(self._stamp_ptr(st_off, 0), cs.cuda_stream),

@@ -4,7 +4,7 @@
 //   tools/link_probe
 //
 // Cases: one H2D stream issuing 2.6 MB chunks (a (block, layer) chunk of a
-// 13B session) as cudaMemcpyAsync or batched; 2 / 4 concurrent H2D streams;
+// 13B session) as cudaMemcpyAsync or strided 2-D copies; 2 / 4 concurrent H2D streams;
 // H2D with a concurrent D2H stream; 64 MB chunks.  Diagnostics only.
 #include <cuda_runtime.h>
 
@@ -50,14 +50,13 @@ int main() {
           sz.push_back(chunk);
         }
         if (batch) {
-          // 23-chunk batches = one (session, layer) pre-load
+          // strided 2-D copies of 23 chunks = one (session, layer) pre-load
+          // of consecutive arena blocks (the pre-loader's strided form)
           for (size_t i = 0; i < ds.size(); i += 23) {
             const size_t m = ds.size() - i < 23 ? ds.size() - i : 23;
-            cudaMemcpyAttributes attr = {};
-            attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-            size_t ai = 0, fail = 0;
-            CK(cudaMemcpyBatchAsync(ds.data() + i, ss.data() + i, sz.data() + i, m, &attr, &ai, 1,
-                                    &fail, st[k]));
+            const size_t sp = m > 1 ? (size_t)((char*)ss[i + 1] - (char*)ss[i]) : chunk;
+            const size_t dp = m > 1 ? (size_t)((char*)ds[i + 1] - (char*)ds[i]) : chunk;
+            CK(cudaMemcpy2DAsync(ds[i], dp, ss[i], sp, chunk, m, cudaMemcpyHostToDevice, st[k]));
           }
         } else {
           for (size_t i = 0; i < ds.size(); ++i)
@@ -80,12 +79,12 @@ int main() {
     return 0;
   };
   if (run("1 stream, 2.6 MB memcpy", 1, 2621440, false, false)) return 1;
-  if (run("1 stream, 2.6 MB x23 batches", 1, 2621440, true, false)) return 1;
-  if (run("2 streams, 2.6 MB x23 batches", 2, 2621440, true, false)) return 1;
-  if (run("4 streams, 2.6 MB x23 batches", 4, 2621440, true, false)) return 1;
+  if (run("1 stream, 2.6 MB x23 2-D", 1, 2621440, true, false)) return 1;
+  if (run("2 streams, 2.6 MB x23 2-D", 2, 2621440, true, false)) return 1;
+  if (run("4 streams, 2.6 MB x23 2-D", 4, 2621440, true, false)) return 1;
   if (run("1 stream, 64 MB memcpy", 1, 64 << 20, false, false)) return 1;
-  if (run("1 stream, 2.6 MB x23 batches + 2 GB D2H", 1, 2621440, true, true)) return 1;
-  if (run("2 streams, 2.6 MB x23 batches + 2 GB D2H", 2, 2621440, true, true)) return 1;
+  if (run("1 stream, 2.6 MB x23 2-D + 2 GB D2H", 1, 2621440, true, true)) return 1;
+  if (run("2 streams, 2.6 MB x23 2-D + 2 GB D2H", 2, 2621440, true, true)) return 1;
   // D2H alone
   {
     CK(cudaDeviceSynchronize());

@@ -70,8 +70,8 @@ def provenance_cases():
     """The round-1 initcheck reports (rope_new<64> / reembed<64> reading
     "uninitialized" rows inside the layer loop) came from inputs written by
     engines the tool may not track: a cuBLASLt GEMM output (TMA stores) feeding
-    rope_new, and a read-buffer slot written by cudaMemcpyBatchAsync (the
-    pre-loader) feeding K2.  Reproduce each provenance in isolation: the same
+    rope_new, and a read-buffer slot written by the copy engines (the
+    pre-loader's DMAs) feeding K2.  Reproduce each provenance in isolation: the same
     kernels on SM-written inputs report nothing (rope_cases)."""
     import torch.nn.functional as F
     from paper_2403_19708_b200 import ops
@@ -94,7 +94,7 @@ def provenance_cases():
     slot = torch.empty(4 * bt, row, device="cuda", dtype=torch.bfloat16)
     kept = 40
     ops.preload_layer(slot, arena.buffer, [2, 0, 3], block_bytes, 0, bt * row * 2,
-                      (kept - 2 * bt) * row * 2)      # cudaMemcpyBatchAsync
+                      (kept - 2 * bt) * row * 2)      # copy-engine DMA (K1)
     dst = torch.empty(kept, row, device="cuda", dtype=torch.bfloat16)
     ops.reembed(slot, kept, hkv, d, table, dst)
     torch.cuda.synchronize()
