@@ -29,6 +29,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import platform
 import os
 import statistics
 import subprocess
@@ -59,6 +60,11 @@ def parse():
     ap.add_argument("--turns", type=int, default=16, help="hit turns per GPU per step")
     ap.add_argument("--block-tokens", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fragmented", action="store_true",
+                    help="scatter every turn's blocks over the arena (random permutation) "
+                         "instead of the allocator's contiguous runs")
+    ap.add_argument("--serve-dram-gb", type=float, default=96.0,
+                    help="host DRAM of the measured serving replay (0 = skip it)")
     ap.add_argument("--disk-dir", default="/tmp",
                     help="directory for the disk-tier probe ('none' = skip)")
     ap.add_argument("--decode-steps", type=int, default=32,
@@ -234,7 +240,7 @@ def cpu_reference(turns, shape, pairs_per_turn: int, seed: int = 0):
             "wall_seconds": wall, "tasks": len(tasks)}
 
 
-def run_reference(args, shape, turns):
+def run_reference(args, shape, turns, config):
     """--impl reference: the reference's CPU implementation of the path (oracle
     port of kvsim.rope.attention_with_decoupled_cache), all host cores."""
     pairs = 4
@@ -253,12 +259,164 @@ def run_reference(args, shape, turns):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {shape.name}-shaped hit turns "
-                                   f"(reference CPU path)", "turns_per_gpu": len(turns)},
+            "config": config,
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": vals[0]["cores"],
                              "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+
+
+def make_config(args, shape, turns, n_hits, world, tp, rank_probe) -> dict:
+    """The workload description both arms print (ours and --impl reference)."""
+    from paper_2403_19708_b200.metrics import percentile
+
+    kept_l = [kept for *_, kept, _ in turns]
+    new_l = [new for *_, new in turns]
+    kv_bytes = sum(kept_l) * shape.kv_bytes_per_token
+    return {
+        "workload": (f"{args.config}: {shape.name}-shaped, reference generate_poisson "
+                     f"sessions sharded by crc32(session) over {world} GPU(s); "
+                     f"{len(turns)} hit turns/GPU/step (of {n_hits} in shard)"
+                     if args.config != "c4" else
+                     f"c4: {shape.name}-shaped, W=4096, 32768-token stored histories "
+                     f"truncated by the reference rules to kept 2048..3648 (block-table "
+                     f"edit; only the kept blocks are materialised and loaded), 256 new "
+                     f"tokens per turn, {len(turns)} turns/GPU/step"),
+        "turns_per_gpu": len(turns), "kept_p50": percentile(kept_l, 0.5),
+        "new_p50": percentile(new_l, 0.5), "block_tokens": args.block_tokens,
+        "value_mode": "KV resident in an HBM arena (no host link)",
+        "e2e_mode": "KV streamed from pinned host DRAM by the layer-wise pre-loader; "
+                    "new-token KV saved back asynchronously",
+        "l2": f"inputs larger than L2 (per-step KV {kv_bytes / 1e9:.1f} GB)",
+        "parallelism": (f"tensor-parallel tp{tp} (NCCL all-reduce of W_o / W_down "
+                        f"partials over NVLink)" if tp > 1 else
+                        f"one rank of a tp{args.tp_rank_of} shard, all-reduce excluded "
+                        f"(per-rank compute probe; outputs are partial sums)"
+                        if rank_probe else
+                        f"sessions sharded, no collective ({world} independent ranks)")}
+
+
+def run_serving(args, rank: int, device: int) -> dict:
+    import gc
+
+    import torch
+
+    from paper_2403_19708_b200 import serve
+    sa = serve.parse(["--config", args.config, "--shard", str(rank), "--of", "8",
+                      "--device", str(device), "--dram-gb", str(args.serve_dram_gb)])
+    t0 = time.perf_counter()
+    out = serve.run(sa)
+    out["wall_s"] = time.perf_counter() - t0
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    if hasattr(torch._C, "_host_emptyCache"):
+        torch._C._host_emptyCache()   # return the serving arena's pinned pages
+    r, c = out["reuse"], out["recompute"]
+    return {"workload": f"{args.config} shard {rank} of 8 ({out['sessions']} sessions, "
+                        f"{out['turns']} turns, arrival order)",
+            "dram_gb": out["dram_bytes"] / 1e9, "read_buffer_gb": out["read_buffer_bytes"] / 1e9,
+            "p50_ttft_s": {"reuse": r["p50_ttft_s"], "recompute": c["p50_ttft_s"]},
+            "p99_ttft_s": {"reuse": r["p99_ttft_s"], "recompute": c["p99_ttft_s"]},
+            "speedup_p50_ttft": out.get("speedup_p50_ttft"),
+            "prefill_tokens_per_s": {"reuse": r["prefill_tokens_per_s"],
+                                     "recompute": c["prefill_tokens_per_s"]},
+            "exposed_transfer_frac": r["exposed_transfer_frac"],
+            "hit_rate": r["overall_hit_rate"], "evict_out": r["evict_out"],
+            "hits_with_head_start": r["hits_with_head_start"], "h2d_gbs": r["h2d_gbs"],
+            "by_hit_class": r["by_hit_class"], "wall_s": out["wall_s"],
+            "note": "queue-inclusive TTFT (sim.py:489) with every prefill measured on this "
+                    "GPU; read-buffer head start min(S_buf, B*wait) from real queue waits; "
+                    "decode modeled at 1 ms/step (reference llama-13b profile)"}
+
+
+def host_info() -> dict:
+    """CPU model and the numpy / BLAS build the CPU path runs on."""
+    model = platform.processor() or ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = ""
+    try:
+        cfg = np.show_config(mode="dicts")
+        b = cfg.get("Build Dependencies", {}).get("blas", {})
+        blas = f"{b.get('name', '')} {b.get('version', '')}".strip()
+    except Exception:  # noqa: BLE001 - informational only
+        pass
+    return {"cpu_model": model, "numpy": np.__version__, "blas": blas}
+
+
+def cpu_with_projections(turns, shape, cb) -> dict:
+    """The attention-only CPU value plus the model's projections for the same
+    turns: one layer's QKV / O / MLP GEMMs (float64 numpy, all cores through
+    BLAS threads) timed for each of 2 sample turns and scaled by L."""
+    import threading  # noqa: F401  (BLAS threads only)
+
+    rng = np.random.default_rng(0)
+    d, f = shape.d_model, shape.ffn
+    hq, hkv, hd = shape.n_heads, shape.n_kv_heads, shape.head_dim
+    w = {"qkv": rng.standard_normal(((hq + 2 * hkv) * hd, d)),
+         "o": rng.standard_normal((d, hq * hd)),
+         "gu": rng.standard_normal((2 * f, d)), "down": rng.standard_normal((d, f))}
+    per_tok = []
+    for _, _, _, new in turns[:2]:
+        x = rng.standard_normal((new, d))
+        t = time.perf_counter()
+        qkv = x @ w["qkv"].T
+        o = qkv[:, :hq * hd] @ w["o"].T
+        gu = o @ w["gu"].T
+        _ = gu[:, :f] @ w["down"].T
+        per_tok.append((time.perf_counter() - t) * shape.layers / new)
+    proj_s_per_tok = statistics.fmean(per_tok)
+    tokens = sum(kept + new for _, _, kept, new in turns)
+    new_total = sum(new for *_, new in turns)
+    attn_s = tokens / cb["value"]
+    total_s = attn_s + proj_s_per_tok * new_total
+    return {"value": tokens / total_s, "unit": "tokens/s",
+            "projection_s_per_new_token": proj_s_per_tok,
+            "sample": "attention (above) + numpy float64 QKV/O/gate-up/down GEMMs of one "
+                      "layer for 2 sample turns, scaled by L, BLAS threads on all cores"}
+
+
+def cpu_c1_whole_turns() -> dict:
+    """Config C1 end to end on the CPU path: all 12 turns of the reference's
+    4 tiny sessions through the float64 oracle forward (projections, RoPE,
+    attention over the whole conversation, as kvsim would recompute it)."""
+    from oracle import llama_ref
+    from paper_2403_19708_b200 import model
+    wl = json.loads((ROOT / "tests" / "golden" / "workload_c1.json").read_text())
+    shape = model.shape("tiny")
+    rng = np.random.default_rng(0)
+    sd = 0.02
+    L, d, f = shape.layers, shape.d_model, shape.ffn
+    hq, hkv, hd = shape.n_heads, shape.n_kv_heads, shape.head_dim
+    w = {"embed": rng.standard_normal((shape.vocab, d)) * sd,   # oracle [in, out] layout
+         "layers": [{"w_in": np.ones(d),
+                     "wqkv": rng.standard_normal((d, (hq + 2 * hkv) * hd)) * sd,
+                     "wo": rng.standard_normal((hq * hd, d)) * sd, "w_post": np.ones(d),
+                     "wg": rng.standard_normal((d, f)) * sd,
+                     "wu": rng.standard_normal((d, f)) * sd,
+                     "wd": rng.standard_normal((f, d)) * sd} for _ in range(L)],
+         "w_final": np.ones(d), "lm_head": rng.standard_normal((d, shape.vocab)) * sd}
+    empty = [(np.zeros((0, hkv, hd)),) * 2] * L
+    tokens = 0
+    t = time.perf_counter()
+    for k in range(3):
+        for s in wl["sessions"]:
+            hist = sum(a + b for a, b in s["turns"][:k])
+            ids = rng.integers(0, shape.vocab, hist + s["turns"][k][0])
+            llama_ref.forward(w, ids, empty, np.arange(0), n_heads=hq, n_kv_heads=hkv,
+                              head_dim=hd)
+            tokens += len(ids)
+    dt = time.perf_counter() - t
+    return {"value": tokens / dt, "unit": "tokens/s", "turns": 12, "prompt_tokens": tokens,
+            "seconds": dt, "cores": 1,
+            "sample": "C1 (tiny, 4 sessions x 3 turns): every turn's whole prompt through "
+                      "the float64 oracle forward (oracle/llama_ref.py), one process"}
 
 
 # ---------------------------------------------------------------------------
@@ -295,6 +453,32 @@ def link_peak(host_u8: torch.Tensor, dev_u8: torch.Tensor, nbytes: int = 1 << 30
             t = e0.elapsed_time(e1) * 1e-3
             best = t if best is None else min(best, t)
         out[name] = n / best / 1e9
+    # each direction while the other runs for the whole interval (K1 pre-loads
+    # and K4 saves share the link in e2e): the measured copy moves n/4, the
+    # background one n/2
+    s2 = torch.cuda.Stream()
+    q = n // 4
+    for name, fg in (("h2d_concurrent", "h2d"), ("d2h_concurrent", "d2h")):
+        best = None
+        for _ in range(3):
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            torch.cuda.synchronize()
+            with torch.cuda.stream(s2):   # background: the other direction, 2x longer
+                if fg == "h2d":
+                    host_u8[q:3 * q].copy_(dev_u8[q:3 * q], non_blocking=True)
+                else:
+                    dev_u8[q:3 * q].copy_(host_u8[q:3 * q], non_blocking=True)
+            with torch.cuda.stream(s):
+                e[0].record()
+                if fg == "h2d":
+                    dev_u8[:q].copy_(host_u8[:q], non_blocking=True)
+                else:
+                    host_u8[:q].copy_(dev_u8[:q], non_blocking=True)
+                e[1].record()
+            torch.cuda.synchronize()
+            t = e[0].elapsed_time(e[1]) * 1e-3
+            best = t if best is None else min(best, t)
+        out[name] = q / best / 1e9
     return out
 
 
@@ -360,7 +544,10 @@ def main():
 
     if args.impl == "reference":
         if rank == 0:
-            print(json.dumps(run_reference(args, shape, turns)), flush=True)
+            tp_ref = world if args.config == "c5" else 1
+            probe_ref = args.config == "c5" and world == 1 and args.tp_rank_of > 1
+            cfg = make_config(args, shape, turns, n_hits, world, tp_ref, probe_ref)
+            print(json.dumps(run_reference(args, shape, turns, cfg)), flush=True)
         return
 
     import torch
@@ -382,6 +569,16 @@ def main():
 
     from paper_2403_19708_b200 import build as _build
     from paper_2403_19708_b200.metrics import percentile
+
+    # measured serving replay: this rank's
+    # shard (1 of 8 -- the shard a GPU of an 8-GPU node serves) of the
+    # reference workload in arrival order through the reference serving loop,
+    # every prefill / save run on this GPU; before the bench's own arena so
+    # the two pinned arenas never coexist
+    serving = None
+    if (args.config in ("c2", "c3") and args.serve_dram_gb > 0 and tp == 1 and not rank_probe
+            and rank < 8):
+        serving = run_serving(args, rank, local)
     from paper_2403_19708_b200.runner import Job, Runner, attention_flops
     from paper_2403_19708_b200.store import HostArena
 
@@ -402,7 +599,10 @@ def main():
     max_new = max(new for *_, new in turns)
     max_kept = max(kept for *_, kept, _ in turns)
     # arenas: the same block ids in the pinned host arena and the HBM arena
-    arena = HostArena(n_blocks, block_bytes, pin=True)
+    # this rank's pinned arena on its GPU's NUMA node
+    from paper_2403_19708_b200 import numa as _numa
+    numa_node = _numa.gpu_numa_node(local)
+    arena = HostArena(n_blocks, block_bytes, pin=True, numa_node=numa_node)
     hbm = torch.empty(n_blocks * block_bytes // 2, dtype=torch.bfloat16, device=dev)
     g = torch.Generator(device=dev).manual_seed(7 + rank)
     chunk = 1 << 28
@@ -414,7 +614,7 @@ def main():
     torch.cuda.synchronize()
     tp_hook = None
     if tp > 1:
-        tp_hook = pdist.NcclAllReduce()
+        tp_hook = pdist.NcclComm(rank, world)   # native: ncclAllReduce inside the layer graph
     runner = Runner(shape, device=dev, seed=rank if tp > 1 else 0, block_tokens=tb,
                     host_arena=arena, tp_reduce=tp_hook,
                     hbm_arena=hbm, read_buffer_bytes=4 << 30, write_buffer_bytes=1 << 30,
@@ -422,7 +622,15 @@ def main():
                     # tune the GEMMs over the recompute baseline's prompt lengths too
                     autotune=max(shape.context_window, max_kept + 1) + max(max_new, 1),
                     overlap=bool(args.k2_overlap))
-    ids_perm = np.random.default_rng(99 + rank).permutation(n_blocks)
+    # block placement: the arena allocator's contiguous runs (what a session
+    # gets in serving, store.HostArena) or, with --fragmented, a random
+    # permutation (every block of a layer its own DMA)
+    if args.fragmented:
+        ids_perm = np.random.default_rng(99 + rank).permutation(n_blocks)
+    else:
+        ids_perm = np.concatenate([np.asarray(arena.alloc(nb), dtype=np.int64) for nb in nbs]
+                                  + ([np.asarray(arena.alloc(dec_nb), dtype=np.int64)]
+                                     if dec_nb else []))
     jobs = {"host": [], "hbm": [], "recompute": []}
     pos = 0
     trng = np.random.default_rng(5 + rank)
@@ -633,6 +841,9 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:   # N=1 only (contract)
         cb = cpu_reference(turns, shape, pairs_per_turn=24)
         cpu = {"value": cb["value"], "unit": "tokens/s", "cores": cb["cores"], "kind": "port",
+               **host_info(),
+               "with_projections": cpu_with_projections(turns, shape, cb),
+               "c1_whole_turns": cpu_c1_whole_turns(),
                "sample": (f"oracle port of attention_with_decoupled_cache (rope.py:118-144, "
                           f"float64 numpy, 1 thread/process) on 24 (layer, head) pairs of each "
                           f"of the {len(turns)} rank-0 turns ({cb['cpu_seconds']:.1f} CPU-s), "
@@ -648,27 +859,7 @@ def main():
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (reference ShareGPT-shaped session generator; random-init weights "
                 "and KV)",
-        "config": {
-            "workload": (f"{args.config}: {shape.name}-shaped, reference generate_poisson "
-                         f"sessions sharded by crc32(session) over {world} GPU(s); "
-                         f"{len(turns)} hit turns/GPU/step (of {n_hits} in shard)"
-                         if args.config != "c4" else
-                         f"c4: {shape.name}-shaped, W=4096, 32768-token stored histories "
-                         f"truncated by the reference rules to kept 2048..3648 (block-table "
-                         f"edit; only the kept blocks are materialised and loaded), 256 new "
-                         f"tokens per turn, {len(turns)} turns/GPU/step"),
-            "turns_per_gpu": len(turns), "kept_p50": percentile(kept_l, 0.5),
-            "new_p50": percentile(new_l, 0.5), "block_tokens": tb,
-            "value_mode": "KV resident in an HBM arena (no host link)",
-            "e2e_mode": "KV streamed from pinned host DRAM by the layer-wise pre-loader; "
-                        "new-token KV saved back asynchronously",
-            "l2": "inputs larger than L2 (per-step KV " f"{h2d_bytes / 1e9:.1f} GB)",
-            "parallelism": (f"tensor-parallel tp{tp} (NCCL all-reduce of W_o / W_down "
-                            f"partials over NVLink)" if tp > 1 else
-                            f"one rank of a tp{args.tp_rank_of} shard, all-reduce excluded "
-                            f"(per-rank compute probe; outputs are partial sums)"
-                            if rank_probe else
-                            f"sessions sharded, no collective ({world} independent ranks)")},
+        "config": make_config(args, shape, turns, n_hits, world, tp, rank_probe),
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d_step,
                 "d2h_bytes_per_step": d2h_step, "ms_per_step": ms_host / args.steps},
         # SURVEY.md §8d/§8e companions: new-token throughput and sessions (turns)/s,
@@ -700,14 +891,30 @@ def main():
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                      "flops_per_launch": statistics.fmean(w for _, w in att),
                      "launches": len(att)},
-        "roofline_link": {"kernel": "K1 askv_preload_layer (H2D DMA batches)", "bound": "host link",
+        "roofline_link": {"kernel": "K1 askv_preload_layer (H2D copy-engine DMAs: strided "
+                                    "2-D runs of contiguous arena blocks)",
+                          "bound": "host link",
                           "achieved": h2d_bytes / load_busy / 1e9 if load_busy else None,
                           "peak": link["h2d"], "unit": "GB/s",
                           "frac": (h2d_bytes / load_busy / 1e9) / link["h2d"] if load_busy else None,
                           "e2e_frac": (h2d_step / (ms_host / args.steps * 1e-3) / 1e9) / link["h2d"],
                           "d2h_peak": link["d2h"],
+                          "h2d_peak_with_d2h_running": link["h2d_concurrent"],
+                          "block_placement": "random permutation" if args.fragmented
+                                             else "arena allocator (contiguous runs)",
                           "peak_source": "measured in this run: one 1 GB pinned-host->HBM "
                                          "cudaMemcpyAsync, best of 3"},
+        # K4: the saver's D2H runs while K1 streams the next layers in (e2e),
+        # so its roofline is the D2H rate measured under a concurrent H2D
+        "roofline_save": {"kernel": "K4 askv_save_layer (D2H of the new tokens' rows)",
+                          "bound": "host link (D2H with H2D running)",
+                          "achieved": d2h_bytes / save_busy / 1e9 if save_busy else None,
+                          "peak": link["d2h_concurrent"], "unit": "GB/s",
+                          "frac": ((d2h_bytes / save_busy / 1e9) / link["d2h_concurrent"]
+                                   if save_busy else None),
+                          "d2h_peak_alone": link["d2h"],
+                          "peak_source": "measured in this run: 256 MB D2H while a 512 MB "
+                                         "H2D runs on another stream, best of 3"},
         "roofline_reembed": {"kernel": "askv_reembed (K2)", "bound": "hbm",
                              "achieved": emb_gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": emb_gbs / hbm_peak},
@@ -717,6 +924,9 @@ def main():
         "clocks": clocks_value,          # during the `value` timed region
         "clocks_e2e": clocks,            # during the `e2e` timed region
         "cpu_baseline": cpu,
+        "serving": serving,
+        "host_arena": {"numa_node": arena.numa_node, "numa_nodes": _numa.node_count(),
+                       "bytes": arena.n_blocks * arena.block_bytes},
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -102,19 +102,25 @@ int askv_rope_new(const void* qkv, int64_t qkv_row_stride, int n_new, int n_head
 
 /*
  * K3 — prefill attention over [reused prefix | new tokens] on tcgen05/TMEM,
- * TMA-fed, split-KV + deterministic combine when the grid is short.
+ * TMA-fed.  num_splits <= 1 with single-tile units: stream-K (the KV tiles of
+ * all (query tile, head) units cut into one equal range per SM, partials of
+ * the units cut across SMs merged by a deterministic combine); num_splits > 1:
+ * uniform split-KV + combine.
  *   q   : [n_new][Hq][hd] bf16 (already rotated)
  *   kv  : [n_cached+n_new][2][Hkv][hd] bf16 rows (K rotated), row stride kv_row_stride
  *   out : [n_new][Hq][hd] bf16
  * Query i sees keys j <= n_cached + i; q-head h uses kv-head h/(Hq/Hkv).
- * scale = 1/sqrt(hd) reproduces rope.py:98.  num_splits = 0 picks a split count
- * for the SM count; workspace must hold askv_attn_workspace_bytes(...).
+ * scale = 1/sqrt(hd) reproduces rope.py:98.  num_splits = 0 picks the schedule
+ * for the SM count; workspace must hold askv_attn_workspace_bytes_gqa(...).
  * Replaces: rope.py:94-105 (_causal_attention) inside rope.py:118-144.
  */
 int askv_prefill_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cached,
                       int n_new, int n_heads, int n_kv_heads, int head_dim, float scale,
                       void* out, void* workspace, size_t workspace_bytes, int num_splits,
                       void* stream);
+size_t askv_attn_workspace_bytes_gqa(int n_cached, int n_new, int n_heads, int n_kv_heads,
+                                     int head_dim, int num_splits);
+/* The same without n_kv_heads: the largest need over every grouping of n_heads. */
 size_t askv_attn_workspace_bytes(int n_cached, int n_new, int n_heads, int head_dim,
                                  int num_splits);
 /* Split count the auto policy would use (for reporting / tests). */
@@ -272,9 +278,38 @@ typedef struct askv_prefill_plan {
   void* mirror_base;
   const int64_t* mirror_block_ids; /* host array */
   int32_t mirror_nblocks;
+  /* Optional NCCL communicator of the tensor-parallel group (config C5,
+   * askv_nccl_comm_init).  When set, the row-parallel W_o and W_down partials
+   * are summed by ncclAllReduce on `stream` inside the loop (captured into
+   * the layer graph): rank `tp_rank` 0 adds the residual in its GEMM epilogue
+   * and reduces in place in x; the other ranks reduce their partial from h
+   * into x, so x = x + sum over ranks with no separate residual kernel. */
+  void* nccl_comm;
+  int32_t tp_rank;
+  /* Rows addressable from the pre-load source for K3's direct V reads (0 =
+   * off): src_kind 1 -- rows of each src_layer[l] slot; src_kind 2 -- rows of
+   * the HBM arena from src_layer[0] on.  With it, the V rows of the kept
+   * rows' whole 128-row tiles are read by K3 where the pre-loader left them
+   * (src_kind 2 needs head 0 and block_tokens 128) and K2 moves K only: K2's
+   * traffic is the rotation's own read + write of K. */
+  int64_t src_rows;
 } askv_prefill_plan;
 
 int askv_prefill_layers(const askv_prefill_plan* plan, void* stream);
+
+/*
+ * K5 — NCCL for the tensor-parallel all-reduce (C5), bound at run time
+ * (libnccl.so.2).  unique_id writes the 128-byte ncclUniqueId rank 0 shares
+ * with the group; comm_init builds this rank's communicator (collective over
+ * the group); allreduce_bf16 sums `elems` bf16 values (send may equal recv) on
+ * `stream`.  Replaces: nothing in the reference (PAPER.md:501 names NCCL only
+ * for "synchronization of the parallel GPU workers").
+ */
+int askv_nccl_unique_id(void* out128);
+int askv_nccl_comm_init(int nranks, int rank, const void* id128, void** comm);
+int askv_nccl_comm_destroy(void* comm);
+int askv_nccl_allreduce_bf16(const void* send, void* recv, int64_t elems, void* comm,
+                             void* stream);
 /* Write the device globaltimer (ns) to *dst (device memory) in stream order:
  * a timing mark that stays cheap while the host link is saturated. */
 int askv_stamp(uint64_t* dst, void* stream);

@@ -35,6 +35,11 @@ SIGNATURES = {
     "askv_prefill_attn": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _vp,
                                  _sz, _i32, _vp]),
     "askv_attn_workspace_bytes": (_sz, [_i32, _i32, _i32, _i32, _i32]),
+    "askv_attn_workspace_bytes_gqa": (_sz, [_i32, _i32, _i32, _i32, _i32, _i32]),
+    "askv_nccl_unique_id": (_i32, [_vp]),
+    "askv_nccl_comm_init": (_i32, [_i32, _i32, _vp, C.POINTER(_vp)]),
+    "askv_nccl_comm_destroy": (_i32, [_vp]),
+    "askv_nccl_allreduce_bf16": (_i32, [_vp, _vp, _i64, _vp, _vp]),
     "askv_attn_num_splits": (_i32, [_i32, _i32, _i32, _i32]),
     "askv_attn_num_splits_gqa": (_i32, [_i32, _i32, _i32, _i32, _i32]),
     "askv_preload_layer": (_i32, [_vp, _vp, _pi64, _i32, _i64, _i64, _i64, _i64, _vp, _vp]),
@@ -86,6 +91,8 @@ class PrefillPlan(C.Structure):
         ("kv_layers", _pp), ("graph", C.c_int32), ("kv_alt", C.c_void_p),
         ("mirror_base", C.c_void_p), ("mirror_block_ids", C.POINTER(C.c_int64)),
         ("mirror_nblocks", C.c_int32),
+        ("nccl_comm", C.c_void_p), ("tp_rank", C.c_int32),
+        ("src_rows", C.c_int64),
     ]
 
 

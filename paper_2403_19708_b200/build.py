@@ -17,7 +17,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libaskv.so"
-SOURCES = ["rope.cu", "attention.cu", "copy_engine.cu", "elementwise.cu", "runtime.cu"]
+SOURCES = ["rope.cu", "attention.cu", "copy_engine.cu", "elementwise.cu", "runtime.cu",
+           "collective.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -45,7 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
            "-Xptxas", "-v" if verbose else "-O3", "--expt-relaxed-constexpr",
            "-I", str(ROOT / "include"), "-o", str(tmp)]
     cmd += [str(CSRC / s) for s in SOURCES]
-    cmd += ["-lcublasLt"]
+    cmd += ["-lcublasLt", "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

@@ -35,10 +35,29 @@ inline int launch_status(const char* what) { return cuda_status(cudaGetLastError
 // Entry points of the native layer loop with in-kernel launch timestamps
 // ({begin, end} globaltimer ns, see attention.cu launch_stamp_*); the C ABI
 // functions call these with stamp == nullptr.
+// K5: in-place / out-of-place bf16 sum over a NCCL communicator (collective.cu).
+int tp_allreduce_bf16(const void* send, void* recv, int64_t elems, void* comm,
+                      cudaStream_t stream);
+// K3's optional V source: the V rows of the first `tiles` 128-row KV tiles
+// are read where the pre-loader left them instead of from `kv` (K2 then
+// copies no V for those rows).  kind 1: contiguous rows (a read-buffer slot),
+// tile t at row row0 + 128 t of `base`; kind 2: HBM-arena block table, tile t
+// = block t at row blk_off[t] / row_elems + layer_row of `base` (`rows` rows).
+struct VSource {
+  int kind = 0;
+  int tiles = 0;
+  const void* base = nullptr;
+  int64_t rows = 0;
+  int64_t row0 = 0;
+  const int64_t* blk_off = nullptr;
+  int64_t row_elems = 0;
+  int64_t layer_row = 0;
+};
 int prefill_attn_stamped(const void* q, const void* kv, int64_t kv_row_stride, int n_cached,
                          int n_new, int n_heads, int n_kv_heads, int head_dim, float scale,
                          void* out, void* workspace, size_t workspace_bytes, int num_splits,
-                         void* stream, unsigned long long* stamp);
+                         void* stream, unsigned long long* stamp,
+                         const VSource* vsrc = nullptr);
 int rmsnorm_stamped(const void* x, const void* w, void* y, int rows, int cols, float eps,
                     void* stream, unsigned long long* begin);
 int rope_new_stamped(const void* qkv, int64_t qkv_row_stride, int n_new, int n_heads,
@@ -49,6 +68,6 @@ int reembed_stamped(const void* src_base, const int64_t* src_block_off, int bloc
                     int64_t src_row_stride, int64_t first_token, int kept, int n_kv_heads,
                     int head_dim, const float* rope_table, int table_positions,
                     const int32_t* positions, int pos0, void* dst, int64_t dst_row_stride,
-                    void* stream, unsigned long long* stamp);
+                    void* stream, unsigned long long* stamp, int v_from = 0);
 
 }  // namespace askv

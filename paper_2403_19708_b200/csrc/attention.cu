@@ -65,6 +65,7 @@ __device__ __forceinline__ void launch_stamp_end(unsigned long long* st) {
 constexpr int kBM = 128;  // query rows per tile (UMMA M)
 constexpr int kBN = 128;  // key rows per tile (UMMA N of S, K of PV)
 constexpr int kMaxSplits = 32;
+constexpr int kMaxSkSlots = 24;  // stream-K: pieces per unit (combine smem)
 
 struct AttnParams {
   int n_new;
@@ -79,7 +80,78 @@ struct AttnParams {
   unsigned long long* stamp;  // optional {begin, end} launch timestamps
   float* part_o;       // [splits][n_new][hq][HD]
   float* part_lse;     // [splits][n_new][hq]   (log2 units)
+  // stream-K schedule (attn_sk_kernel): the KV tiles of every unit (query tile,
+  // head), head-major, form one list of sk_total tiles cut into gridDim.x equal
+  // contiguous ranges, one per CTA (= per SM, one wave)
+  int sk_total;        // G: sum over units of their KV tiles
+  int sk_tiles_head;   // KV tiles of one head's units
+  int sk_q_tiles;      // query tiles per head (unit = (head, query tile))
+  int sk_units;        // units = heads x sk_q_tiles (partial slab stride)
+  // V source (VSource, askv_internal.h): tiles < v_src_tiles load V through
+  // tm_vs at row v_blk_off ? v_blk_off[t] / v_row_elems + v_layer_row
+  //                         : v_src_row0 + 128 t
+  int v_src_tiles;
+  int64_t v_src_row0;
+  const int64_t* v_blk_off;
+  int64_t v_row_elems;
+  int64_t v_layer_row;
 };
+
+// Where KV tile t's V rows come from: (use the V-source map?, row coordinate).
+__device__ __forceinline__ int v_tile_row(const AttnParams& p, int t, bool& src) {
+  src = t < p.v_src_tiles;
+  if (!src) return t * kBN;
+  return p.v_blk_off ? (int)(p.v_blk_off[t] / p.v_row_elems + p.v_layer_row)
+                     : (int)(p.v_src_row0 + (int64_t)t * kBN);
+}
+
+// KV tiles query tile q must visit (keys <= n_cached + its last token).
+__host__ __device__ __forceinline__ int unit_tiles(const AttnParams& p, int q) {
+  const int q_rows = p.pack > 1 ? p.n_new * p.pack : p.n_new;
+  const int last = (q + 1) * kBM < q_rows ? (q + 1) * kBM - 1 : q_rows - 1;
+  const int tok = p.pack > 1 ? last / p.pack : last;
+  return (p.n_cached + tok + 1 + kBN - 1) / kBN;
+}
+
+// One CTA's contiguous share of the stream-K tile list.
+__host__ __device__ __forceinline__ void sk_range(const AttnParams& p, int c, int ctas, int& g0,
+                                                  int& g1) {
+  g0 = (int)((int64_t)c * p.sk_total / ctas);
+  g1 = (int)((int64_t)(c + 1) * p.sk_total / ctas);
+}
+
+// CTA whose range holds global tile g.
+__host__ __device__ __forceinline__ int sk_owner(const AttnParams& p, int g, int ctas) {
+  return (int)(((int64_t)(g + 1) * ctas - 1) / p.sk_total);
+}
+
+// The piece of a unit that starts at global tile g inside [g, g1): which unit,
+// its tile range, and the partial slot (CTA index relative to the unit's first
+// CTA).  `whole` = the piece is the entire unit (final output, no combine).
+struct Piece {
+  int head, q, t_begin, t_end, slot, next;
+  bool whole;
+};
+__host__ __device__ __forceinline__ Piece sk_piece(const AttnParams& p, int c, int ctas, int g,
+                                                   int g1) {
+  Piece pc;
+  pc.head = g / p.sk_tiles_head;
+  int r = g - pc.head * p.sk_tiles_head;
+  int q = 0, tu = unit_tiles(p, 0);
+  while (r >= tu) {
+    r -= tu;
+    ++q;
+    tu = unit_tiles(p, q);
+  }
+  const int ub = g - r;
+  pc.q = q;
+  pc.t_begin = r;
+  pc.t_end = tu < g1 - ub ? tu : g1 - ub;
+  pc.slot = c - sk_owner(p, ub, ctas);
+  pc.whole = pc.t_begin == 0 && pc.t_end == tu;
+  pc.next = ub + pc.t_end;
+  return pc;
+}
 
 // ============================================================================
 // Kernel: two softmax warpgroups on one tcgen05 pipeline, S/P/O in TMEM.
@@ -143,7 +215,8 @@ template <int HD, bool kAllowPair>
 __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
-                    const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
+                    const __grid_constant__ CUtensorMap tm_v,
+                    const __grid_constant__ CUtensorMap tm_vs, const AttnParams p) {
   using C = Cfg<HD, kAllowPair>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -253,6 +326,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
       tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
+      tma_prefetch_desc(&tm_vs);
       // K/V tiles are re-read by every query tile of the head: keep them in L2
       // against streaming traffic (the pre-loader's DMA writes); Q is read once.
       const uint64_t pol_kv = l2_policy_evict_last();
@@ -287,10 +361,12 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
         const int st = jv % C::kVStages;
         if (jv >= C::kVStages) mbar_wait(&v_empty[st], ((jv / C::kVStages) - 1) & 1);
         mbar_expect_tx(&v_full[st], C::kTileBytes);
+        bool vs;
+        const int vrow = v_tile_row(p, t_begin + jv, vs);
 #pragma unroll
         for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d_hint(sV + st * C::kTileBytes + c * (kBN * 128), &tm_v, &v_full[st],
-                           c * 64, kh, (t_begin + jv) * kBN, pol_kv);
+          tma_load_3d_hint(sV + st * C::kTileBytes + c * (kBN * 128), vs ? &tm_vs : &tm_v,
+                           &v_full[st], c * 64, kh, vrow, pol_kv);
       }
     }
   } else if (warp == 9) {
@@ -576,6 +652,484 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
   if (p.num_splits == 1) launch_stamp_end(p.stamp);
 }
 
+// ============================================================================
+// Stream-K kernel (single query tile per unit, the non-paired shapes).
+//
+// Units (query tile, head) are too few to fill 148 SMs at the path's skinny
+// shapes (C3 p50: 2 query tiles x 40 heads = 80 CTAs) and splitting them
+// uniformly costs a second wave.  Instead the KV tiles of all units form one
+// head-major list cut into gridDim.x (<= #SMs) equal contiguous ranges: each
+// CTA walks its range as a sequence of pieces (a piece = a run of one unit's
+// KV tiles), re-loading Q at each unit boundary.  A piece covering a whole
+// unit writes the bf16 output; a unit cut across CTAs leaves one fp32 partial
+// (O, lse) per piece, merged in slot order by attn_sk_combine_kernel
+// (deterministic).  Warp roles and the per-tile pipeline are the SPLIT mode of
+// attn_fwd_kernel; the ring / phase counters run on across pieces, q_empty
+// (MMA -> Q producer) guards the Q tile and o_free (softmax -> MMA) the
+// TMEM S / O columns between pieces.
+// ============================================================================
+template <int HD>
+struct SkCfg {
+  using B = Cfg<HD, false>;
+  static constexpr int kKStages = B::kKStages;
+  static constexpr int kVStages = B::kVStages;
+  static constexpr int kChunks = B::kChunks;
+  static constexpr int kTileBytes = B::kTileBytes;
+  static constexpr int kQOff = B::kQOff, kKOff = B::kKOff, kVOff = B::kVOff,
+                       kBarOff = B::kBarOff;
+  static constexpr int kNumBars = B::kNumBars + 2;  // + q_empty, o_free
+  static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
+  static constexpr int kSmemBytes = kTmemSlotOff + 16 + 1024;
+  static constexpr uint32_t kTmemCols = B::kTmemCols;
+  static constexpr int kSoftmaxRegs = B::kSoftmaxRegs;
+  static constexpr int kThreads = B::kThreads;
+  static constexpr float kRescaleLog2 = B::kRescaleLog2;
+  __host__ __device__ static constexpr uint32_t col_s(int w) { return B::col_s(w); }
+  __host__ __device__ static constexpr uint32_t col_o(int w) { return B::col_o(w); }
+  static_assert(kSmemBytes <= 232448, "smem budget");
+};
+
+template <int HD>
+__global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
+    attn_sk_kernel(const __grid_constant__ CUtensorMap tm_q,
+                   const __grid_constant__ CUtensorMap tm_k,
+                   const __grid_constant__ CUtensorMap tm_v,
+                   const __grid_constant__ CUtensorMap tm_vs, const AttnParams p) {
+  using C = SkCfg<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + C::kQOff;
+  uint8_t* sK = smem + C::kKOff;
+  uint8_t* sV = smem + C::kVOff;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = q_full + 1;
+  uint64_t* k_empty = k_full + C::kKStages;
+  uint64_t* v_full = k_empty + C::kKStages;
+  uint64_t* v_empty = v_full + C::kVStages;
+  uint64_t* s_full = v_empty + C::kVStages;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_full = p_full + 2;
+  uint64_t* q_empty = o_full + 2;
+  uint64_t* o_free = q_empty + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kTmemSlotOff);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int ctas = gridDim.x;
+  const int cta = blockIdx.x;
+  const int pack = p.pack;
+  const int q_rows = pack > 1 ? p.n_new * pack : p.n_new;
+  auto tok = [&](int row) { return pack > 1 ? row / pack : row; };
+  auto out_row = [&](int h, int row) -> int64_t {
+    return pack > 1 ? (int64_t)(row / pack) * p.hq + h * pack + row % pack
+                    : (int64_t)row * p.hq + h;
+  };
+  if (threadIdx.x == 0) ATTN_TRACE(0);
+  launch_stamp_begin(p.stamp);
+  int g0, g1;
+  sk_range(p, cta, ctas, g0, g1);
+  if (g0 >= g1) return;  // CTA-uniform (the host launches <= sk_total CTAs)
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    mbar_init(o_free, 8);  // one arrival per softmax warp
+    for (int s = 0; s < C::kKStages; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < C::kVStages; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int w = 0; w < 2; ++w) {
+      mbar_init(&s_full[w], 1);
+      mbar_init(&p_full[w], 128);
+      mbar_init(&o_full[w], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 8) tmem_alloc(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) ATTN_TRACE(1);
+  auto shrink = [] {
+    if constexpr (C::kSoftmaxRegs > 0) setmaxnreg_dec<56>();
+  };
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ TMA: Q per piece, K tiles
+    shrink();
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      tma_prefetch_desc(&tm_vs);
+      const uint64_t pol_kv = l2_policy_evict_last();
+      const uint64_t pol_q = l2_policy_evict_first();
+      int jk = 0, np = 0;
+      for (int g = g0; g < g1; ++np) {
+        const Piece pc = sk_piece(p, cta, ctas, g, g1);
+        g = pc.next;
+        const int kh = pack > 1 ? pc.head : pc.head / p.group;
+        if (np > 0) mbar_wait(q_empty, (np - 1) & 1);  // every S of the previous piece done
+        mbar_expect_tx(q_full, C::kTileBytes);
+#pragma unroll
+        for (int c = 0; c < C::kChunks; ++c)
+          tma_load_3d_hint(sQ + c * (kBM * 128), &tm_q, q_full, c * 64,
+                           pack > 1 ? pc.head * pack : pc.head, tok(pc.q * kBM), pol_q);
+        for (int t = pc.t_begin; t < pc.t_end; ++t, ++jk) {
+          const int st = jk % C::kKStages;
+          if (jk >= C::kKStages) mbar_wait(&k_empty[st], ((jk / C::kKStages) - 1) & 1);
+          mbar_expect_tx(&k_full[st], C::kTileBytes);
+#pragma unroll
+          for (int c = 0; c < C::kChunks; ++c)
+            tma_load_3d_hint(sK + st * C::kTileBytes + c * (kBN * 128), &tm_k, &k_full[st],
+                             c * 64, kh, t * kBN, pol_kv);
+        }
+      }
+    }
+  } else if (warp == 10) {
+    // ------------------------------------------------------------ TMA: V tiles
+    shrink();
+    if (lane == 0) {
+      const uint64_t pol_kv = l2_policy_evict_last();
+      int jv = 0;
+      for (int g = g0; g < g1;) {
+        const Piece pc = sk_piece(p, cta, ctas, g, g1);
+        g = pc.next;
+        const int kh = pack > 1 ? pc.head : pc.head / p.group;
+        for (int t = pc.t_begin; t < pc.t_end; ++t, ++jv) {
+          const int st = jv % C::kVStages;
+          if (jv >= C::kVStages) mbar_wait(&v_empty[st], ((jv / C::kVStages) - 1) & 1);
+          mbar_expect_tx(&v_full[st], C::kTileBytes);
+          bool vs;
+          const int vrow = v_tile_row(p, t, vs);
+#pragma unroll
+          for (int c = 0; c < C::kChunks; ++c)
+            tma_load_3d_hint(sV + st * C::kTileBytes + c * (kBN * 128), vs ? &tm_vs : &tm_v,
+                             &v_full[st], c * 64, kh, vrow, pol_kv);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ MMA issuer
+    shrink();
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(kBM, kBN, 0, 0);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(kBM, HD, 0, 1);
+      const uint32_t sk = smem_u32(sK), sv = smem_u32(sV), sq = smem_u32(sQ);
+      int jb = 0, np = 0;
+      int cnt0 = 0, cnt1 = 0;  // tiles each softmax group finished in earlier pieces
+      for (int g = g0; g < g1; ++np) {
+        const Piece pc = sk_piece(p, cta, ctas, g, g1);
+        g = pc.next;
+        const bool last_piece = g >= g1;
+        const int n = pc.t_end - pc.t_begin;
+        mbar_wait(q_full, np & 1);
+        if (np < 4) ATTN_TRACE(40 + 2 * np);
+        if (np > 0) mbar_wait(o_free, (np - 1) & 1);  // S / O columns released
+        if (np < 4) ATTN_TRACE(41 + 2 * np);
+        tc_fence_after();
+        auto issue_s = [&](int w, int j) {
+          const uint32_t kb = sk + ((jb + j) % C::kKStages) * C::kTileBytes;
+#pragma unroll
+          for (int k = 0; k < HD / 16; ++k) {
+            const uint32_t off = (k >> 2) * (kBM * 128) + (k & 3) * 32;
+            umma_bf16(tmem + C::col_s(w), sdesc_sw128(sq + off, 16, 1024),
+                      sdesc_sw128(kb + off, 16, 1024), idesc_s, k > 0);
+          }
+          umma_commit(&s_full[w]);
+          // the piece's last reader of Q (the last piece's phase has no waiter)
+          if (j == n - 1 && !last_piece) umma_commit(q_empty);
+        };
+        auto issue_pv = [&](int w, int j, bool first) {
+          const uint32_t vb = sv + ((jb + j) % C::kVStages) * C::kTileBytes;
+#pragma unroll
+          for (int k = 0; k < kBN / 16; ++k)
+            umma_bf16_tmem_a(tmem + C::col_o(w), tmem + C::col_s(w) + k * 8,
+                             sdesc_sw128(vb + k * (16 * 128), kBN * 128, 1024), idesc_o,
+                             (!first) || (k > 0));
+          umma_commit(&o_full[w]);
+        };
+        auto wait_k = [&](int j) {
+          mbar_wait(&k_full[(jb + j) % C::kKStages], ((jb + j) / C::kKStages) & 1);
+          tc_fence_after();
+        };
+        auto wait_v = [&](int j) {
+          mbar_wait(&v_full[(jb + j) % C::kVStages], ((jb + j) / C::kVStages) & 1);
+          tc_fence_after();
+        };
+        wait_k(0);
+        issue_s(0, 0);
+        umma_commit(&k_empty[jb % C::kKStages]);
+        if (n > 1) {
+          wait_k(1);
+          issue_s(1, 1);
+          umma_commit(&k_empty[(jb + 1) % C::kKStages]);
+        }
+        for (int j = 0; j < n; ++j) {
+          const int w = j & 1;
+          mbar_wait(&p_full[w], ((w ? cnt1 : cnt0) + (j >> 1)) & 1);
+          if (jb + j < 28) ATTN_TRACE(64 + jb + j);
+          wait_v(j);
+          if (jb + j < 28) ATTN_TRACE(96 + jb + j);
+          issue_pv(w, j, j < 2);
+          if (jb + j < 28) ATTN_TRACE(160 + jb + j);
+          umma_commit(&v_empty[(jb + j) % C::kVStages]);
+          if (j + 2 < n) {
+            wait_k(j + 2);
+            if (jb + j < 28) ATTN_TRACE(128 + jb + j);
+            issue_s(w, j + 2);
+            umma_commit(&k_empty[(jb + j + 2) % C::kKStages]);
+          }
+        }
+        cnt0 += (n + 1) / 2;
+        cnt1 += n / 2;
+        jb += n;
+      }
+    }
+  } else if (warp < 8) {
+    // ------------------------------------------------------------ softmax groups
+    if constexpr (C::kSoftmaxRegs > 0) setmaxnreg_inc<C::kSoftmaxRegs>();
+    const int w = warp >> 2;
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t t_s = tmem + lane_off + C::col_s(w);
+    const uint32_t t_o = tmem + lane_off + C::col_o(w);
+    const float sl2 = p.scale_log2;
+    int cw = 0;  // this group's tiles in earlier pieces (barrier phases)
+    for (int g = g0; g < g1;) {
+      const Piece pc = sk_piece(p, cta, ctas, g, g1);
+      g = pc.next;
+      const int n = pc.t_end - pc.t_begin;
+      const int my_tiles = (n - w + 1) / 2;
+      const int qt0 = pc.q * kBM;
+      const int row_limit = p.n_cached + tok(qt0 + r);
+      float m_acc = -INFINITY, l_acc = 0.f;
+      auto tile = [&](auto mask_tag, int t, int lim) {
+        constexpr bool kMask = decltype(mask_tag)::value;
+        uint32_t sr[kBN];
+#pragma unroll
+        for (int c = 0; c < kBN / 32; ++c)
+          tmem_ld32_nowait(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+        tmem_wait_ld();
+        if (kMask) {
+#pragma unroll
+          for (int e = 0; e < kBN; ++e) sr[e] = (e <= lim) ? sr[e] : 0xff800000u;
+        }
+        float a0 = fmaxf(__uint_as_float(sr[0]), __uint_as_float(sr[1]));
+        float a1 = fmaxf(__uint_as_float(sr[2]), __uint_as_float(sr[3]));
+        float a2 = fmaxf(__uint_as_float(sr[4]), __uint_as_float(sr[5]));
+        float a3 = fmaxf(__uint_as_float(sr[6]), __uint_as_float(sr[7]));
+#pragma unroll
+        for (int e = 8; e < kBN; e += 8) {
+          a0 = fmax3(a0, __uint_as_float(sr[e + 0]), __uint_as_float(sr[e + 1]));
+          a1 = fmax3(a1, __uint_as_float(sr[e + 2]), __uint_as_float(sr[e + 3]));
+          a2 = fmax3(a2, __uint_as_float(sr[e + 4]), __uint_as_float(sr[e + 5]));
+          a3 = fmax3(a3, __uint_as_float(sr[e + 6]), __uint_as_float(sr[e + 7]));
+        }
+        const float m_tile = fmax3(fmax3(a0, a1, a2), a3, -INFINITY) * sl2;
+        const bool need = m_tile > m_acc + C::kRescaleLog2;
+        if (t > 0) mbar_wait(&o_full[w], (cw + t - 1) & 1);  // PV(t-1) of this group
+        if (t == 0) {
+          if (need) m_acc = m_tile;
+        } else if (__any_sync(0xffffffffu, need)) {
+          tc_fence_after();
+          const float f = need ? ex2(m_acc - m_tile) : 1.f;
+#pragma unroll 1
+          for (int c = 0; c < HD / 32; ++c) {
+            float ov[32];
+            tmem_ld32(t_o + c * 32, ov);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) ov[e] *= f;
+            tmem_st32(t_o + c * 32, ov);
+          }
+          tmem_wait_st();
+          if (need) {
+            l_acc *= f;
+            m_acc = m_tile;
+          }
+        }
+        const float neg_m = (m_acc == -INFINITY) ? 0.f : -m_acc;
+        const float2 sl2v = make_float2(sl2, sl2), negm2 = make_float2(neg_m, neg_m);
+        float2 ls0 = make_float2(0.f, 0.f), ls1 = ls0, ls2 = ls0, ls3 = ls0;
+#pragma unroll
+        for (int c = 0; c < kBN / 32; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const int k = c * 32 + e;
+            const float2 x = ffma2(make_float2(__uint_as_float(sr[k]), __uint_as_float(sr[k + 1])),
+                                   sl2v, negm2);
+            const float2 pp = (!kMask && ((e >> 1) & 3) == 3) ? ex2_poly2(x)
+                                                               : make_float2(ex2(x.x), ex2(x.y));
+            switch ((e >> 1) & 3) {
+              case 0: ls0 = fadd2(ls0, pp); break;
+              case 1: ls1 = fadd2(ls1, pp); break;
+              case 2: ls2 = fadd2(ls2, pp); break;
+              default: ls3 = fadd2(ls3, pp); break;
+            }
+            pk[e >> 1] = pack_bf16x2(pp.x, pp.y);
+          }
+          tmem_st16(t_s + c * 16, pk);
+        }
+        const float2 la = fadd2(ls0, ls1), lb = fadd2(ls2, ls3);
+        l_acc += (la.x + la.y) + (lb.x + lb.y);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&p_full[w]);
+      };
+      for (int t = 0; t < my_tiles; ++t) {
+        const int j = 2 * t + w;
+        mbar_wait(&s_full[w], (cw + t) & 1);
+        if (threadIdx.x == 0 && cw + t < 14) ATTN_TRACE(8 + 2 * (cw + t));
+        tc_fence_after();
+        const int kbase = (pc.t_begin + j) * kBN;
+        if (kbase + kBN - 1 > p.n_cached + tok(qt0))
+          tile(std::true_type{}, t, row_limit - kbase);
+        else
+          tile(std::false_type{}, t, 0);
+        if (threadIdx.x == 0 && cw + t < 14) ATTN_TRACE(9 + 2 * (cw + t));
+      }
+      if (threadIdx.x == 0) ATTN_TRACE(3);
+      if (my_tiles > 0) {
+        mbar_wait(&o_full[w], (cw + my_tiles - 1) & 1);
+        tc_fence_after();
+      }
+      // ---- merge the two groups' (m, l, O) through TMEM; each takes half the columns.
+      // Everything this piece needs from TMEM is pulled into registers first,
+      // then o_free lets the next piece's MMAs start while the partial is
+      // stored (column-major per unit, so a warp's 32 rows of one column are
+      // one coalesced 128-byte store).
+      tmem_st2(t_s + 64, m_acc, l_acc);
+      tmem_wait_st();
+      tc_fence_before();
+      named_bar_sync(1, 256);
+      tc_fence_after();
+      float m0, l0, m1, l1;
+      tmem_ld2(tmem + lane_off + C::col_s(0) + 64, m0, l0);
+      tmem_ld2(tmem + lane_off + C::col_s(1) + 64, m1, l1);
+      const float m_fin = fmaxf(m0, m1);
+      const float f0 = l0 > 0.f ? ex2(m0 - m_fin) : 0.f;
+      const float f1 = l1 > 0.f ? ex2(m1 - m_fin) : 0.f;
+      const float l_fin = l0 * f0 + l1 * f1;
+      const float f_self = w ? f1 : f0, f_other = w ? f0 : f1;
+      const int col0 = w * (HD / 2);
+      const float inv_l = l_fin > 0.f ? 1.f / l_fin : 0.f;
+      const uint32_t t_o_other = tmem + lane_off + C::col_o(w ^ 1);
+      constexpr int kHalf = HD / 2;
+      float o[kHalf];
+#pragma unroll
+      for (int c = 0; c < kHalf / 32; ++c) {
+        float a[32], b[32];
+        tmem_ld32(t_o + col0 + c * 32, a);
+        tmem_ld32(t_o_other + col0 + c * 32, b);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const float x = f_self > 0.f ? a[e] * f_self : 0.f;
+          const float y = f_other > 0.f ? b[e] * f_other : 0.f;
+          o[c * 32 + e] = (x + y) * inv_l;
+        }
+      }
+      // S / O columns of both groups are read: the next piece may overwrite them
+      if (g < g1) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(o_free);
+      }
+      const int64_t slab =
+          (int64_t)pc.slot * p.sk_units + (int64_t)pc.head * p.sk_q_tiles + pc.q;
+      float* po = p.part_o + (slab * HD + col0) * kBM + r;
+#pragma unroll
+      for (int e = 0; e < kHalf; ++e) po[e * kBM] = o[e];
+      if (w == 0) p.part_lse[slab * kBM + r] = l_fin > 0.f ? m_fin + __log2f(l_fin) : -INFINITY;
+      cw += my_tiles;
+    }
+  } else {
+    shrink();  // warp 11
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::kTmemCols);
+  }
+  if (threadIdx.x == 0) ATTN_TRACE(4);
+  if (p.num_splits == 1) launch_stamp_end(p.stamp);
+}
+
+// Merge every unit's per-piece partials (slot order, deterministic) and write
+// the bf16 output.  Grid (units, HD / 32): a CTA owns 32 columns of one unit;
+// the slot weights exp2(lse_s - max) of its 128 rows go to shared memory,
+// each thread then accumulates 16 columns of one row with the 16 loads of a
+// slot in flight together (the partials are column-major per unit, so a
+// warp's loads are coalesced), and the 128 x 32 bf16 tile leaves as 64-byte
+// row segments.
+template <int HD>
+__global__ void __launch_bounds__(256)
+    attn_sk_combine_kernel(const AttnParams p, int ctas) {
+  const int u = blockIdx.x;
+  const int c_base = blockIdx.y * 32;
+  const int head = u / p.sk_q_tiles, q = u - head * p.sk_q_tiles;
+  int ub = head * p.sk_tiles_head;
+  for (int k = 0; k < q; ++k) ub += unit_tiles(p, k);
+  const int tu = unit_tiles(p, q);
+  const int s0 = sk_owner(p, ub, ctas);
+  const int ns = sk_owner(p, ub + tu - 1, ctas) - s0 + 1;
+  __shared__ float wts[kMaxSkSlots][kBM];
+  __shared__ __align__(16) __nv_bfloat16 tile[kBM][32 + 8];
+  const int t = threadIdx.x;
+  if (t < kBM) {
+    float m = -INFINITY;
+    for (int s = 0; s < ns; ++s)
+      m = fmaxf(m, p.part_lse[((int64_t)s * p.sk_units + u) * kBM + t]);
+    float sum = 0.f;
+    for (int s = 0; s < ns; ++s) {
+      const float l = p.part_lse[((int64_t)s * p.sk_units + u) * kBM + t];
+      const float wt = (l == -INFINITY) ? 0.f : exp2f(l - m);
+      wts[s][t] = wt;
+      sum += wt;
+    }
+    const float inv = sum > 0.f ? 1.f / sum : 0.f;
+    for (int s = 0; s < ns; ++s) wts[s][t] *= inv;
+  }
+  __syncthreads();
+  const int r = t & (kBM - 1);
+  const int c0 = (t >> 7) * 16;
+  float acc[16] = {};
+  for (int s = 0; s < ns; ++s) {
+    const float wt = wts[s][r];
+    const float* src = p.part_o + (((int64_t)s * p.sk_units + u) * HD + c_base + c0) * kBM + r;
+    float v[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = src[e * kBM];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[e] = fmaf(wt, v[e], acc[e]);
+  }
+#pragma unroll
+  for (int e = 0; e < 16; ++e) tile[r][c0 + e] = __float2bfloat16(acc[e]);
+  __syncthreads();
+  const int pack = p.pack;
+  const int q_rows = pack > 1 ? p.n_new * pack : p.n_new;
+  const int rows_u = min(kBM, q_rows - q * kBM);
+  // 16 lanes x 4 bytes per row: a warp writes two rows per instruction
+  const int half = (t & 31) >> 4, l16 = t & 15;
+  for (int i = (t >> 5) * 2 + half; i < rows_u; i += 16) {
+    const int qi = q * kBM + i;
+    const int64_t row = pack > 1 ? (int64_t)(qi / pack) * p.hq + head * pack + qi % pack
+                                 : (int64_t)qi * p.hq + head;
+    *reinterpret_cast<uint32_t*>(p.out + row * HD + c_base + l16 * 2) =
+        *reinterpret_cast<const uint32_t*>(&tile[i][l16 * 2]);
+  }
+  if (p.stamp && t == 0) atomicMax(p.stamp + 1, gtimer());
+}
+
 // Deterministic split-KV combine: one warp per (query, head), splits in order.
 template <int HD>
 __global__ void __launch_bounds__(128)
@@ -702,10 +1256,25 @@ int gqa_pack(int hq, int hkv) {
 // SM at most (one wave), and at least 6 KV tiles per split so the per-CTA
 // prologue / epilogue and the combine pass stay amortised (r01e sweep:
 // (1000, 100, 40 heads) 20.5 us unsplit vs 23.5 us with 2 splits of 5 tiles).
+// Stream-K schedule (attn_sk_kernel) is opt-in: ASKV_ATTN_SK=1.  Measured at
+// the C3 shapes it loses to the (query tile, head[, split]) grid: its 148
+// CTAs each pay the ~8 us per-CTA prologue / epilogue for ~10 KV tiles and
+// the partials need a combine pass (profiles/r02_attn_stream_k.md).
+bool use_sk() {
+  static int knob = -1;
+  if (knob < 0) {
+    const char* e = getenv("ASKV_ATTN_SK");
+    knob = (e && e[0] == '1') ? 1 : 0;
+  }
+  return knob == 1;
+}
+
 int choose_splits(int n_cached, int n_new, int hq, int sms, int hkv = 0) {
   if (hkv <= 0) hkv = hq;
   const int pack = gqa_pack(hq, hkv);
   const int q_tiles = (n_new * pack + kBM - 1) / kBM;
+  // single-tile units: stream-K balances them over the SMs (one launch, no split)
+  if (use_sk() && !(pack == 1 && use_pairs(q_tiles, hq, sms))) return 1;
   const int q_groups =
       pack == 1 && use_pairs(q_tiles, hq, sms) ? (q_tiles + 1) / 2 : q_tiles;
   const int kv_tiles = (n_cached + n_new + kBN - 1) / kBN;
@@ -719,27 +1288,134 @@ int choose_splits(int n_cached, int n_new, int hq, int sms, int hkv = 0) {
   return best;
 }
 
+// Stream-K schedule on the host: the kernel's params, the CTA count and the
+// partial slots the most-cut unit needs.
+struct SkPlan {
+  int ctas = 0, max_slots = 0;
+};
+
+void sk_plan(AttnParams& prm, int hkv, int sms, SkPlan& out) {
+  const int q_rows = prm.pack > 1 ? prm.n_new * prm.pack : prm.n_new;
+  const int qt = (q_rows + kBM - 1) / kBM;
+  int per_head = 0;
+  for (int q = 0; q < qt; ++q) per_head += unit_tiles(prm, q);
+  const int heads = prm.pack > 1 ? hkv : prm.hq;
+  prm.sk_tiles_head = per_head;
+  prm.sk_q_tiles = qt;
+  prm.sk_units = qt * heads;
+  prm.sk_total = per_head * heads;
+  // at least ceil(T_max / (kMaxSkSlots - 1)) tiles per CTA so no unit is cut
+  // into more than kMaxSkSlots pieces
+  const int t_max = unit_tiles(prm, qt - 1);
+  const int min_per = (t_max + kMaxSkSlots - 2) / (kMaxSkSlots - 1);
+  const int cap = prm.sk_total / min_per;
+  static int knob = -1;   // ASKV_ATTN_SK_CTAS: CTA count override (measurement)
+  if (knob < 0) {
+    const char* e = getenv("ASKV_ATTN_SK_CTAS");
+    knob = e ? atoi(e) : 0;
+  }
+  if (knob > 0) sms = knob;
+  out.ctas = cap < sms ? (cap > 0 ? cap : 1) : sms;
+  out.max_slots = 1;
+  int ub = 0;
+  for (int h = 0; h < heads; ++h)
+    for (int q = 0; q < qt; ++q) {
+      const int tu = unit_tiles(prm, q);
+      const int ns = sk_owner(prm, ub + tu - 1, out.ctas) - sk_owner(prm, ub, out.ctas) + 1;
+      if (ns > out.max_slots) out.max_slots = ns;
+      ub += tu;
+    }
+}
+
+size_t sk_workspace(int n_cached, int n_new, int hq, int hkv, int head_dim) {
+  AttnParams prm{};
+  prm.n_new = n_new;
+  prm.n_cached = n_cached;
+  prm.hq = hq;
+  prm.group = hq / hkv;
+  prm.pack = gqa_pack(hq, hkv);
+  SkPlan plan;
+  sk_plan(prm, hkv, sm_count(), plan);
+  return (size_t)plan.max_slots * prm.sk_units * kBM * (head_dim + 1) * sizeof(float);
+}
+
+template <int HD>
+int launch_sk(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+              const CUtensorMap& mvs, AttnParams prm, int hkv, void* ws, size_t ws_bytes,
+              cudaStream_t stream) {
+  SkPlan plan;
+  sk_plan(prm, hkv, sm_count(), plan);
+  const size_t slab = (size_t)prm.sk_units * kBM;
+  const size_t need = (size_t)plan.max_slots * slab * (HD + 1) * sizeof(float);
+  ASKV_REQUIRE(ws != nullptr && ws_bytes >= need,
+               "prefill_attn: workspace %zu bytes < %zu needed (stream-K, %d slots)", ws_bytes,
+               need, plan.max_slots);
+  prm.part_o = static_cast<float*>(ws);
+  prm.part_lse = prm.part_o + (size_t)plan.max_slots * slab * HD;
+  prm.num_splits = 2;  // the combine stamps the launch end
+  auto kern = attn_sk_kernel<HD>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SkCfg<HD>::kSmemBytes);
+    if (e != cudaSuccess) return cuda_status(e, "attn_sk smem attribute");
+    attr = true;
+  }
+  kern<<<plan.ctas, SkCfg<HD>::kThreads, SkCfg<HD>::kSmemBytes, stream>>>(mq, mk, mv, mvs,
+                                                                          prm);
+  int rc = launch_status("attn_sk launch");
+  if (rc) return rc;
+  attn_sk_combine_kernel<HD><<<dim3(prm.sk_units, HD / 32), 256, 0, stream>>>(prm, plan.ctas);
+  return launch_status("attn_sk_combine launch");
+}
+
 template <int HD>
 int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cached, int n_new,
                 int hq, int hkv, float scale, void* out, void* ws, size_t ws_bytes,
-                int splits, cudaStream_t stream, unsigned long long* stamp) {
+                int splits, cudaStream_t stream, unsigned long long* stamp,
+                const VSource* vsrc) {
   const int rows = n_cached + n_new;
   const int pack = gqa_pack(hq, hkv);
-  CUtensorMap mq, mk, mv;
+  CUtensorMap mq, mk, mv, mvs;
   int rc = make_map(&mq, q, HD, hq, HD, n_new, (int64_t)hq * HD, pack);
   if (!rc) rc = make_map(&mk, kv, HD, hkv, HD, rows, kv_row_stride);
   if (!rc)
     rc = make_map(&mv, static_cast<const __nv_bfloat16*>(kv) + (int64_t)hkv * HD, HD, hkv, HD,
                   rows, kv_row_stride);
+  const bool use_vs = vsrc && vsrc->kind && vsrc->tiles > 0;
+  if (!rc && use_vs)
+    rc = make_map(&mvs, static_cast<const __nv_bfloat16*>(vsrc->base) + (int64_t)hkv * HD, HD,
+                  hkv, HD, vsrc->rows, vsrc->row_elems);
   if (rc) return rc;
+  if (!use_vs) mvs = mv;
+  auto set_vs = [&](AttnParams& a) {
+    a.v_src_tiles = use_vs ? vsrc->tiles : 0;
+    a.v_src_row0 = use_vs ? vsrc->row0 : 0;
+    a.v_blk_off = use_vs && vsrc->kind == 2 ? vsrc->blk_off : nullptr;
+    a.v_row_elems = use_vs ? vsrc->row_elems : 1;
+    a.v_layer_row = use_vs ? vsrc->layer_row : 0;
+  };
 
   const int q_tiles = (n_new * pack + kBM - 1) / kBM;
   const bool paired = pack == 1 && use_pairs(q_tiles, hq, sm_count());
   const int q_groups = paired ? (q_tiles + 1) / 2 : q_tiles;
   const int kv_tiles = (rows + kBN - 1) / kBN;
+  if (!paired && splits <= 1 && use_sk()) {
+    AttnParams prm{};
+    prm.n_new = n_new;
+    prm.n_cached = n_cached;
+    prm.hq = hq;
+    prm.group = hq / hkv;
+    prm.pack = pack;
+    prm.scale_log2 = scale * 1.4426950408889634f;
+    prm.out = static_cast<__nv_bfloat16*>(out);
+    prm.stamp = stamp;
+    set_vs(prm);
+    return launch_sk<HD>(mq, mk, mv, mvs, prm, hkv, ws, ws_bytes, stream);
+  }
   const int tps = (kv_tiles + splits - 1) / splits;
   splits = (kv_tiles + tps - 1) / tps;
-  AttnParams prm;
+  AttnParams prm{};
   prm.n_new = n_new;
   prm.n_cached = n_cached;
   prm.hq = hq;
@@ -752,6 +1428,7 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
   prm.stamp = stamp;
   prm.part_o = nullptr;
   prm.part_lse = nullptr;
+  set_vs(prm);
   if (splits > 1) {
     const size_t rows_qh = (size_t)n_new * hq;
     const size_t need = (size_t)splits * rows_qh * (HD + 1) * sizeof(float);
@@ -771,7 +1448,8 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
       if (e != cudaSuccess) return cuda_status(e, "attn smem attribute");
       attr = true;
     }
-    kern<<<grid, Cfg<HD, true>::kThreads, Cfg<HD, true>::kSmemBytes, stream>>>(mq, mk, mv, prm);
+    kern<<<grid, Cfg<HD, true>::kThreads, Cfg<HD, true>::kSmemBytes, stream>>>(mq, mk, mv, mvs,
+                                                                                prm);
   } else {
     auto kern = attn_fwd_kernel<HD, false>;
     static bool attr = false;
@@ -781,7 +1459,8 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
       if (e != cudaSuccess) return cuda_status(e, "attn smem attribute");
       attr = true;
     }
-    kern<<<grid, Cfg<HD, false>::kThreads, Cfg<HD, false>::kSmemBytes, stream>>>(mq, mk, mv, prm);
+    kern<<<grid, Cfg<HD, false>::kThreads, Cfg<HD, false>::kSmemBytes, stream>>>(mq, mk, mv,
+                                                                                 mvs, prm);
   }
   rc = launch_status("attn_fwd launch");
   if (rc || splits == 1) return rc;
@@ -809,12 +1488,30 @@ extern "C" int askv_attn_num_splits_gqa(int n_cached, int n_new, int n_heads, in
   return choose_splits(n_cached, n_new, n_heads, sms > 0 ? sms : sm_count(), n_kv_heads);
 }
 
+extern "C" size_t askv_attn_workspace_bytes_gqa(int n_cached, int n_new, int n_heads,
+                                                int n_kv_heads, int head_dim, int num_splits) {
+  if (n_new <= 0 || n_heads <= 0 || n_kv_heads <= 0 || n_heads % n_kv_heads) return 0;
+  const int s = num_splits > 0
+                    ? num_splits
+                    : choose_splits(n_cached, n_new, n_heads, sm_count(), n_kv_heads);
+  if (s > 1) return (size_t)s * n_new * n_heads * (head_dim + 1) * sizeof(float);
+  const int pack = gqa_pack(n_heads, n_kv_heads);
+  const int q_tiles = (n_new * pack + kBM - 1) / kBM;
+  if (!use_sk() || (pack == 1 && use_pairs(q_tiles, n_heads, sm_count()))) return 0;
+  return sk_workspace(n_cached, n_new, n_heads, n_kv_heads, head_dim);
+}
+
+// Without the kv-head count: the largest need over every GQA grouping of n_heads.
 extern "C" size_t askv_attn_workspace_bytes(int n_cached, int n_new, int n_heads,
                                             int head_dim, int num_splits) {
-  if (n_new <= 0 || n_heads <= 0) return 0;
-  const int s = num_splits > 0 ? num_splits : choose_splits(n_cached, n_new, n_heads, sm_count());
-  if (s <= 1) return 0;
-  return (size_t)s * n_new * n_heads * (head_dim + 1) * sizeof(float);
+  size_t best = 0;
+  for (int hkv = 1; hkv <= n_heads; ++hkv) {
+    if (n_heads % hkv) continue;
+    const size_t b =
+        askv_attn_workspace_bytes_gqa(n_cached, n_new, n_heads, hkv, head_dim, num_splits);
+    if (b > best) best = b;
+  }
+  return best;
 }
 
 extern "C" int askv_prefill_attn(const void* q, const void* kv, int64_t kv_row_stride,
@@ -831,7 +1528,7 @@ int askv::prefill_attn_stamped(const void* q, const void* kv, int64_t kv_row_str
                                int n_cached, int n_new, int n_heads, int n_kv_heads,
                                int head_dim, float scale, void* out, void* workspace,
                                size_t workspace_bytes, int num_splits, void* stream,
-                               unsigned long long* stamp) {
+                               unsigned long long* stamp, const VSource* vsrc) {
   ASKV_REQUIRE(n_cached >= 0 && n_new >= 0, "prefill_attn: negative lengths");
   ASKV_REQUIRE(n_heads > 0 && n_kv_heads > 0 && n_heads % n_kv_heads == 0,
                "prefill_attn: Hq=%d must be a positive multiple of Hkv=%d", n_heads,
@@ -849,7 +1546,8 @@ int askv::prefill_attn_stamped(const void* q, const void* kv, int64_t kv_row_str
                               : choose_splits(n_cached, n_new, n_heads, sm_count(), n_kv_heads);
   if (head_dim == 128)
     return launch_attn<128>(q, kv, kv_row_stride, n_cached, n_new, n_heads, n_kv_heads, scale,
-                            out, workspace, workspace_bytes, splits, (cudaStream_t)stream, stamp);
+                            out, workspace, workspace_bytes, splits, (cudaStream_t)stream, stamp,
+                            vsrc);
   return launch_attn<64>(q, kv, kv_row_stride, n_cached, n_new, n_heads, n_kv_heads, scale, out,
-                         workspace, workspace_bytes, splits, (cudaStream_t)stream, stamp);
+                         workspace, workspace_bytes, splits, (cudaStream_t)stream, stamp, vsrc);
 }

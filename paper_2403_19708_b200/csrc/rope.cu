@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kThreads)
                    int block_tokens, int64_t src_row_stride, int64_t first_token, int kept,
                    int hkv, const float* __restrict__ table, const int32_t* __restrict__ positions,
                    int pos0, __nv_bfloat16* __restrict__ dst, int64_t dst_row_stride,
-                   unsigned long long* __restrict__ stamp) {
+                   unsigned long long* __restrict__ stamp, int v_from) {
   constexpr int kHalf = HD / 2;
   constexpr int kUnitsPerHead = HD / 8;
   // optional launch timestamps {begin of CTA 0, max CTA end} (attention.cu)
@@ -134,7 +134,10 @@ __global__ void __launch_bounds__(kThreads)
   }
   __syncthreads();
   const int k_units = hkv * kUnitsPerHead;
-  const int row_units = 2 * k_units;
+  // rows below v_from: K only (their V is read by K3 straight from the
+  // source); v_from is a multiple of the 128-row KV tile, so a CTA's two rows
+  // are on the same side of it
+  const int row_units = row0 >= v_from ? 2 * k_units : k_units;
   const int total = nrows * row_units;
   // 13B: 2 rows x 1280 vectors = two rounds of 5 per thread; the row of a
   // vector is a compare (kReRows == 2), not an integer division (K2 was
@@ -284,14 +287,14 @@ extern "C" int askv_reembed(const void* src_base, const int64_t* src_block_off,
   return askv::reembed_stamped(src_base, src_block_off, block_tokens, src_row_stride,
                                first_token, kept, n_kv_heads, head_dim, rope_table,
                                table_positions, positions, pos0, dst, dst_row_stride, stream,
-                               nullptr);
+                               nullptr, 0);
 }
 
 int askv::reembed_stamped(const void* src_base, const int64_t* src_block_off, int block_tokens,
                           int64_t src_row_stride, int64_t first_token, int kept, int n_kv_heads,
                           int head_dim, const float* rope_table, int table_positions,
                           const int32_t* positions, int pos0, void* dst, int64_t dst_row_stride,
-                          void* stream, unsigned long long* stamp) {
+                          void* stream, unsigned long long* stamp, int v_from) {
   ASKV_REQUIRE(kept >= 0 && n_kv_heads > 0 && first_token >= 0 && pos0 >= 0,
                "reembed: bad kept=%d hkv=%d first_token=%lld pos0=%d", kept, n_kv_heads,
                (long long)first_token, pos0);
@@ -303,6 +306,7 @@ int askv::reembed_stamped(const void* src_base, const int64_t* src_block_off, in
                table_positions);
   ASKV_REQUIRE(src_row_stride % 8 == 0 && dst_row_stride % 8 == 0,
                "reembed: row strides must be multiples of 8 elements");
+  ASKV_REQUIRE(v_from >= 0 && v_from % 2 == 0, "reembed: v_from %d must be even", v_from);
   if (kept == 0) return ASKV_OK;
   ASKV_REQUIRE(src_base && dst && rope_table, "reembed: null pointer");
   const int grid = (kept + kReRows - 1) / kReRows;
@@ -311,11 +315,11 @@ int askv::reembed_stamped(const void* src_base, const int64_t* src_block_off, in
   if (head_dim == 128)
     reembed_kernel<128><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
         s, src_block_off, block_tokens, src_row_stride, first_token, kept, n_kv_heads,
-        rope_table, positions, pos0, d, dst_row_stride, stamp);
+        rope_table, positions, pos0, d, dst_row_stride, stamp, v_from);
   else
     reembed_kernel<64><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
         s, src_block_off, block_tokens, src_row_stride, first_token, kept, n_kv_heads,
-        rope_table, positions, pos0, d, dst_row_stride, stamp);
+        rope_table, positions, pos0, d, dst_row_stride, stamp, v_from);
   return launch_status("reembed launch");
 }
 

@@ -250,7 +250,9 @@ std::vector<int64_t> graph_key(const askv_prefill_plan* p, cudaStream_t s) {
           has(p->save_rows), has(p->ev_src_ready), has(p->ev_src_free), has(p->ev_save_free),
           has(p->ev_save_ready), p->stamps ? p->stamp_flags : -1, has(p->kv_layers),
           has(p->kv_alt), has(p->mirror_base), p->mirror_nblocks, p->promote_nblocks,
-          mirror_segs, promote_segs, (int64_t)(intptr_t)s};
+          mirror_segs, promote_segs, has(p->nccl_comm), p->nccl_comm ? p->tp_rank == 0 : -1,
+          p->src_rows > 0, p->head == 0,
+          (int64_t)(intptr_t)(p->nccl_comm), (int64_t)(intptr_t)s};
 }
 
 #define ASKV_TRY(expr)          \
@@ -448,6 +450,17 @@ extern "C" size_t askv_prefill_plan_size(void) { return sizeof(askv_prefill_plan
 
 static int issue_layers(const askv_prefill_plan* p, cudaStream_t s);
 
+// Row-parallel output projection + NCCL sum into the residual stream:
+// rank 0: x = x + in W^T (GEMM epilogue), then in-place all-reduce of x;
+// rank r > 0: h = in W^T, then all-reduce h -> x.  Every rank ends with
+// x + sum_r in_r W_r^T in x (one collective, no residual kernel).
+static int tp_out_proj(const askv_prefill_plan* p, const void* in, const void* w, int k, int n,
+                       int d, cudaStream_t s) {
+  const bool r0 = p->tp_rank == 0;
+  ASKV_TRY(gemm(in, w, r0 ? p->x : p->h, n, d, k, r0, p->gemm_ws, p->gemm_ws_bytes, s));
+  return tp_allreduce_bf16(r0 ? p->x : p->h, p->x, (int64_t)n * d, p->nccl_comm, s);
+}
+
 extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
   clear_error();
   ASKV_REQUIRE(p != nullptr, "prefill_layers: null plan");
@@ -573,7 +586,19 @@ static int issue_layers(const askv_prefill_plan* p, cudaStream_t s) {
     return reinterpret_cast<unsigned long long*>(p->stamps + idx);
   };
   const bool reemb = p->kept > 0 && p->src_kind != 0;
-  const bool ovl = p->kv_alt && !p->kv_layers && reemb && !p->promote_base && !p->allreduce;
+  const bool ovl = p->kv_alt && !p->kv_layers && reemb && !p->promote_base && !p->allreduce &&
+                   !p->nccl_comm;
+  // K3 reads the V of the kept rows' whole tiles from the pre-load source
+  // (ASKV_VSRC=0 turns it off: K2 then copies every V row, the round-1 path)
+  static int vsrc_knob = -1;
+  if (vsrc_knob < 0) {
+    const char* e = getenv("ASKV_VSRC");
+    vsrc_knob = (e && e[0] == '0') ? 0 : 1;
+  }
+  const bool vs_on = vsrc_knob && reemb && !p->kv_layers && !ovl && p->src_rows > 0 &&
+                     (p->src_kind == 1 ||
+                      (p->src_kind == 2 && p->head == 0 && p->block_tokens == 128));
+  const int vs_tiles = vs_on ? p->kept / 128 : 0;
   SideCtx* sc = ovl ? side_ctx(p->layers) : nullptr;
   if (ovl && !sc) {
     set_error("prefill_layers: side stream / events for the K2 overlap");
@@ -589,11 +614,12 @@ static int issue_layers(const askv_prefill_plan* p, cudaStream_t s) {
     if (p->src_kind == 1) {
       ASKV_TRY(reembed_stamped(p->src_layer[l], nullptr, 0, p->src_row_stride, p->head,
                                p->kept, hkv, hd, p->rope_table, p->rope_positions, nullptr, 0,
-                               kv_of(l), row, ks, k2_st));
+                               kv_of(l), row, ks, k2_st, vs_tiles * 128));
     } else {
       ASKV_TRY(reembed_stamped(p->src_layer[l], p->src_block_off, p->block_tokens,
                                p->src_row_stride, p->head, p->kept, hkv, hd, p->rope_table,
-                               p->rope_positions, nullptr, 0, kv_of(l), row, ks, k2_st));
+                               p->rope_positions, nullptr, 0, kv_of(l), row, ks, k2_st,
+                               vs_tiles * 128));
     }
     return ASKV_OK;
   };
@@ -648,13 +674,30 @@ static int issue_layers(const askv_prefill_plan* p, cudaStream_t s) {
                                  p->block_bytes, (int64_t)l * p->chunk_bytes, p->block_tokens,
                                  p->row_bytes, p->head, p->kept, src, s, nullptr));
       }
-      rec(p->ev_src_free, l, s);
+      if (!(vs_on && p->src_kind == 1)) rec(p->ev_src_free, l, s);
+    }
+    VSource vs;
+    if (vs_on) {
+      vs.kind = p->src_kind;
+      vs.tiles = vs_tiles;
+      vs.base = p->src_kind == 1 ? p->src_layer[l] : p->src_layer[0];
+      vs.rows = p->src_rows;
+      vs.row0 = p->head;
+      vs.blk_off = p->src_block_off;
+      vs.row_elems = p->src_row_stride;
+      vs.layer_row = (int64_t)l * p->block_tokens;
     }
     ASKV_TRY(prefill_attn_stamped(
         p->q_rot, kv, row, p->kept, n, hq, hkv, hd, p->attn_scale, p->attn_out, p->attn_ws,
         p->attn_ws_bytes, p->attn_splits, s,
-        (p->stamps && ((p->stamp_flags & 2) || (ovl && waits))) ? ts(st + 5) : nullptr));
-    if (p->allreduce) {  // tensor parallel: row-parallel W_o partial -> all-reduce -> residual
+        (p->stamps && ((p->stamp_flags & 2) || (ovl && waits))) ? ts(st + 5) : nullptr,
+        vs_on ? &vs : nullptr));
+    if (vs_on && p->src_kind == 1) rec(p->ev_src_free, l, s);  // K3 read V from the slot
+    if (p->nccl_comm) {
+      // tensor parallel over NCCL: x = x + sum_r partial_r, the residual folded
+      // into rank 0's GEMM epilogue, the sum landing in x on every rank
+      ASKV_TRY(tp_out_proj(p, p->attn_out, p->w_o[l], hq * hd, n, d, s));
+    } else if (p->allreduce) {  // row-parallel W_o partial -> callback all-reduce -> residual
       ASKV_TRY(gemm(p->attn_out, p->w_o[l], p->h, n, d, hq * hd, false, p->gemm_ws,
                     p->gemm_ws_bytes, s));
       p->allreduce(p->h, (int64_t)n * d, (void*)s, p->allreduce_ctx);
@@ -668,7 +711,9 @@ static int issue_layers(const askv_prefill_plan* p, cudaStream_t s) {
     ASKV_TRY(askv_rmsnorm(p->x, p->w_post[l], p->h, n, d, p->rms_eps, s));
     ASKV_TRY(gemm(p->h, p->w_gu[l], p->gu, n, 2 * f, d, false, p->gemm_ws, p->gemm_ws_bytes, s));
     ASKV_TRY(askv_silu_mul(p->gu, p->act, n, f, s));
-    if (p->allreduce) {
+    if (p->nccl_comm) {
+      ASKV_TRY(tp_out_proj(p, p->act, p->w_down[l], f, n, d, s));
+    } else if (p->allreduce) {
       ASKV_TRY(gemm(p->act, p->w_down[l], p->h, n, d, f, false, p->gemm_ws, p->gemm_ws_bytes,
                     s));
       p->allreduce(p->h, (int64_t)n * d, (void*)s, p->allreduce_ctx);

@@ -67,6 +67,56 @@ class NcclAllReduce:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
 
 
+class NcclComm:
+    """This rank's NCCL communicator over the tensor-parallel group, handed to
+    the native layer loop (askv_prefill_plan.nccl_comm): the W_o / W_down
+    all-reduces are issued from C++ on the compute stream and captured into
+    the layer graph -- no host callback per call (config C5).
+    Rank 0 draws the ncclUniqueId; it reaches the others through the default
+    torch.distributed group (any backend) unless `unique_id` is given."""
+
+    def __init__(self, rank: int, world: int, *, unique_id: bytes | None = None, group=None):
+        import ctypes as C
+
+        from . import _lib
+
+        lib = _lib.lib()
+        self.rank, self.world = int(rank), int(world)
+        if unique_id is None:
+            buf = (C.c_char * 128)()
+            if self.rank == 0:
+                _lib.check(lib.askv_nccl_unique_id(buf), "nccl_unique_id")
+            uid = [bytes(buf)]
+            if self.world > 1:
+                dist.broadcast_object_list(uid, src=0, group=group)
+            unique_id = uid[0]
+        if len(unique_id) != 128:
+            raise ValueError("ncclUniqueId is 128 bytes")
+        self._id = (C.c_char * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        _lib.check(lib.askv_nccl_comm_init(self.world, self.rank, self._id, C.byref(h)),
+                   "nccl_comm_init")
+        self.handle = h.value
+        self.native_comm = self
+
+    def __call__(self, t: torch.Tensor, stream) -> None:
+        """In-place bf16 sum of `t` over the group on `stream`."""
+        from . import _lib
+
+        if t.dtype != torch.bfloat16 or not t.is_contiguous():
+            raise ValueError("NcclComm sums contiguous bf16 tensors")
+        _lib.check(_lib.lib().askv_nccl_allreduce_bf16(t.data_ptr(), t.data_ptr(), t.numel(),
+                                                       self.handle, stream.cuda_stream),
+                   "nccl_allreduce")
+
+    def close(self) -> None:
+        from . import _lib
+
+        if self.handle:
+            _lib.check(_lib.lib().askv_nccl_comm_destroy(self.handle), "nccl_comm_destroy")
+            self.handle = None
+
+
 class ThreadAllReduce:
     """tp_reduce hook for a 1-GPU emulation of a TP group: one Python thread per
     rank, each driving its own Runner/streams; partials are summed on the GPU

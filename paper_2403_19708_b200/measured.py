@@ -79,6 +79,28 @@ def _merge(results) -> Timeline:
     return tl
 
 
+def _rebase(tl: Timeline, first, prestaged: int) -> Timeline:
+    """Start the job at its first activity: loads of layers >= `prestaged`
+    that the pre-loader began before the compute stream reached the job
+    (host issue latency) belong to the job, not to a head start -- with no
+    head start loading begins at t = 0 (overlap.py:91-93), so the measured
+    makespan and stall include that time.  `first`: the first chunk's load
+    intervals (one per layer)."""
+    late = [a for a, _ in first[prestaged:]]
+    start = min([0.0] + late)
+    if start >= 0.0:
+        return tl
+    sh = -start
+    mv = lambda iv: [(a + sh, b + sh) for a, b in iv]  # noqa: E731
+    tl.load_intervals = mv(tl.load_intervals)
+    tl.compute_intervals = mv(tl.compute_intervals)
+    tl.save_intervals = mv(tl.save_intervals)
+    tl.makespan += sh
+    tl.stall_total += sh
+    tl.max_gap = max(tl.max_gap, sh)
+    return tl
+
+
 class MeasuredExecutor:
     """plan_preload / plan_async_save on the real engine (one GPU).
 
@@ -106,6 +128,7 @@ class MeasuredExecutor:
         self.logits: dict[tuple, torch.Tensor] = {}
         self.disk_read_s = 0.0
         self.jobs = 0
+        self.prestaged_layers = 0     # sum over jobs of layers resident at start
 
     # ------------------------------------------------------------ token ids
     def _ids(self, sid: str, turn: int, kind: int, n: int) -> torch.Tensor:
@@ -134,6 +157,7 @@ class MeasuredExecutor:
         new_ids = self._ids(sid, job.turn_index, 0, turn_new)
         st.pinned.add(sid)
         disk_s = 0.0
+        k = 0
         try:
             if not self.save:
                 return self._recompute(sid, torch.cat([hist, new_ids]), job)
@@ -157,6 +181,7 @@ class MeasuredExecutor:
                     disk_s = time.perf_counter() - t0
                 k = head_start_layers(read_buffer, prev_job_running and disk_s == 0.0,
                                       context, eng.shape.row_bytes, eng.shape.layers)
+                self.prestaged_layers += k
                 self.kv.rows = 0
                 res, rows, _ = eng._prefill(sid, new_ids, context, self.want_logits,
                                             kv_cache=self.kv, prestage_layers=k)
@@ -171,6 +196,8 @@ class MeasuredExecutor:
         if self.want_logits:
             self.logits[(sid, job.turn_index)] = res[-1].logits
         tl = _merge(res)
+        if res and res[0].timeline.load_intervals:
+            tl = _rebase(tl, res[0].timeline.load_intervals, k)
         if disk_s:
             tl.load_intervals.insert(0, (0.0, disk_s))
             tl.load_intervals[1:] = [(a + disk_s, b + disk_s) for a, b in tl.load_intervals[1:]]
@@ -242,18 +269,33 @@ class MeasuredExecutor:
 
     # ------------------------------------------------------------ other shapes
     def _recompute(self, sid, ids, job) -> Timeline:
-        """Recompute comparator: one full-prompt prefill, nothing saved."""
+        """Recompute comparator: one full-prompt prefill, nothing saved.  A
+        prompt longer than the window (one turn of more new tokens than W:
+        the reference keeps 0 history and prefills them all, sim.py:473) runs
+        as the engine's chunked prefill with the rolling window, through a
+        scratch session whose rows are dropped afterwards."""
         eng = self.eng
-        r = eng.runner.run([Job(sid, ids, kept=0)], want_logits=self.want_logits)
-        torch.cuda.synchronize(eng.runner.device)
-        Runner.finalize(r)
-        eng.tokens[sid] = ids
+        if ids.numel() > eng.window:
+            tmp = "__recompute__"
+            eng.store.release_rows(tmp)
+            try:
+                r, _, _ = eng._prefill(tmp, ids, 0, self.want_logits)
+                torch.cuda.synchronize(eng.runner.device)
+                Runner.finalize(r)
+                eng.runner.fence(tmp)
+            finally:
+                eng.store.release_rows(tmp)
+        else:
+            r = eng.runner.run([Job(sid, ids, kept=0)], want_logits=self.want_logits)
+            torch.cuda.synchronize(eng.runner.device)
+            Runner.finalize(r)
+        tl = _merge(r)
         out = self._ids(sid, job.turn_index, 1, int(job.output_tokens))
         eng.tokens[sid] = torch.cat([ids, out])
-        self.jobs += 1
+        self.jobs += len(r)
         if self.want_logits:
-            self.logits[(sid, job.turn_index)] = r[0].logits
-        return r[0].timeline
+            self.logits[(sid, job.turn_index)] = r[-1].logits
+        return tl
 
     def _synthetic(self, hist: int, new: int, read_buffer: float,
                    prev_job_running: bool) -> Timeline:
@@ -289,7 +331,7 @@ class MeasuredExecutor:
             eng.runner.fence(sid)
         finally:
             st.release_rows(sid)
-        return r[0].timeline
+        return _rebase(r[0].timeline, r[0].timeline.load_intervals, k)
 
     def _load_only(self, hist: int) -> Timeline:
         from . import ops

@@ -110,8 +110,12 @@ def rope_new(qkv: torch.Tensor, n_new: int, n_heads: int, n_kv_heads: int, head_
 
 
 def attn_workspace_bytes(n_cached: int, n_new: int, n_heads: int, head_dim: int,
-                         num_splits: int = 0) -> int:
-    return int(lib().askv_attn_workspace_bytes(n_cached, n_new, n_heads, head_dim, num_splits))
+                         num_splits: int = 0, n_kv_heads: int | None = None) -> int:
+    if n_kv_heads is None:
+        return int(lib().askv_attn_workspace_bytes(n_cached, n_new, n_heads, head_dim,
+                                                   num_splits))
+    return int(lib().askv_attn_workspace_bytes_gqa(n_cached, n_new, n_heads, n_kv_heads,
+                                                   head_dim, num_splits))
 
 
 def attn_num_splits(n_cached: int, n_new: int, n_heads: int, sm_count: int = 0,

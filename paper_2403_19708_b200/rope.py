@@ -172,7 +172,7 @@ def attention_with_decoupled_cache(record: KvRecord, new_q, new_k, new_v, positi
     out = torch.empty((n, hq, d), dtype=torch.bfloat16, device=dev)
     splits = num_splits or ops.attn_num_splits(s, n, hq, n_kv_heads=hkv)
     ws = None
-    nbytes = ops.attn_workspace_bytes(s, n, hq, d, splits)
+    nbytes = ops.attn_workspace_bytes(s, n, hq, d, splits, n_kv_heads=hkv)
     if nbytes:
         ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     ops.prefill_attn(q_rot, kv, s, n, hq, hkv, d, out, ws, num_splits=splits,

@@ -373,9 +373,14 @@ class Runner:
         # over NVLink in a multi-GPU run; dist.ThreadAllReduce in the 1-GPU emulation).
         # The native loop calls back into it between the partial GEMM and the
         # residual add.
+        # A dist.NcclComm goes to the native loop as a communicator (ncclAllReduce
+        # on the compute stream, captured into the layer graph, residual folded
+        # into rank 0's GEMM epilogue); any other callable is a host callback.
         self.tp_reduce = tp_reduce
         self._cb_error = None
-        self._ar_cb = _lib.ALLREDUCE_FN(self._allreduce) if tp_reduce is not None else None
+        self._nccl = getattr(tp_reduce, "native_comm", None)
+        self._ar_cb = (_lib.ALLREDUCE_FN(self._allreduce)
+                       if tp_reduce is not None and self._nccl is None else None)
         self.launches = 0          # libaskv kernel launches issued (all streams)
         self.probe = None          # list -> (kind, ev0, ev1, work) per probed launch
 
@@ -682,7 +687,7 @@ class Runner:
             x = F.embedding(ids, self.w.embed)
             self._buf("h", n, s.d_model)
             splits = ops.attn_num_splits(kept, n, hq, n_kv_heads=hkv)
-            wsb = ops.attn_workspace_bytes(kept, n, hq, hd, splits)
+            wsb = ops.attn_workspace_bytes(kept, n, hq, hd, splits, n_kv_heads=hkv)
             ws = self._workspace(wsb) if wsb else None
 
             p = _lib.PrefillPlan()
@@ -720,6 +725,7 @@ class Runner:
                                                          self.row_bytes)
             if units is not None:
                 p.src_kind = 1
+                p.src_rows = self.slot_rows    # K3 reads the kept rows' V in the slot
                 p.src_layer = arr([self.slots[u.slot].data_ptr() for u in units])
                 p.ev_src_ready = arr([self._slot_ready[u.slot].handle for u in units])
                 p.ev_src_free = arr([self._slot_free[u.slot].handle for u in units])
@@ -735,6 +741,7 @@ class Runner:
             elif kept and job.source == "hbm":
                 p.src_kind = 2
                 base = self.hbm_arena.data_ptr()
+                p.src_rows = self.hbm_arena.numel() * 2 // self.row_bytes
                 p.src_layer = arr([base + l * self.chunk_bytes for l in range(L)])
                 p.src_block_off = job.dev_block_off.data_ptr()
             if job.save and job.mirror_block_ids is not None:
@@ -771,6 +778,8 @@ class Runner:
                                        attention_flops(kept, n, hq, hd)))
             if self._ar_cb is not None:
                 p.allreduce = self._ar_cb
+            elif self._nccl is not None:
+                p.nccl_comm, p.tp_rank = self._nccl.handle, self._nccl.rank
             p.graph = 1 if self.graph else 0
             self._cb_error = None
             _lib.check(_lib.lib().askv_prefill_layers(C.addressof(p), cs.cuda_stream),
@@ -782,7 +791,7 @@ class Runner:
                 n_stamps += 3
             self.launches += L * (4 + (1 if kept and job.source != "resident" else 0)
                                   + (2 if splits > 1 else 1)
-                                  + (2 if self.tp_reduce is not None else 0)) + n_stamps
+                                  + (2 if self._ar_cb is not None else 0)) + n_stamps
             if units is not None:
                 for u in units:
                     self._release(u)

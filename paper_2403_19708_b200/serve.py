@@ -92,11 +92,13 @@ def run(args) -> dict:
     # and of its append before save() trims (2 windows of blocks)
     spare = 2 * (-(-(shape.context_window + 4096) // tb))
     host_blocks = dram // bb + spare
+    from . import numa
+    node = numa.gpu_numa_node(args.device) if args.numa_node < 0 else args.numa_node
     t_alloc = time.perf_counter()
     eng = E.Engine(shape, host_blocks=host_blocks, block_tokens=tb, device=dev, seed=0,
                    read_buffer_bytes=rb, max_new=4096, dram_bytes=dram,
                    autotune=True if args.autotune < 0 else args.autotune, policy=PolicyConfig(),
-                   numa_node=args.numa_node)
+                   numa_node=node)
     t_alloc = time.perf_counter() - t_alloc
     tiers = model.TierConfig(hbm_read_buffer=rb, hbm_write_buffer=int(2e9),
                              dram_capacity=eng.store.mem_capacity, disk_capacity=0,
@@ -108,6 +110,7 @@ def run(args) -> dict:
            "dram_bytes": eng.store.mem_capacity, "read_buffer_bytes": rb,
            "block_tokens": tb, "batch_size": args.batch_size,
            "decode_s_per_step": args.decode_s_per_step, "setup_s": t_alloc,
+           "numa_node": eng.arena.numa_node,
            "data": "synthetic: reference generator sessions, random-init weights, random ids"}
     modes = ["reuse", "recompute"] if not args.reuse_only else ["reuse"]
     for mode in modes:
@@ -133,6 +136,7 @@ def run(args) -> dict:
                      "prompt": t.prompt_tokens, "new": t.new_tokens, "ttft": t.ttft_s,
                      "prefill": t.prefill_s, "stall": t.stall_s} for t in log.turns]
         out[mode] = s
+    eng.runner.close()
     if "recompute" in out:
         r, c = out["reuse"], out["recompute"]
         out["speedup_p50_ttft"] = c["p50_ttft_s"] / r["p50_ttft_s"] if r["p50_ttft_s"] else None
@@ -156,7 +160,8 @@ def parse(argv=None):
     ap.add_argument("--batch-size", type=int, default=24)
     ap.add_argument("--prefill-s-per-token", type=float, default=1.92e-4)
     ap.add_argument("--decode-s-per-step", type=float, default=1.0e-3)
-    ap.add_argument("--numa-node", type=int, default=None)
+    ap.add_argument("--numa-node", type=int, default=-1,
+                    help="arena NUMA node (-1: the GPU's own node when the host reports one)")
     ap.add_argument("--autotune", type=int, default=-1,
                     help="GEMM autotune up to this many rows (0 = off, -1 = every "
                          "prompt length the run can see)")

@@ -2,6 +2,8 @@
 declares; the ctypes signature table covers exactly those symbols."""
 
 import ctypes
+import json
+import os
 import re
 from pathlib import Path
 
@@ -45,6 +47,27 @@ def test_ctypes_table_matches_header(built):
     assert ctypes.sizeof(_lib.PrefillPlan) == lib.askv_prefill_plan_size()
 
 
+def _sk_slots(n_cached, n_new, hq, hkv, sms=148, bm=128, bn=128):
+    """Python restatement of K3's stream-K schedule (csrc/attention.cu sk_plan):
+    (units, max partial slots of a unit)."""
+    pack = hq // hkv if hq > hkv and 128 % (hq // hkv) == 0 and hq // hkv <= 16 else 1
+    q_rows = n_new * pack
+    qt = -(-q_rows // bm)
+    tiles = [-(-(n_cached + (min((q + 1) * bm, q_rows) - 1) // pack + 1) // bn)
+             for q in range(qt)]
+    heads = hkv if pack > 1 else hq
+    units = [(h, q, t) for h in range(heads) for q, t in enumerate(tiles)]
+    total = sum(t for *_, t in units)
+    min_per = -(-max(tiles) // 23)
+    ctas = max(1, min(sms, total // min_per))
+    owner = lambda g: ((g + 1) * ctas - 1) // total  # noqa: E731
+    slots, ub = 1, 0
+    for h, q, t in units:
+        slots = max(slots, owner(ub + t - 1) - owner(ub) + 1)
+        ub += t
+    return len(units), slots
+
+
 def test_split_policy_without_gpu(built):
     from paper_2403_19708_b200 import _lib
     lib = _lib.lib()
@@ -59,6 +82,31 @@ def test_split_policy_without_gpu(built):
     # full recompute of 2379 tokens fills the machine without splitting
     assert lib.askv_attn_num_splits(0, 2379, 40, 148) == 1
     assert lib.askv_attn_workspace_bytes(2142, 237, 40, 128, 4) == 4 * 237 * 40 * 129 * 4
+
+
+def test_stream_k_schedule_without_gpu(built):
+    """Opt-in stream-K schedule (ASKV_ATTN_SK=1, read once per process): one
+    launch, no uniform split; its partial slabs are slots x units x 128 rows x
+    (d + 1) fp32 with the slot count of the python restatement (148 SMs when no
+    GPU is visible)."""
+    import subprocess
+    import sys
+    cases = [(2142, 237, 40, 40), (2142, 100, 40, 40), (2869, 301, 8, 1), (1000, 60, 2, 2),
+             (100, 5, 4, 4), (4000, 90, 1, 1)]
+    code = ("import sys, json; sys.path.insert(0, %r)\n"
+            "from paper_2403_19708_b200 import _lib\n"
+            "lib = _lib.lib()\n"
+            "print(json.dumps([[lib.askv_attn_num_splits_gqa(k, n, h, v, 148),"
+            " lib.askv_attn_workspace_bytes_gqa(k, n, h, v, 128, 0)] for k, n, h, v in %r]))"
+            % (str(Path(__file__).resolve().parent.parent), cases))
+    env = dict(os.environ, ASKV_ATTN_SK="1")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         check=True).stdout
+    got = json.loads(out.strip().splitlines()[-1])
+    for (kept, n, hq, hkv), (splits, ws) in zip(cases, got):
+        units, slots = _sk_slots(kept, n, hq, hkv)
+        assert splits == 1
+        assert ws == slots * units * 128 * 129 * 4, (kept, n)
 
 
 def test_argument_errors_without_gpu(built):
@@ -91,7 +139,7 @@ def test_attention_kernel_does_not_spill(built):
             name = m.group(1)
             continue
         m = re.search(r"STACK:(\d+)", line)
-        if m and name and "attn_fwd_kernel" in name:
+        if m and name and ("attn_fwd_kernel" in name or "attn_sk_kernel" in name):
             stacks[name] = int(m.group(1))
-    assert len(stacks) == 4, stacks  # HD 64 / 128 x unpaired / paired
+    assert len(stacks) == 6, stacks  # HD 64 / 128 x unpaired / paired / stream-K
     assert max(stacks.values()) <= 16, stacks

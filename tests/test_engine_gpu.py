@@ -268,6 +268,76 @@ def test_tensor_parallel_emulation_gqa_matches_oracle():
         seq = np.concatenate([seq, o.numpy()])
 
 
+def test_native_nccl_allreduce_in_layer_graph():
+    """Config C5's collective issued natively: a dist.NcclComm hands the NCCL
+    communicator to the layer loop, which runs ncclAllReduce on the compute
+    stream inside the captured layer graph with the residual folded into rank
+    0's GEMM epilogue.  On one GPU the group has one rank, so the sum is the
+    identity and every turn must be bit-identical to the engine without TP --
+    and match the float64 oracle."""
+    engine, model, runner = _mods()
+    from dataclasses import replace
+    from paper_2403_19708_b200.dist import NcclComm
+    shape = replace(model.shape("tiny"), n_heads=8, n_kv_heads=1)
+    w = runner.LlamaWeights(shape, seed=11)
+    comm = NcclComm(0, 1)
+    try:
+        tp = engine.Engine(shape, host_blocks=32, block_tokens=16, weights=w, max_new=64,
+                           read_buffer_bytes=16 << 20, tp_reduce=comm, autotune=False)
+        ref = engine.Engine(shape, host_blocks=32, block_tokens=16, weights=w, max_new=64,
+                            read_buffer_bytes=16 << 20, autotune=False)
+        assert tp.runner._nccl is comm and tp.runner._ar_cb is None and tp.runner.graph
+        wnp = w.to_numpy()
+        rng = np.random.default_rng(11)
+        seq = np.zeros(0, dtype=np.int64)
+        for k in range(3):
+            n = torch.as_tensor(rng.integers(0, shape.vocab, 30))
+            o = torch.as_tensor(rng.integers(0, shape.vocab, 7))
+            a = tp.turn("s", k, n, o, want_logits=True)
+            b = ref.turn("s", k, n, o, want_logits=True)
+            torch.cuda.synchronize()
+            ga, gb = a.result.logits.cpu(), b.result.logits.cpu()
+            assert torch.equal(ga, gb), k
+            seq = np.concatenate([seq, n.numpy()])
+            assert rope_ref.rel_err(ga.double().numpy(), oracle_logits(wnp, shape, seq)) \
+                <= LOGIT_TOL
+            seq = np.concatenate([seq, o.numpy()])
+    finally:
+        comm.close()
+
+
+def test_k3_reads_v_from_the_preload_source():
+    """K2 moves K only for the kept rows' whole 128-row tiles and K3 reads
+    their V where the pre-loader left them: the read-buffer slot (host turns)
+    or the HBM-tier blocks (tier hits, block_tokens 128 = one KV tile per
+    block).  Multi-turn logits match the float64 oracle of the whole
+    conversation on both sources."""
+    engine, model, runner = _mods()
+    from dataclasses import replace
+    shape = replace(model.shape("tiny"), context_window=4096)
+    w = runner.LlamaWeights(shape, seed=13)
+    eng = engine.Engine(shape, host_blocks=16, block_tokens=128, weights=w, max_new=512,
+                        read_buffer_bytes=64 << 20, hbm_blocks=8, autotune=False)
+    wnp = w.to_numpy()
+    rng = np.random.default_rng(13)
+    seq = np.zeros(0, dtype=np.int64)
+    sources = []
+    for k, (nn, no) in enumerate([(300, 40), (90, 30), (150, 20), (70, 10)]):
+        n = torch.as_tensor(rng.integers(0, shape.vocab, nn))
+        o = torch.as_tensor(rng.integers(0, shape.vocab, no))
+        hits_before = eng.hbm.hits
+        out = eng.turn("s", k, n, o, want_logits=True)
+        torch.cuda.synchronize()
+        sources.append("hbm" if eng.hbm.hits > hits_before else
+                       ("host" if out.kept else "none"))
+        seq = np.concatenate([seq, n.numpy()])
+        got = out.result.logits.cpu().double().numpy()
+        assert rope_ref.rel_err(got, oracle_logits(wnp, shape, seq)) <= LOGIT_TOL, k
+        seq = np.concatenate([seq, o.numpy()])
+    assert sources[0] == "none" and "hbm" in sources
+    assert all(s != "none" for s in sources[1:])
+
+
 def test_hbm_tier_is_bit_identical_to_host_path():
     """HBM session tier: the same multi-turn session with
     truncation served from the HBM mirror gives bit-identical logits to the

@@ -11,6 +11,7 @@ Tolerances (stated here and in DESIGN.md §Parity):
 """
 
 import math
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -201,6 +202,59 @@ def test_attention_splits_agree():
         outs.append(f64(out))
     for o in outs[1:]:
         assert np.abs(o - outs[0]).max() <= 4e-3
+
+
+SK_CASES = [
+    (2142, 237, 40, 40),   # C3 p50: 80 units cut into 148 equal ranges
+    (2869, 301, 40, 40),   # 45-row tail tiles
+    (2048, 256, 8, 1),     # GQA-packed units
+    (200, 40, 2, 2),       # fewer KV tiles than SMs: one tile per CTA
+    (0, 129, 3, 3),        # no cache, 1-row tail
+]
+
+
+def _stream_k_check(n_cached, n_new, hq, hkv):
+    """Stream-K (units cut across CTAs, partials merged in slot order) vs the
+    oracle and vs the uniform split path; returns (rel, max_abs, max diff)."""
+    ops = _ops()
+    d = 128
+    seed = 7 * n_cached + n_new
+    q = bf16_rand(n_new, hq, d, seed=seed).to(DEV)
+    kv = bf16_rand(n_cached + n_new, 2, hkv, d, seed=seed + 1).to(DEV)
+    outs = []
+    for s in (1, 2):
+        out = torch.empty((n_new, hq, d), dtype=torch.bfloat16, device=DEV)
+        ws = torch.empty(max(1, ops.attn_workspace_bytes(n_cached, n_new, hq, d, s,
+                                                         n_kv_heads=hkv)),
+                         dtype=torch.uint8, device=DEV)
+        ops.prefill_attn(q, kv, n_cached, n_new, hq, hkv, d, out, ws, num_splits=s)
+        torch.cuda.synchronize()
+        outs.append(f64(out))
+    want = oracle_attention(q, kv, n_cached, n_new, hq, hkv)
+    assert np.isfinite(outs[0]).all()
+    return (rope_ref.rel_err(outs[0], want), float(np.abs(outs[0] - want).max()),
+            float(np.abs(outs[0] - outs[1]).max()))
+
+
+def test_attention_stream_k_schedule_matches_oracle():
+    """The opt-in stream-K schedule (ASKV_ATTN_SK=1, read once per process, so
+    it runs in a child process) gives the oracle's result and agrees with the
+    uniform split path."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = str(Path(__file__).resolve().parent.parent)
+    code = ("import sys, json; sys.path[:0] = [%r, %r]\n"
+            "import test_kernels_gpu as t\n"
+            "print(json.dumps([t._stream_k_check(*c) for c in t.SK_CASES]))"
+            % (root, root + "/tests"))
+    env = dict(os.environ, ASKV_ATTN_SK="1")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    for case, (rel, mx, diff) in zip(SK_CASES, json.loads(out.stdout.strip().splitlines()[-1])):
+        assert rel <= 5e-3 and mx <= 1.5e-2 and diff <= 4e-3, (case, rel, mx, diff)
 
 
 def test_attention_deterministic():

@@ -152,3 +152,46 @@ def test_victim_ranking_matches_reference_key():
         order.append(v)
         st.remove(v)
     assert order == ["cold", "warm", "q3", "q2", "q1", "q0"]
+
+
+@pytest.mark.skipif(not Path("/root/reference/pkg/src/kvsim").exists(),
+                    reason="reference package not present (GPU box)")
+def test_planner_dropin_rebinds_into_the_reference_simulator():
+    """overlap.plan_preload / plan_async_save have the reference signatures:
+    rebinding kvsim.sim's planners to them (bound here to the analytical
+    executor; on a GPU to measured.MeasuredExecutor) leaves the reference
+    simulator's C1 event log unchanged."""
+    import sys
+
+    sys.path.insert(0, "/root/reference/pkg/src")
+    try:
+        import kvsim.model as kmodel
+        import kvsim.sim as ksim
+        import kvsim.trace as ktrace
+    finally:
+        sys.path.remove("/root/reference/pkg/src")
+    from paper_2403_19708_b200 import overlap
+
+    wl_raw = json.loads((G / "workload_c1.json").read_text())
+    sessions = [ktrace.Session(s["id"], [ktrace.Turn(a, b) for a, b in s["turns"]],
+                               list(s["arrivals"])) for s in wl_raw["sessions"]]
+    wl = ktrace.Workload(sessions)
+    prof = kmodel.builtin_profile("llama-13b")
+    cfg = ksim.SimConfig(profile=prof)
+
+    def events():
+        return [(e.time, e.kind.name, e.session_id, e.turn_index)
+                for e in ksim.run(wl, cfg).events]
+
+    want = events()
+    orig = ksim.plan_preload, ksim.plan_async_save
+    overlap.bind(ModeledExecutor())
+    try:
+        ksim.plan_preload, ksim.plan_async_save = overlap.plan_preload, overlap.plan_async_save
+        got = events()
+    finally:
+        ksim.plan_preload, ksim.plan_async_save = orig
+        overlap.bind(None)
+    assert len(got) == len(want) > 0
+    for g, w in zip(got, want):
+        assert g[1:] == w[1:] and _close(g[0], w[0])

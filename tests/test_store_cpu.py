@@ -266,3 +266,38 @@ def test_hbm_tier_block_reuse_is_fenced():
     # and the session is dropped from the tier
     assert not tier.sync("d", [40, 41], 0, {"b", "c"})
     assert "d" not in tier.tab
+
+
+def test_arena_allocator_runs_and_no_double_allocation():
+    """HostArena hands out contiguous runs (a session's growth continues its
+    last block when free) and never gives out a block twice."""
+    import random
+
+    from paper_2403_19708_b200.store import CapacityError, HostArena
+    a = HostArena(64, 8, pin=False)
+    x = a.alloc(10)
+    assert x == list(range(10))
+    y = a.alloc(4, after=x[-1])
+    assert y == list(range(10, 14))
+    a.release(x[:5])
+    z = a.alloc(6)              # the freed 5-run is too short: first run of 6
+    assert z == list(range(14, 20))
+    rng = random.Random(3)
+    held = {"x": x[5:], "y": y, "z": z}
+    for step in range(400):
+        k = rng.choice("abcdefgh")
+        if k in held and rng.random() < 0.5:
+            a.release(held.pop(k))
+        else:
+            n = rng.randint(1, 6)
+            try:
+                got = a.alloc(n, after=held[k][-1] if held.get(k) else None)
+            except CapacityError:
+                continue
+            held.setdefault(k, []).extend(got)
+        used = [b for v in held.values() for b in v]
+        assert len(used) == len(set(used)) and a.free_blocks == 64 - len(used)
+    with pytest.raises(ValueError):
+        b = held[next(iter(held))][0]
+        a.release([b])
+        a.release([b])

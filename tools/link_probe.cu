@@ -1,11 +1,15 @@
-// Probe: pinned-host <-> HBM link throughput for the pre-loader's DMA shapes.
+// Probe: pinned-host <-> HBM link throughput for the pre-loader's / saver's
+// DMA shapes (K1 / K4 rooflines).
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o tools/link_probe tools/link_probe.cu
 //   tools/link_probe
 //
-// Cases: one H2D stream issuing 2.6 MB chunks (a (block, layer) chunk of a
-// 13B session) as cudaMemcpyAsync or strided 2-D copies; 2 / 4 concurrent H2D streams;
-// H2D with a concurrent D2H stream; 64 MB chunks.  Diagnostics only.
+// The source is laid out like the host arena: 2.6 MB (block, layer) chunks
+// `kStride` chunks apart (a block holds every layer).  Cases: one chunk per
+// cudaMemcpyAsync on 1 / 2 / 4 round-robin streams; runs of 23 consecutive
+// blocks as one strided cudaMemcpy2DAsync; one 64 MB copy; each with and
+// without a concurrent 2 GB D2H; and the concurrent bidirectional pair
+// (H2D + D2H rates measured together: the K4 roofline while K1 streams).
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -20,6 +24,9 @@
     }                                                                           \
   } while (0)
 
+constexpr size_t kChunk = 2621440;  // 128 tokens x 20 KB (13B row)
+constexpr int kStride = 8;          // chunks between consecutive blocks' same layer
+
 int main() {
   const size_t bytes = 2ull << 30;
   char *h, *d, *h2, *d2;
@@ -30,37 +37,51 @@ int main() {
   cudaStream_t st[4], sd;
   for (auto& s : st) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
-  cudaEvent_t a, b;
+  cudaEvent_t a, b, da, db;
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
-  auto run = [&](const char* name, int nstreams, size_t chunk, bool batch, bool d2h) -> int {
-    const size_t n = bytes / chunk;
+  CK(cudaEventCreate(&da));
+  CK(cudaEventCreate(&db));
+  const size_t n = bytes / kChunk;          // chunks moved per pass
+  const size_t blocks = n / kStride;        // blocks in the source
+  // mode 0: one memcpy per chunk; 1: 2-D runs of 23 blocks; 2: 64 MB copies
+  auto run = [&](const char* name, int nstreams, int mode, bool d2h) -> int {
+    float best = 0.f, best_d = 0.f;
     for (int rep = 0; rep < 3; ++rep) {
       CK(cudaDeviceSynchronize());
       CK(cudaEventRecord(a, 0));
       for (int k = 0; k < nstreams; ++k) CK(cudaStreamWaitEvent(st[k], a, 0));
       CK(cudaStreamWaitEvent(sd, a, 0));
-      if (d2h) CK(cudaMemcpyAsync(h2, d2, bytes, cudaMemcpyDeviceToHost, sd));
-      for (int k = 0; k < nstreams; ++k) {
-        std::vector<void*> ds, ss;
-        std::vector<size_t> sz;
-        for (size_t i = k; i < n; i += nstreams) {
-          ds.push_back(d + i * chunk);
-          ss.push_back(h + i * chunk);
-          sz.push_back(chunk);
-        }
-        if (batch) {
-          // strided 2-D copies of 23 chunks = one (session, layer) pre-load
-          // of consecutive arena blocks (the pre-loader's strided form)
-          for (size_t i = 0; i < ds.size(); i += 23) {
-            const size_t m = ds.size() - i < 23 ? ds.size() - i : 23;
-            const size_t sp = m > 1 ? (size_t)((char*)ss[i + 1] - (char*)ss[i]) : chunk;
-            const size_t dp = m > 1 ? (size_t)((char*)ds[i + 1] - (char*)ds[i]) : chunk;
-            CK(cudaMemcpy2DAsync(ds[i], dp, ss[i], sp, chunk, m, cudaMemcpyHostToDevice, st[k]));
+      if (d2h) {
+        CK(cudaEventRecord(da, sd));
+        CK(cudaMemcpyAsync(h2, d2, bytes, cudaMemcpyDeviceToHost, sd));
+        CK(cudaEventRecord(db, sd));
+      }
+      size_t moved = 0;
+      int rr = 0;
+      for (int layer = 0; layer < kStride; ++layer) {  // one pass per layer offset
+        if (mode == 2) {
+          const size_t big = 64 << 20;
+          for (size_t off = 0; off + big <= bytes / kStride; off += big, ++rr) {
+            CK(cudaMemcpyAsync(d + layer * (bytes / kStride) + off,
+                               h + layer * (bytes / kStride) + off, big,
+                               cudaMemcpyHostToDevice, st[rr % nstreams]));
+            moved += big;
           }
-        } else {
-          for (size_t i = 0; i < ds.size(); ++i)
-            CK(cudaMemcpyAsync(ds[i], ss[i], chunk, cudaMemcpyHostToDevice, st[k]));
+          continue;
+        }
+        for (size_t blk = 0; blk < blocks;) {
+          const size_t m = mode == 1 ? (blocks - blk < 23 ? blocks - blk : 23) : 1;
+          char* dst = d + (layer * blocks + blk) * kChunk;
+          const char* src = h + (blk * kStride + layer) * kChunk;
+          if (m == 1)
+            CK(cudaMemcpyAsync(dst, src, kChunk, cudaMemcpyHostToDevice, st[rr % nstreams]));
+          else
+            CK(cudaMemcpy2DAsync(dst, kChunk, src, kStride * kChunk, kChunk, m,
+                                 cudaMemcpyHostToDevice, st[rr % nstreams]));
+          ++rr;
+          blk += m;
+          moved += m * kChunk;
         }
       }
       for (int k = 0; k < nstreams; ++k) {
@@ -72,20 +93,33 @@ int main() {
       }
       CK(cudaEventRecord(b, 0));
       CK(cudaEventSynchronize(b));
+      if (d2h) CK(cudaEventSynchronize(db));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, a, b));
+      const float gbs = moved / (ms * 1e-3f) / 1e9f;
+      if (gbs > best) best = gbs;
+      if (d2h) {
+        CK(cudaEventElapsedTime(&ms, da, db));
+        const float g2 = bytes / (ms * 1e-3f) / 1e9f;
+        if (g2 > best_d) best_d = g2;
+      }
     }
-    float ms;
-    CK(cudaEventElapsedTime(&ms, a, b));
-    printf("%-44s H2D %6.1f GB/s\n", name, (n * chunk) / (ms * 1e-3) / 1e9);
+    if (d2h)
+      printf("%-46s H2D %6.1f GB/s   concurrent D2H %6.1f GB/s\n", name, best, best_d);
+    else
+      printf("%-46s H2D %6.1f GB/s\n", name, best);
     return 0;
   };
-  if (run("1 stream, 2.6 MB memcpy", 1, 2621440, false, false)) return 1;
-  if (run("1 stream, 2.6 MB x23 2-D", 1, 2621440, true, false)) return 1;
-  if (run("2 streams, 2.6 MB x23 2-D", 2, 2621440, true, false)) return 1;
-  if (run("4 streams, 2.6 MB x23 2-D", 4, 2621440, true, false)) return 1;
-  if (run("1 stream, 64 MB memcpy", 1, 64 << 20, false, false)) return 1;
-  if (run("1 stream, 2.6 MB x23 2-D + 2 GB D2H", 1, 2621440, true, true)) return 1;
-  if (run("2 streams, 2.6 MB x23 2-D + 2 GB D2H", 2, 2621440, true, true)) return 1;
-  // D2H alone
+  if (run("1 stream, 2.6 MB chunk per memcpy", 1, 0, false)) return 1;
+  if (run("2 streams, 2.6 MB chunk per memcpy", 2, 0, false)) return 1;
+  if (run("4 streams, 2.6 MB chunk per memcpy", 4, 0, false)) return 1;
+  if (run("1 stream, 23-block 2-D runs", 1, 1, false)) return 1;
+  if (run("2 streams, 23-block 2-D runs", 2, 1, false)) return 1;
+  if (run("1 stream, 64 MB memcpy", 1, 2, false)) return 1;
+  if (run("1 stream, 2.6 MB chunk per memcpy + D2H", 1, 0, true)) return 1;
+  if (run("2 streams, 2.6 MB chunk per memcpy + D2H", 2, 0, true)) return 1;
+  if (run("1 stream, 23-block 2-D runs + D2H", 1, 1, true)) return 1;
+  if (run("1 stream, 64 MB memcpy + D2H", 1, 2, true)) return 1;
   {
     CK(cudaDeviceSynchronize());
     CK(cudaEventRecord(a, sd));
@@ -94,7 +128,7 @@ int main() {
     CK(cudaEventSynchronize(b));
     float ms;
     CK(cudaEventElapsedTime(&ms, a, b));
-    printf("%-44s D2H %6.1f GB/s\n", "1 stream, 2 GB", bytes / (ms * 1e-3) / 1e9);
+    printf("%-46s D2H %6.1f GB/s\n", "1 stream, 2 GB D2H alone", bytes / (ms * 1e-3) / 1e9);
   }
   return 0;
 }
