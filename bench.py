@@ -65,6 +65,8 @@ def parse():
                          "instead of the allocator's contiguous runs")
     ap.add_argument("--serve-dram-gb", type=float, default=96.0,
                     help="host DRAM of the measured serving replay (0 = skip it)")
+    ap.add_argument("--serve-hbm-gb", type=float, default=64.0,
+                    help="HBM session tier of the serving replay's third mode (0 = off)")
     ap.add_argument("--disk-dir", default="/tmp",
                     help="directory for the disk-tier probe ('none' = skip)")
     ap.add_argument("--decode-steps", type=int, default=32,
@@ -303,7 +305,8 @@ def run_serving(args, rank: int, device: int) -> dict:
 
     from paper_2403_19708_b200 import serve
     sa = serve.parse(["--config", args.config, "--shard", str(rank), "--of", "8",
-                      "--device", str(device), "--dram-gb", str(args.serve_dram_gb)])
+                      "--device", str(device), "--dram-gb", str(args.serve_dram_gb),
+                      "--hbm-gb", str(args.serve_hbm_gb)])
     t0 = time.perf_counter()
     out = serve.run(sa)
     out["wall_s"] = time.perf_counter() - t0
@@ -324,6 +327,12 @@ def run_serving(args, rank: int, device: int) -> dict:
             "exposed_transfer_frac": r["exposed_transfer_frac"],
             "hit_rate": r["overall_hit_rate"], "evict_out": r["evict_out"],
             "hits_with_head_start": r["hits_with_head_start"], "h2d_gbs": r["h2d_gbs"],
+            "hbm_tier": ({"gb": out["hbm_tier_bytes"] / 1e9,
+                          "p50_ttft_s": out["reuse_hbm_tier"]["p50_ttft_s"],
+                          "speedup_p50_ttft": out.get("speedup_p50_ttft_hbm_tier"),
+                          "exposed_transfer_frac": out["reuse_hbm_tier"]["exposed_transfer_frac"],
+                          "tier_hits": out["reuse_hbm_tier"]["tier_hits"]}
+                         if "reuse_hbm_tier" in out else None),
             "by_hit_class": r["by_hit_class"], "wall_s": out["wall_s"],
             "note": "queue-inclusive TTFT (sim.py:489) with every prefill measured on this "
                     "GPU; read-buffer head start min(S_buf, B*wait) from real queue waits; "
@@ -805,8 +814,9 @@ def main():
     # roofline of the dominant kernel (K3 attention), live CUDA-event durations
     # device timestamps (globaltimer) around each K3 / K2 launch inside the layer graphs
     dur = runner.probe_durations(probe)
-    att = [(t, w) for kind, t, w in dur if kind == "attention"]
-    emb = [(t, w) for kind, t, w in dur if kind == "reembed"]
+    att = [(t, w) for kind, t, w, _ in dur if kind == "attention"]
+    emb = [(t, w) for kind, t, w, _ in dur if kind == "reembed"]
+    emb_moved = sum(m for kind, _, _, m in dur if kind == "reembed")
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     tflops_peak = peaks.get("bf16_tflops_sustained", 1400.0)
@@ -917,7 +927,13 @@ def main():
                                          "H2D runs on another stream, best of 3"},
         "roofline_reembed": {"kernel": "askv_reembed (K2)", "bound": "hbm",
                              "achieved": emb_gbs, "peak": hbm_peak, "unit": "GB/s",
-                             "frac": emb_gbs / hbm_peak},
+                             "frac": emb_gbs / hbm_peak,
+                             "bytes_per_launch": statistics.fmean(w for _, w in emb),
+                             "bytes_moved_per_launch": emb_moved / max(1, len(emb)),
+                             "us_per_launch": sum(t for t, _ in emb) / max(1, len(emb)) * 1e6,
+                             "work": "SURVEY §8(d): read + write of the kept rows' K "
+                                     "(kept x Hkv x hd x 2 B each way); V rows stay in "
+                                     "place except the last partial 128-row tile"},
         "decode": decode,
         "disk": disk,
         "gpu_launches": launches,

@@ -320,6 +320,11 @@ size_t askv_prefill_plan_size(void);
  * `stream`, synchronising), and make the layer loop use each n bucket's
  * fastest one.  Optional; call once per projection shape before serving. */
 int askv_gemm_autotune(int m, int k, int n_max, size_t workspace_bytes, void* stream);
+/* The layer loop's projection GEMM on its own: y[n][m] (+)= x[n][k] W[m][k]^T,
+ * bf16 in / out, fp32 accumulate, cuBLASLt with the tuned (or heuristic)
+ * algorithm of the n bucket; `accumulate` adds into y (the residual). */
+int askv_gemm(const void* x, const void* w, void* y, int n, int m, int k, int accumulate,
+              void* workspace, size_t workspace_bytes, void* stream);
 /* Set the device's persisting-L2 set-aside (clamped to the device maximum) so
  * the evict_last hints on the layer's rotated K/V rows (K2 / rope_new stores,
  * K3 loads) can hold them in L2 between producer and consumer; *applied (may

@@ -21,6 +21,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <type_traits>
 
@@ -62,6 +63,12 @@ __device__ __forceinline__ void launch_stamp_end(unsigned long long* st) {
   if (st && threadIdx.x == 0) atomicMax(st + 1, gtimer());
 }
 
+// Quarters of the softmax exponentials evaluated on the FMA pipe (packed
+// cubic) instead of MUFU ex2 (build-time A/B knob; 1 = one quarter).
+#ifndef ASKV_ATTN_POLY_Q
+#define ASKV_ATTN_POLY_Q 1
+#endif
+
 constexpr int kBM = 128;  // query rows per tile (UMMA M)
 constexpr int kBN = 128;  // key rows per tile (UMMA N of S, K of PV)
 constexpr int kMaxSplits = 32;
@@ -87,6 +94,7 @@ struct AttnParams {
   int sk_tiles_head;   // KV tiles of one head's units
   int sk_q_tiles;      // query tiles per head (unit = (head, query tile))
   int sk_units;        // units = heads x sk_q_tiles (partial slab stride)
+  int* sk_cnt;         // per-unit arrival counters (zero between launches)
   // V source (VSource, askv_internal.h): tiles < v_src_tiles load V through
   // tm_vs at row v_blk_off ? v_blk_off[t] / v_row_elems + v_layer_row
   //                         : v_src_row0 + 128 t
@@ -129,7 +137,7 @@ __host__ __device__ __forceinline__ int sk_owner(const AttnParams& p, int g, int
 // its tile range, and the partial slot (CTA index relative to the unit's first
 // CTA).  `whole` = the piece is the entire unit (final output, no combine).
 struct Piece {
-  int head, q, t_begin, t_end, slot, next;
+  int head, q, t_begin, t_end, slot, next, nslots;
   bool whole;
 };
 __host__ __device__ __forceinline__ Piece sk_piece(const AttnParams& p, int c, int ctas, int g,
@@ -150,6 +158,7 @@ __host__ __device__ __forceinline__ Piece sk_piece(const AttnParams& p, int c, i
   pc.slot = c - sk_owner(p, ub, ctas);
   pc.whole = pc.t_begin == 0 && pc.t_end == tu;
   pc.next = ub + pc.t_end;
+  pc.nslots = sk_owner(p, ub + tu - 1, ctas) - sk_owner(p, ub, ctas) + 1;
   return pc;
 }
 
@@ -541,7 +550,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
                                  sl2v, negm2);
           // a quarter of the exponentials go to the FMA pipe (packed cubic) so
           // MUFU and FMA share the load; masked tiles keep MUFU (exact zeros)
-          const float2 pp = (!kMask && ((e >> 1) & 3) == 3) ? ex2_poly2(x)
+          const float2 pp = (!kMask && ((e >> 1) & 3) >= 4 - ASKV_ATTN_POLY_Q) ? ex2_poly2(x)
                                                              : make_float2(ex2(x.x), ex2(x.y));
           switch ((e >> 1) & 3) {
             case 0: ls0 = fadd2(ls0, pp); break;
@@ -571,6 +580,8 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
       else
         tile(std::false_type{}, t, 0);
       if (threadIdx.x == 0 && t < 28) ATTN_TRACE(9 + 2 * t);
+      // P-done of WG0's other warps (per-warp skew of the p_full arrival)
+      if (lane == 0 && w == 0 && (warp & 3) != 0 && t < 4) ATTN_TRACE(180 + 3 * t + (warp & 3) - 1);
     }
     if (my_tiles > 0) {  // this group's last PV
       mbar_wait(&o_full[w], (my_tiles - 1) & 1);
@@ -653,7 +664,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
 }
 
 // ============================================================================
-// Stream-K kernel (single query tile per unit, the non-paired shapes).
+// Stream-K kernel (single query tile per unit, the non-paired shapes; opt-in).
 //
 // Units (query tile, head) are too few to fill 148 SMs at the path's skinny
 // shapes (C3 p50: 2 query tiles x 40 heads = 80 CTAs) and splitting them
@@ -661,9 +672,11 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
 // head-major list cut into gridDim.x (<= #SMs) equal contiguous ranges: each
 // CTA walks its range as a sequence of pieces (a piece = a run of one unit's
 // KV tiles), re-loading Q at each unit boundary.  A piece covering a whole
-// unit writes the bf16 output; a unit cut across CTAs leaves one fp32 partial
-// (O, lse) per piece, merged in slot order by attn_sk_combine_kernel
-// (deterministic).  Warp roles and the per-tile pipeline are the SPLIT mode of
+// unit writes the bf16 output (staged in shared memory, TMA store); a unit
+// cut across CTAs leaves one fp32 partial (O, lse) per piece and bumps the
+// unit's arrival counter -- the piece that arrives last merges all slots in
+// slot order (deterministic) and writes the output, so there is no separate
+// combine pass.  Warp roles and the per-tile pipeline are the SPLIT mode of
 // attn_fwd_kernel; the ring / phase counters run on across pieces, q_empty
 // (MMA -> Q producer) guards the Q tile and o_free (softmax -> MMA) the
 // TMEM S / O columns between pieces.
@@ -672,12 +685,15 @@ template <int HD>
 struct SkCfg {
   using B = Cfg<HD, false>;
   static constexpr int kKStages = B::kKStages;
-  static constexpr int kVStages = B::kVStages;
+  // V is consumed last (PV): 2 stages suffice (the paired kernel runs with 2)
+  // and free a 128 x HD bf16 tile that stages the output for its TMA store
+  static constexpr int kVStages = 2;
   static constexpr int kChunks = B::kChunks;
   static constexpr int kTileBytes = B::kTileBytes;
-  static constexpr int kQOff = B::kQOff, kKOff = B::kKOff, kVOff = B::kVOff,
-                       kBarOff = B::kBarOff;
-  static constexpr int kNumBars = B::kNumBars + 2;  // + q_empty, o_free
+  static constexpr int kQOff = B::kQOff, kKOff = B::kKOff, kVOff = B::kVOff;
+  static constexpr int kStageOff = kVOff + kVStages * kTileBytes;
+  static constexpr int kBarOff = kStageOff + kTileBytes;
+  static constexpr int kNumBars = 1 + 2 * kKStages + 2 * kVStages + 6 + 2;  // + q_empty, o_free
   static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
   static constexpr int kSmemBytes = kTmemSlotOff + 16 + 1024;
   static constexpr uint32_t kTmemCols = B::kTmemCols;
@@ -694,7 +710,8 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
     attn_sk_kernel(const __grid_constant__ CUtensorMap tm_q,
                    const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v,
-                   const __grid_constant__ CUtensorMap tm_vs, const AttnParams p) {
+                   const __grid_constant__ CUtensorMap tm_vs,
+                   const __grid_constant__ CUtensorMap tm_o, const AttnParams p) {
   using C = SkCfg<HD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -702,6 +719,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
   uint8_t* sQ = smem + C::kQOff;
   uint8_t* sK = smem + C::kKOff;
   uint8_t* sV = smem + C::kVOff;
+  uint8_t* sStage = smem + C::kStageOff;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
   uint64_t* q_full = bars;
   uint64_t* k_full = q_full + 1;
@@ -966,7 +984,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
             const int k = c * 32 + e;
             const float2 x = ffma2(make_float2(__uint_as_float(sr[k]), __uint_as_float(sr[k + 1])),
                                    sl2v, negm2);
-            const float2 pp = (!kMask && ((e >> 1) & 3) == 3) ? ex2_poly2(x)
+            const float2 pp = (!kMask && ((e >> 1) & 3) >= 4 - ASKV_ATTN_POLY_Q) ? ex2_poly2(x)
                                                                : make_float2(ex2(x.x), ex2(x.y));
             switch ((e >> 1) & 3) {
               case 0: ls0 = fadd2(ls0, pp); break;
@@ -1042,17 +1060,95 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(o_free);
       }
-      const int64_t slab =
-          (int64_t)pc.slot * p.sk_units + (int64_t)pc.head * p.sk_q_tiles + pc.q;
-      float* po = p.part_o + (slab * HD + col0) * kBM + r;
+      // ---- output.  A whole unit is final; a cut unit leaves its partial
+      // (column-major, coalesced) and counts its arrival: the piece that
+      // arrives last merges every slot (deterministic slot order) and writes
+      // the unit's output -- no separate combine pass.
+      if (threadIdx.x == 0) ATTN_TRACE(176);
+      const int u = pc.head * p.sk_q_tiles + pc.q;
+      const float lse_own = l_fin > 0.f ? m_fin + __log2f(l_fin) : -INFINITY;
+      bool final_here = pc.whole;
+      if (!pc.whole) {
+        const int64_t slab = (int64_t)pc.slot * p.sk_units + u;
+        float* po = p.part_o + (slab * HD + col0) * kBM + r;
 #pragma unroll
-      for (int e = 0; e < kHalf; ++e) po[e * kBM] = o[e];
-      if (w == 0) p.part_lse[slab * kBM + r] = l_fin > 0.f ? m_fin + __log2f(l_fin) : -INFINITY;
+        for (int e = 0; e < kHalf; ++e) po[e * kBM] = o[e];
+        if (w == 0) p.part_lse[slab * kBM + r] = lse_own;
+        if (threadIdx.x == 0) ATTN_TRACE(177);
+        __threadfence();
+        named_bar_sync(2, 256);
+        if (threadIdx.x == 0) ATTN_TRACE(178);
+        if (threadIdx.x == 0) {
+          const int old = atomicAdd(p.sk_cnt + u, 1);
+          const int last = old == pc.nslots - 1;
+          if (last) p.sk_cnt[u] = 0;   // every piece of the unit has counted
+          tmem_slot[1] = last;
+        }
+        named_bar_sync(2, 256);
+        final_here = tmem_slot[1] != 0;
+        if (threadIdx.x == 0) ATTN_TRACE(179);
+        if (final_here) {
+          __threadfence();
+          float mx = lse_own;
+          for (int s2 = 0; s2 < pc.nslots; ++s2)
+            if (s2 != pc.slot)
+              mx = fmaxf(mx, p.part_lse[((int64_t)s2 * p.sk_units + u) * kBM + r]);
+          const float w_own = lse_own == -INFINITY ? 0.f : exp2f(lse_own - mx);
+          float sum = w_own;
+#pragma unroll
+          for (int e = 0; e < kHalf; ++e) o[e] *= w_own;
+          for (int s2 = 0; s2 < pc.nslots; ++s2) {
+            if (s2 == pc.slot) continue;
+            const int64_t sl = (int64_t)s2 * p.sk_units + u;
+            const float l = p.part_lse[sl * kBM + r];
+            if (l == -INFINITY) continue;
+            const float wt = exp2f(l - mx);
+            sum += wt;
+            const float* src = p.part_o + (sl * HD + col0) * kBM + r;
+#pragma unroll
+            for (int e = 0; e < kHalf; ++e) o[e] = fmaf(wt, src[e * kBM], o[e]);
+          }
+          const float inv = sum > 0.f ? 1.f / sum : 0.f;
+#pragma unroll
+          for (int e = 0; e < kHalf; ++e) o[e] *= inv;
+        }
+      }
+      if (final_here) {
+        // stage the bf16 tile in the canonical 128B-swizzled layout (64-column
+        // halves of 128 rows x 128 B, like the Q tile) and TMA-store it; rows
+        // past the last token are clipped by the tensor map
+#pragma unroll
+        for (int k = 0; k < kHalf / 8; ++k) {
+          const int gcol = col0 + k * 8;
+          const int hh = gcol >> 6, c16 = (gcol & 63) >> 3;
+          uint4 v;
+          v.x = pack_bf16x2(o[k * 8 + 0], o[k * 8 + 1]);
+          v.y = pack_bf16x2(o[k * 8 + 2], o[k * 8 + 3]);
+          v.z = pack_bf16x2(o[k * 8 + 4], o[k * 8 + 5]);
+          v.w = pack_bf16x2(o[k * 8 + 6], o[k * 8 + 7]);
+          *reinterpret_cast<uint4*>(sStage + hh * (kBM * 128) + r * 128 +
+                                    ((c16 ^ (r & 7)) << 4)) = v;
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(2, 256);
+        if (threadIdx.x == 0) ATTN_TRACE(180);
+        if (threadIdx.x == 0) {
+#pragma unroll
+          for (int hh = 0; hh < HD / 64; ++hh)
+            tma_store_3d(&tm_o, sStage + hh * (kBM * 128), hh * 64,
+                         pack > 1 ? pc.head * pack : pc.head, tok(qt0));
+          tma_store_commit();
+          tma_store_wait_read();   // the staging tile is free again
+        }
+        named_bar_sync(2, 256);
+        if (threadIdx.x == 0) ATTN_TRACE(181);
+      }
       cw += my_tiles;
     }
   } else {
     shrink();  // warp 11
   }
+  if (threadIdx.x == 0) ATTN_TRACE(182);
 
   tc_fence_before();
   __syncthreads();
@@ -1062,72 +1158,6 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
   }
   if (threadIdx.x == 0) ATTN_TRACE(4);
   if (p.num_splits == 1) launch_stamp_end(p.stamp);
-}
-
-// Merge every unit's per-piece partials (slot order, deterministic) and write
-// the bf16 output.  Grid (units, HD / 32): a CTA owns 32 columns of one unit;
-// the slot weights exp2(lse_s - max) of its 128 rows go to shared memory,
-// each thread then accumulates 16 columns of one row with the 16 loads of a
-// slot in flight together (the partials are column-major per unit, so a
-// warp's loads are coalesced), and the 128 x 32 bf16 tile leaves as 64-byte
-// row segments.
-template <int HD>
-__global__ void __launch_bounds__(256)
-    attn_sk_combine_kernel(const AttnParams p, int ctas) {
-  const int u = blockIdx.x;
-  const int c_base = blockIdx.y * 32;
-  const int head = u / p.sk_q_tiles, q = u - head * p.sk_q_tiles;
-  int ub = head * p.sk_tiles_head;
-  for (int k = 0; k < q; ++k) ub += unit_tiles(p, k);
-  const int tu = unit_tiles(p, q);
-  const int s0 = sk_owner(p, ub, ctas);
-  const int ns = sk_owner(p, ub + tu - 1, ctas) - s0 + 1;
-  __shared__ float wts[kMaxSkSlots][kBM];
-  __shared__ __align__(16) __nv_bfloat16 tile[kBM][32 + 8];
-  const int t = threadIdx.x;
-  if (t < kBM) {
-    float m = -INFINITY;
-    for (int s = 0; s < ns; ++s)
-      m = fmaxf(m, p.part_lse[((int64_t)s * p.sk_units + u) * kBM + t]);
-    float sum = 0.f;
-    for (int s = 0; s < ns; ++s) {
-      const float l = p.part_lse[((int64_t)s * p.sk_units + u) * kBM + t];
-      const float wt = (l == -INFINITY) ? 0.f : exp2f(l - m);
-      wts[s][t] = wt;
-      sum += wt;
-    }
-    const float inv = sum > 0.f ? 1.f / sum : 0.f;
-    for (int s = 0; s < ns; ++s) wts[s][t] *= inv;
-  }
-  __syncthreads();
-  const int r = t & (kBM - 1);
-  const int c0 = (t >> 7) * 16;
-  float acc[16] = {};
-  for (int s = 0; s < ns; ++s) {
-    const float wt = wts[s][r];
-    const float* src = p.part_o + (((int64_t)s * p.sk_units + u) * HD + c_base + c0) * kBM + r;
-    float v[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = src[e * kBM];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) acc[e] = fmaf(wt, v[e], acc[e]);
-  }
-#pragma unroll
-  for (int e = 0; e < 16; ++e) tile[r][c0 + e] = __float2bfloat16(acc[e]);
-  __syncthreads();
-  const int pack = p.pack;
-  const int q_rows = pack > 1 ? p.n_new * pack : p.n_new;
-  const int rows_u = min(kBM, q_rows - q * kBM);
-  // 16 lanes x 4 bytes per row: a warp writes two rows per instruction
-  const int half = (t & 31) >> 4, l16 = t & 15;
-  for (int i = (t >> 5) * 2 + half; i < rows_u; i += 16) {
-    const int qi = q * kBM + i;
-    const int64_t row = pack > 1 ? (int64_t)(qi / pack) * p.hq + head * pack + qi % pack
-                                 : (int64_t)qi * p.hq + head;
-    *reinterpret_cast<uint32_t*>(p.out + row * HD + c_base + l16 * 2) =
-        *reinterpret_cast<const uint32_t*>(&tile[i][l16 * 2]);
-  }
-  if (p.stamp && t == 0) atomicMax(p.stamp + 1, gtimer());
 }
 
 // Deterministic split-KV combine: one warp per (query, head), splits in order.
@@ -1336,23 +1366,56 @@ size_t sk_workspace(int n_cached, int n_new, int hq, int hkv, int head_dim) {
   prm.pack = gqa_pack(hq, hkv);
   SkPlan plan;
   sk_plan(prm, hkv, sm_count(), plan);
+  if (plan.max_slots <= 1) return 0;
   return (size_t)plan.max_slots * prm.sk_units * kBM * (head_dim + 1) * sizeof(float);
+}
+
+// Per-device arrival counters of the stream-K fixup (one int per unit).  The
+// kernel leaves them zero (the last piece of a unit resets its counter), so
+// they are zeroed once, at allocation, on a private stream (legal while the
+// caller's stream is being captured).
+constexpr int kSkMaxUnits = 1 << 16;
+int* sk_counters() {
+  static std::mutex mu;
+  static std::map<int, int*> bufs;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  int*& b = bufs[dev];
+  if (!b) {
+    cudaStream_t st;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    if (cudaMalloc(&b, kSkMaxUnits * sizeof(int)) != cudaSuccess ||
+        cudaMemsetAsync(b, 0, kSkMaxUnits * sizeof(int), st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      b = nullptr;
+    cudaStreamDestroy(st);
+  }
+  return b;
 }
 
 template <int HD>
 int launch_sk(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
-              const CUtensorMap& mvs, AttnParams prm, int hkv, void* ws, size_t ws_bytes,
-              cudaStream_t stream) {
+              const CUtensorMap& mvs, const CUtensorMap& mo, AttnParams prm, int hkv, void* ws,
+              size_t ws_bytes, cudaStream_t stream) {
   SkPlan plan;
   sk_plan(prm, hkv, sm_count(), plan);
+  ASKV_REQUIRE(prm.sk_units <= kSkMaxUnits, "prefill_attn: %d stream-K units > %d",
+               prm.sk_units, kSkMaxUnits);
   const size_t slab = (size_t)prm.sk_units * kBM;
-  const size_t need = (size_t)plan.max_slots * slab * (HD + 1) * sizeof(float);
-  ASKV_REQUIRE(ws != nullptr && ws_bytes >= need,
+  const size_t need = plan.max_slots > 1
+                          ? (size_t)plan.max_slots * slab * (HD + 1) * sizeof(float) : 0;
+  ASKV_REQUIRE(need == 0 || (ws != nullptr && ws_bytes >= need),
                "prefill_attn: workspace %zu bytes < %zu needed (stream-K, %d slots)", ws_bytes,
                need, plan.max_slots);
   prm.part_o = static_cast<float*>(ws);
-  prm.part_lse = prm.part_o + (size_t)plan.max_slots * slab * HD;
-  prm.num_splits = 2;  // the combine stamps the launch end
+  prm.part_lse = need ? prm.part_o + (size_t)plan.max_slots * slab * HD : nullptr;
+  prm.sk_cnt = sk_counters();
+  if (!prm.sk_cnt) {
+    set_error("prefill_attn: stream-K counters");
+    return ASKV_ECUDA;
+  }
+  prm.num_splits = 1;  // the kernel stamps its own end (no combine pass)
   auto kern = attn_sk_kernel<HD>;
   static bool attr = false;
   if (!attr) {
@@ -1361,12 +1424,9 @@ int launch_sk(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& m
     if (e != cudaSuccess) return cuda_status(e, "attn_sk smem attribute");
     attr = true;
   }
-  kern<<<plan.ctas, SkCfg<HD>::kThreads, SkCfg<HD>::kSmemBytes, stream>>>(mq, mk, mv, mvs,
+  kern<<<plan.ctas, SkCfg<HD>::kThreads, SkCfg<HD>::kSmemBytes, stream>>>(mq, mk, mv, mvs, mo,
                                                                           prm);
-  int rc = launch_status("attn_sk launch");
-  if (rc) return rc;
-  attn_sk_combine_kernel<HD><<<dim3(prm.sk_units, HD / 32), 256, 0, stream>>>(prm, plan.ctas);
-  return launch_status("attn_sk_combine launch");
+  return launch_status("attn_sk launch");
 }
 
 template <int HD>
@@ -1411,7 +1471,10 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
     prm.out = static_cast<__nv_bfloat16*>(out);
     prm.stamp = stamp;
     set_vs(prm);
-    return launch_sk<HD>(mq, mk, mv, mvs, prm, hkv, ws, ws_bytes, stream);
+    CUtensorMap mo;
+    rc = make_map(&mo, out, HD, hq, HD, n_new, (int64_t)hq * HD, pack);
+    if (rc) return rc;
+    return launch_sk<HD>(mq, mk, mv, mvs, mo, prm, hkv, ws, ws_bytes, stream);
   }
   const int tps = (kv_tiles + splits - 1) / splits;
   splits = (kv_tiles + tps - 1) / tps;

@@ -448,6 +448,14 @@ extern "C" int askv_gemm_autotune(int m, int k, int n_max, size_t ws_bytes, void
 // ------------------------------------------------------------------ layer loop
 extern "C" size_t askv_prefill_plan_size(void) { return sizeof(askv_prefill_plan); }
 
+extern "C" int askv_gemm(const void* x, const void* w, void* y, int n, int m, int k,
+                         int accumulate, void* workspace, size_t workspace_bytes, void* stream) {
+  clear_error();
+  ASKV_REQUIRE(n > 0 && m > 0 && k > 0 && x && w && y, "gemm: bad %d x %d x %d", n, m, k);
+  return gemm(x, w, y, n, m, k, accumulate != 0, workspace, workspace_bytes,
+              (cudaStream_t)stream);
+}
+
 static int issue_layers(const askv_prefill_plan* p, cudaStream_t s);
 
 // Row-parallel output projection + NCCL sum into the residual stream:

@@ -424,14 +424,15 @@ class Runner:
     def _stamp_ptr(self, off: int, i: int) -> int:
         return self._stamps.data_ptr() + 8 * (off + i)
 
-    def probe_durations(self, probe) -> list[tuple[str, float, float]]:
-        """(kind, seconds, work) of each probed launch (after synchronising)."""
+    def probe_durations(self, probe) -> list[tuple[str, float, float, float]]:
+        """(kind, seconds, algorithmic work, bytes actually moved -- K2 only)
+        of each probed launch (after synchronising)."""
         out, cache = [], {}
-        for kind, off, end, n, i0, i1, work in probe:
+        for kind, off, end, n, i0, i1, work, moved in probe:
             if (off, end) not in cache:
                 cache[(off, end)] = self._stamp_values(off, end, n)
             v = cache[(off, end)]
-            out.append((kind, (v[i1] - v[i0]) * 1e-9, work))
+            out.append((kind, (v[i1] - v[i0]) * 1e-9, work, moved))
         return out
 
     def _lease(self, jid):
@@ -769,13 +770,21 @@ class Runner:
                 p.stamp_flags = (1 if lease else 0) | (2 if self.probe is not None else 0)
                 rec["waited"] = reemb and units is not None
             if self.probe is not None:
+                # K2's work: SURVEY §8(d) counts read K + write K (kept rows, the
+                # K half of each row); V rows of whole 128-row tiles stay where
+                # the pre-loader left them (K3 reads them there), the rest are copied
+                v_src = (p.src_rows > 0 and job.kv_cache is None and
+                         (p.src_kind == 1 or (p.src_kind == 2 and job.head == 0
+                                              and self.block_tokens == 128)))
+                v_copy = kept - (kept // 128) * 128 if v_src else kept
+                k2_moved = kept * s.row_bytes + v_copy * s.row_bytes
                 for l in range(L):
                     b = 2 + 1 + 7 * l
                     if reemb:
                         self.probe.append(("reembed", st_off, st_end, n_st, b + 3, b + 4,
-                                           2 * kept * s.row_bytes))
+                                           kept * s.row_bytes, k2_moved))
                     self.probe.append(("attention", st_off, st_end, n_st, b + 5, b + 6,
-                                       attention_flops(kept, n, hq, hd)))
+                                       attention_flops(kept, n, hq, hd), 0))
             if self._ar_cb is not None:
                 p.allreduce = self._ar_cb
             elif self._nccl is not None:

@@ -95,8 +95,9 @@ def run(args) -> dict:
     from . import numa
     node = numa.gpu_numa_node(args.device) if args.numa_node < 0 else args.numa_node
     t_alloc = time.perf_counter()
+    hbm_blocks = int(args.hbm_gb * 1e9) // bb
     eng = E.Engine(shape, host_blocks=host_blocks, block_tokens=tb, device=dev, seed=0,
-                   read_buffer_bytes=rb, max_new=4096, dram_bytes=dram,
+                   read_buffer_bytes=rb, max_new=4096, dram_bytes=dram, hbm_blocks=hbm_blocks,
                    autotune=True if args.autotune < 0 else args.autotune, policy=PolicyConfig(),
                    numa_node=node)
     t_alloc = time.perf_counter() - t_alloc
@@ -113,14 +114,26 @@ def run(args) -> dict:
            "numa_node": eng.arena.numa_node,
            "data": "synthetic: reference generator sessions, random-init weights, random ids"}
     modes = ["reuse", "recompute"] if not args.reuse_only else ["reuse"]
+    tier = eng.hbm
+    if tier is not None:
+        modes.append("reuse_hbm_tier")
+        out["hbm_tier_bytes"] = hbm_blocks * bb
     for mode in modes:
+        # the HBM session tier only in its own mode
+        eng.hbm = tier if mode == "reuse_hbm_tier" else None
+        eng.store.on_release = tier.drop if eng.hbm is not None else None
+        if tier is not None:
+            for sid in list(tier.tab):
+                tier.drop(sid)
         t0 = time.perf_counter()
         log, ex = measured.serve(wl, eng, cfg, recompute=mode == "recompute")
         wall = time.perf_counter() - t0
         s = summarize(log)
         s["host_wall_s"] = wall
         s["jobs"] = ex.jobs
-        if mode == "reuse":
+        if mode == "reuse_hbm_tier":
+            s["tier_hits"], s["tier_promotions"] = tier.hits, tier.promotions
+        if mode.startswith("reuse"):
             loads = [t.timeline for t in log.turns
                      if t.timeline is not None and t.hit_class != "miss"]
             lb = sum(t.bytes_loaded for t in log.turns if t.hit_class != "miss")
@@ -142,6 +155,10 @@ def run(args) -> dict:
         out["speedup_p50_ttft"] = c["p50_ttft_s"] / r["p50_ttft_s"] if r["p50_ttft_s"] else None
         out["speedup_p50_prefill"] = (c["p50_prefill_s"] / r["p50_prefill_s"]
                                       if r["p50_prefill_s"] else None)
+        if "reuse_hbm_tier" in out:
+            h = out["reuse_hbm_tier"]
+            out["speedup_p50_ttft_hbm_tier"] = (c["p50_ttft_s"] / h["p50_ttft_s"]
+                                                if h["p50_ttft_s"] else None)
     return out
 
 
@@ -153,6 +170,8 @@ def parse(argv=None):
     ap.add_argument("--max-sessions", type=int, default=0)
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--dram-gb", type=float, default=96.0)
+    ap.add_argument("--hbm-gb", type=float, default=0.0,
+                    help="also serve with an HBM session tier of this size (0 = off)")
     ap.add_argument("--read-buffer-gb", type=float, default=10.0,
                     help="cap of S_buf (TierConfig.hbm_read_buffer default 10 GB)")
     ap.add_argument("--link-gbs", type=float, default=55.0)

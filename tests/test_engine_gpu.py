@@ -321,21 +321,21 @@ def test_k3_reads_v_from_the_preload_source():
     wnp = w.to_numpy()
     rng = np.random.default_rng(13)
     seq = np.zeros(0, dtype=np.int64)
-    sources = []
     for k, (nn, no) in enumerate([(300, 40), (90, 30), (150, 20), (70, 10)]):
         n = torch.as_tensor(rng.integers(0, shape.vocab, nn))
         o = torch.as_tensor(rng.integers(0, shape.vocab, no))
-        hits_before = eng.hbm.hits
+        if k == 2:   # force this turn back onto the host link (read-buffer slot)
+            eng.hbm.drop("s")
         out = eng.turn("s", k, n, o, want_logits=True)
         torch.cuda.synchronize()
-        sources.append("hbm" if eng.hbm.hits > hits_before else
-                       ("host" if out.kept else "none"))
+        assert (out.kept >= 128) == (k > 0)
         seq = np.concatenate([seq, n.numpy()])
         got = out.result.logits.cpu().double().numpy()
         assert rope_ref.rel_err(got, oracle_logits(wnp, shape, seq)) <= LOGIT_TOL, k
         seq = np.concatenate([seq, o.numpy()])
-    assert sources[0] == "none" and "hbm" in sources
-    assert all(s != "none" for s in sources[1:])
+    # both V sources were exercised: slot (host turns, promoted into the tier)
+    # and HBM-tier blocks
+    assert eng.hbm.promotions >= 1 and eng.hbm.hits >= 1
 
 
 def test_hbm_tier_is_bit_identical_to_host_path():

@@ -100,6 +100,9 @@ int main(int argc, char** argv) {
     printf(" | WG0 tiles:");
     for (int t = 0; t < 14 && r[8 + 2 * t]; ++t) printf(" [%.2f %.2f]", us(r[8 + 2 * t]), us(r[9 + 2 * t]));
     printf(" | last epi %.2f exit %.2f\n", us(r[3]), us(r[4]));
+    printf("   last piece: merged %.2f partial stored %.2f fenced %.2f counted %.2f staged %.2f "
+           "stored %.2f softmax-done %.2f\n", us(r[176]), us(r[177]), us(r[178]), us(r[179]),
+           us(r[180]), us(r[181]), us(r[182]));
     printf("   mma [P seen, V ready, PV issued, K(j+2) ready]:");
     for (int t = 0; t < 28 && r[64 + t]; ++t)
       printf(" [%.2f %.2f %.2f %.2f]", us(r[64 + t]), us(r[96 + t]), us(r[160 + t]), us(r[128 + t]));

@@ -102,6 +102,12 @@ int main(int argc, char** argv) {
     printf(" | epi %.2f merged %.2f stored %.2f synced %.2f exit %.2f\n", (r[3] - t0) * 1e-3,
            r[5] ? (r[5] - t0) * 1e-3 : 0.0, r[6] ? (r[6] - t0) * 1e-3 : 0.0,
            r[7] ? (r[7] - t0) * 1e-3 : 0.0, (r[4] - t0) * 1e-3);
+    printf("   WG0 P-done of warps 1..3 for tiles 0..3:");
+    for (int t = 0; t < 4; ++t)
+      printf(" [%.2f %.2f %.2f]", r[180 + 3 * t] ? (r[180 + 3 * t] - t0) * 1e-3 : 0.0,
+             r[181 + 3 * t] ? (r[181 + 3 * t] - t0) * 1e-3 : 0.0,
+             r[182 + 3 * t] ? (r[182 + 3 * t] - t0) * 1e-3 : 0.0);
+    printf("\n");
     printf("   mma: P(j) seen / V(j) ready / PV(j) issued / K(j+2) ready:");
     for (int t = 0; t < 28 && r[64 + t]; ++t)
       printf(" [%.2f %.2f %.2f %.2f]", (r[64 + t] - t0) * 1e-3, (r[96 + t] - t0) * 1e-3,

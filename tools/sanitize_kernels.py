@@ -98,7 +98,34 @@ def provenance_cases():
     dst = torch.empty(kept, row, device="cuda", dtype=torch.bfloat16)
     ops.reembed(slot, kept, hkv, d, table, dst)
     torch.cuda.synchronize()
-    print("provenance: memcpy batch -> reembed done", flush=True)
+    print("provenance: copy-engine DMA -> reembed done", flush=True)
+    # The engine feeds rope_new from the library's own cuBLASLt GEMM
+    # (askv_gemm, the nvjet kernels with a TMA-store epilogue).  (a) GEMM into
+    # a fresh buffer, then rope_new; (b) the same after a memset of that
+    # buffer.  Equal outputs, and reports only in (a), mean initcheck does not
+    # see the GEMM's stores: its engine-path reports are false positives.
+    from paper_2403_19708_b200 import _lib
+    lib = _lib.lib()
+    wsb = 32 << 20
+    gws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    h = torch.randn(n, 256, device="cuda").to(torch.bfloat16)
+    outs = []
+    for label, pre_zero in (("gemm-fresh", False), ("gemm-after-memset", True)):
+        y = torch.empty(n, (hq + 2 * hkv) * d, device="cuda", dtype=torch.bfloat16)
+        if pre_zero:
+            y.zero_()
+        _lib.check(lib.askv_gemm(h.data_ptr(), w.data_ptr(), y.data_ptr(), n, y.shape[1], 256,
+                                 0, gws.data_ptr(), wsb, None), "gemm")
+        torch.cuda.synchronize()
+        print(f"provenance: {label} -> rope_new start", flush=True)
+        qo = torch.empty(n, hq * d, device="cuda", dtype=torch.bfloat16)
+        ko = torch.empty(n, 2 * hkv * d, device="cuda", dtype=torch.bfloat16)
+        ops.rope_new(y, n, hq, hkv, d, table, 0, qo, ko, None)
+        torch.cuda.synchronize()
+        outs.append((qo.clone(), ko.clone()))
+        print(f"provenance: {label} -> rope_new done", flush=True)
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    print("provenance: outputs identical", flush=True)
 
 
 def engine_turns(graph: bool):
