@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--turns", type=int, default=16, help="hit turns per GPU per step")
     ap.add_argument("--block-tokens", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--batch-prefill", type=int, default=1,
+                    help="value mode: run each step's turns as one batched layer pass "
+                         "(askv_prefill_layers_batch); 0 = one turn after another")
     ap.add_argument("--fragmented", action="store_true",
                     help="scatter every turn's blocks over the arena (random permutation) "
                          "instead of the allocator's contiguous runs")
@@ -286,7 +289,9 @@ def make_config(args, shape, turns, n_hits, world, tp, rank_probe) -> dict:
                      f"tokens per turn, {len(turns)} turns/GPU/step"),
         "turns_per_gpu": len(turns), "kept_p50": percentile(kept_l, 0.5),
         "new_p50": percentile(new_l, 0.5), "block_tokens": args.block_tokens,
-        "value_mode": "KV resident in an HBM arena (no host link)",
+        "value_mode": ("KV resident in an HBM arena (no host link); the step's turns in one "
+                       "batched layer pass" if getattr(args, "batch_prefill", 0) else
+                       "KV resident in an HBM arena (no host link)"),
         "e2e_mode": "KV streamed from pinned host DRAM by the layer-wise pre-loader; "
                     "new-token KV saved back asynchronously",
         "l2": f"inputs larger than L2 (per-step KV {kv_bytes / 1e9:.1f} GB)",
@@ -626,7 +631,12 @@ def main():
         tp_hook = pdist.NcclComm(rank, world)   # native: ncclAllReduce inside the layer graph
     runner = Runner(shape, device=dev, seed=rank if tp > 1 else 0, block_tokens=tb,
                     host_arena=arena, tp_reduce=tp_hook,
-                    hbm_arena=hbm, read_buffer_bytes=4 << 30, write_buffer_bytes=1 << 30,
+                    hbm_arena=hbm, read_buffer_bytes=4 << 30,
+                    # batched value mode: every (job, layer) of a step holds its
+                    # own write-buffer slot while the batch runs
+                    write_buffer_bytes=max(1 << 30, (len(turns) * shape.layers
+                                                     * max(max_new, 1) * shape.row_bytes
+                                                     if args.batch_prefill else 0)),
                     max_new=max(max_new, 1), max_ctx=max(shape.context_window, max_kept + 1),
                     # tune the GEMMs over the recompute baseline's prompt lengths too
                     autotune=max(shape.context_window, max_kept + 1) + max(max_new, 1),
@@ -673,7 +683,8 @@ def main():
     def sum_over_ranks(x: float) -> float:
         return pdist.sum_over_ranks(x, red_dev)
 
-    def timed(mode: str, steps: int, warmup: int, probe: bool = False, clocks=None):
+    def timed(mode: str, steps: int, warmup: int, probe: bool = False, clocks=None,
+              batch: bool = False):
         js = jobs[mode]
         sampler = ClockSampler(local) if clocks is not None and \
             os.environ.get("ASKV_BENCH_CLOCKS", "1") != "0" else None
@@ -681,7 +692,7 @@ def main():
             sampler.__enter__()
         runner.probe = [] if probe else None   # same graph shapes as the timed steps
         for _ in range(warmup):
-            runner.run(js)
+            runner.run(js, batch=batch)
             runner.join()
         torch.cuda.synchronize()
         barrier()
@@ -694,7 +705,7 @@ def main():
         e0.record(cs)
         res = None
         for _ in range(steps):
-            res = runner.run(js)
+            res = runner.run(js, batch=batch)
             runner.join()
         e1.record(cs)
         torch.cuda.synchronize()
@@ -721,6 +732,13 @@ def main():
     clocks_value: dict = {}
     ms_hbm, res_hbm, _, probe = timed("hbm", args.steps, args.warmup, probe=True,
                                       clocks=clocks_value)
+    # value, batched (scheduler knob): the step's turns in one pass over the
+    # layers -- GEMMs over all their new tokens, K2 / K3 / saves per turn
+    ms_batch = None
+    if args.batch_prefill:
+        clocks_batch: dict = {}
+        ms_batch, _, _, _ = timed("hbm", args.steps, args.warmup, clocks=clocks_batch,
+                                  batch=True)
     # recompute baseline
     ms_re, res_re, _, _ = timed("recompute", max(2, args.steps // 2), 1)
     # prestaged TTFT: each turn starts once its whole KV sits in the read buffer
@@ -807,7 +825,9 @@ def main():
     tok_all = prompt_tokens if tp > 1 else sum_over_ranks(prompt_tokens)
     new_all = new_tokens if tp > 1 else sum_over_ranks(new_tokens)
     turns_all = len(turns) if tp > 1 else sum_over_ranks(len(turns))
-    value = tok_all * args.steps / t_hbm
+    value_unbatched = tok_all * args.steps / t_hbm
+    t_batch = max_over_ranks(ms_batch) * 1e-3 if ms_batch is not None else None
+    value = tok_all * args.steps / t_batch if t_batch else value_unbatched
     e2e = tok_all * args.steps / t_host
     recompute = tok_all * steps_re / t_re
 
@@ -864,7 +884,18 @@ def main():
     new_l = [new for *_, new in turns]
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_hbm / args.steps,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": (ms_batch if ms_batch is not None else ms_hbm) / args.steps,
+        "value_unbatched": {"value": value_unbatched, "ms_per_step": ms_hbm / args.steps,
+                            "note": "value mode with one turn after another (each turn its "
+                                    "own layer pass: the TTFT-optimal schedule)"},
+        "batch_prefill": ({"turns_per_batch": len(turns), "ms_per_step": ms_batch / args.steps,
+                           "clocks": clocks_batch,
+                           "note": "the step's turns in one pass over the layers: norms, "
+                                   "projections and MLP over all their new tokens, pre-load "
+                                   "wait / K2 / K3 / saves per turn (scheduler knob "
+                                   "--batch-prefill; trades TTFT for throughput)"}
+                          if ms_batch is not None else None),
         "higher_is_better": True, "scaling": "strong" if tp > 1 else "weak",
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (reference ShareGPT-shaped session generator; random-init weights "

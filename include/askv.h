@@ -296,6 +296,16 @@ typedef struct askv_prefill_plan {
 } askv_prefill_plan;
 
 int askv_prefill_layers(const askv_prefill_plan* plan, void* stream);
+/* Several jobs (sessions' turns) in one pass over the layers: the norms,
+ * projections and MLP run once over the jobs' concatenated new tokens, while
+ * rope_new, the pre-load wait, K2 and K3 run per job on its own rows.  plans[i]
+ * describes job i as for askv_prefill_layers; the jobs share the model and
+ * their x / h / qkv / q_rot / attn_out / gu / act buffers are consecutive
+ * slices of plans[0]'s (job i's starts after jobs 0..i-1's rows); job 0's
+ * stamps carry the layer timeline.  No tensor parallelism or K2 overlap.
+ * A scheduler knob: batching trades each turn's time to first token for
+ * throughput (GEMMs over thousands of rows instead of a few hundred). */
+int askv_prefill_layers_batch(const askv_prefill_plan* plans, int njobs, void* stream);
 
 /*
  * K5 — NCCL for the tensor-parallel all-reduce (C5), bound at run time

@@ -37,6 +37,7 @@ SIGNATURES = {
     "askv_attn_workspace_bytes": (_sz, [_i32, _i32, _i32, _i32, _i32]),
     "askv_attn_workspace_bytes_gqa": (_sz, [_i32, _i32, _i32, _i32, _i32, _i32]),
     "askv_gemm": (_i32, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _sz, _vp]),
+    "askv_prefill_layers_batch": (_i32, [_vp, _i32, _vp]),
     "askv_nccl_unique_id": (_i32, [_vp]),
     "askv_nccl_comm_init": (_i32, [_i32, _i32, _vp, C.POINTER(_vp)]),
     "askv_nccl_comm_destroy": (_i32, [_vp]),

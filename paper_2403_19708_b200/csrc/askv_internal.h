@@ -53,6 +53,28 @@ struct VSource {
   int64_t row_elems = 0;
   int64_t layer_row = 0;
 };
+// K3 over a batch of jobs in one launch (askv_prefill_layers_batch): job i's
+// queries are rows [q_row0, q_row0 + n_new) of q, its keys / values rows
+// [kv_row0, kv_row0 + n_cached + n_new) of kv; optional V source shared by
+// the jobs (an HBM arena: kind 2, per-job block tables).
+struct VarlenBatch {
+  int n = 0;
+  const void* q = nullptr;
+  const void* kv = nullptr;
+  int64_t kv_row_stride = 0;
+  int hq = 0, hkv = 0, head_dim = 0;
+  float scale = 1.f;
+  const int* n_new = nullptr;
+  const int* n_cached = nullptr;
+  const int* q_row0 = nullptr;
+  const int* kv_row0 = nullptr;
+  void* const* out = nullptr;
+  const void* vsrc_base = nullptr;
+  int64_t vsrc_rows = 0, vsrc_row_elems = 0, v_layer_row = 0;
+  const int* v_src_tiles = nullptr;
+  const int64_t* const* v_blk_off = nullptr;
+};
+int prefill_attn_varlen(const VarlenBatch& b, void* stream, unsigned long long* stamp);
 int prefill_attn_stamped(const void* q, const void* kv, int64_t kv_row_stride, int n_cached,
                          int n_new, int n_heads, int n_kv_heads, int head_dim, float scale,
                          void* out, void* workspace, size_t workspace_bytes, int num_splits,

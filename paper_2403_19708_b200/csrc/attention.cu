@@ -18,6 +18,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -103,6 +104,22 @@ struct AttnParams {
   const int64_t* v_blk_off;
   int64_t v_row_elems;
   int64_t v_layer_row;
+};
+
+// Varlen launch (a batch of jobs in one K3 launch, askv_prefill_layers_batch):
+// per job its sizes, where its rows sit in the shared Q / KV buffers, its
+// output, its V-source block table, and the first CTA of its (query tile,
+// head) grid (1-D over all jobs).  Passed by value in the kernel parameters.
+constexpr int kMaxVarJobs = 24;
+struct VarJob {
+  int n_new, n_cached, q_row0, kv_row0, cta0, q_groups, v_src_tiles;
+  const int64_t* v_blk_off;
+  int64_t v_layer_row;
+  __nv_bfloat16* out;
+};
+struct VarJobs {
+  int n;   // 0: not a varlen launch
+  VarJob j[kMaxVarJobs];
 };
 
 // Where KV tile t's V rows come from: (use the V-source map?, row coordinate).
@@ -225,7 +242,8 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v,
-                    const __grid_constant__ CUtensorMap tm_vs, const AttnParams p) {
+                    const __grid_constant__ CUtensorMap tm_vs, const AttnParams p,
+                    const __grid_constant__ VarJobs vj) {
   using C = Cfg<HD, kAllowPair>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -246,8 +264,31 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int h = blockIdx.y;  // q-head; the kv head when packed
-  const int split = blockIdx.z;
+  // this CTA's job: the launch's only one, or (varlen) the batch job owning
+  // blockIdx.x, with its rows' offsets in the shared Q / KV buffers
+  int bx = blockIdx.x, h = blockIdx.y, split = blockIdx.z;
+  int n_new = n_new, n_cached = n_cached, q_row0 = 0, kv_row0 = 0;
+  __nv_bfloat16* out_base = p.out;
+  int v_src_tiles = p.v_src_tiles;
+  const int64_t* v_blk_off = p.v_blk_off;
+  int64_t v_layer_row = p.v_layer_row;
+  if (vj.n > 0) {
+    int jb = 0;
+    while (jb + 1 < vj.n && vj.j[jb + 1].cta0 <= (int)blockIdx.x) ++jb;
+    const VarJob& J = vj.j[jb];
+    const int local = blockIdx.x - J.cta0;
+    bx = local % J.q_groups;
+    h = local / J.q_groups;
+    split = 0;
+    n_new = J.n_new;
+    n_cached = J.n_cached;
+    q_row0 = J.q_row0;
+    kv_row0 = J.kv_row0;
+    out_base = J.out;
+    v_src_tiles = J.v_src_tiles;
+    v_blk_off = J.v_blk_off;
+    v_layer_row = J.v_layer_row;
+  }
   const int pack = p.pack;
   const int kh = pack > 1 ? h : h / p.group;
   if (threadIdx.x == 0) ATTN_TRACE(0);
@@ -255,20 +296,20 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
   // Query rows of this CTA's row space: tokens of q-head h, or -- GQA packing --
   // the (token, q-head) pairs of kv head h, row = token * pack + head-in-group,
   // so one K/V tile serves 128 rows of every q-head sharing it.
-  const int q_rows = pack > 1 ? p.n_new * pack : p.n_new;
+  const int q_rows = pack > 1 ? n_new * pack : n_new;
   auto tok = [&](int row) { return pack > 1 ? row / pack : row; };
   auto out_row = [&](int row) -> int64_t {  // (token, q-head) index into [n_new][hq]
     return pack > 1 ? (int64_t)(row / pack) * p.hq + h * pack + row % pack
                     : (int64_t)row * p.hq + h;
   };
   // query tiles of this CTA: A at q0, B at q0 + 128 (paired only)
-  const int q0 = blockIdx.x * kBM * C::kQTiles;
+  const int q0 = bx * kBM * C::kQTiles;
   const int rows_a = min(kBM, q_rows - q0);
   const int rows_b = kAllowPair ? max(0, min(kBM, q_rows - q0 - kBM)) : 0;
   // CTA-uniform mode: paired when this CTA really has two query tiles
   const bool paired = rows_b > 0;
   const int last_row = q0 + (rows_b > 0 ? kBM + rows_b : rows_a) - 1;
-  const int kv_end = p.n_cached + tok(last_row) + 1;
+  const int kv_end = n_cached + tok(last_row) + 1;
   const int tiles_total = (kv_end + kBN - 1) / kBN;
   const int t_begin = split * p.tiles_per_split;
   const int t_end = min(tiles_total, t_begin + p.tiles_per_split);
@@ -278,7 +319,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
   // n_cached + q0 + rows_a - 1, so A uses a prefix of the split's tiles
   int nt_a = n_tiles, nt_b = 0;
   if (paired) {
-    const int last_a = (p.n_cached + tok(q0 + rows_a - 1)) / kBN;
+    const int last_a = (n_cached + tok(q0 + rows_a - 1)) / kBN;
     nt_a = max(0, min(n_tiles, last_a + 1 - t_begin));
     nt_b = rows_b > 0 ? n_tiles : 0;
   }
@@ -289,7 +330,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
       const int g = paired ? (warp >> 2) : 0;
       const int rows = g ? rows_b : rows_a;
       if ((paired || warp < 4) && r < rows) {
-        const int64_t row = (int64_t)split * p.n_new * p.hq + out_row(q0 + g * kBM + r);
+        const int64_t row = (int64_t)split * n_new * p.hq + out_row(q0 + g * kBM + r);
         p.part_lse[row] = -INFINITY;
         float4* po = reinterpret_cast<float4*>(p.part_o + row * HD);
 #pragma unroll
@@ -346,7 +387,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
 #pragma unroll
         for (int c = 0; c < C::kChunks; ++c)
           tma_load_3d_hint(sQ + t * C::kTileBytes + c * (kBM * 128), &tm_q, q_full, c * 64,
-                           pack > 1 ? h * pack : h, tok(q0 + t * kBM), pol_q);
+                           pack > 1 ? h * pack : h, q_row0 + tok(q0 + t * kBM), pol_q);
       // K tiles: as far ahead as the K ring allows (S(j) needs K(j) well before
       // PV(j) needs V(j)); V tiles come from warp 10, so a V slot still held by
       // a PV in flight never delays the next K (in-kernel trace: with one
@@ -358,7 +399,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
 #pragma unroll
         for (int c = 0; c < C::kChunks; ++c)
           tma_load_3d_hint(sK + st * C::kTileBytes + c * (kBN * 128), &tm_k, &k_full[st],
-                           c * 64, kh, (t_begin + jk) * kBN, pol_kv);
+                           c * 64, kh, kv_row0 + (t_begin + jk) * kBN, pol_kv);
       }
     }
   } else if (warp == 10) {
@@ -370,8 +411,11 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
         const int st = jv % C::kVStages;
         if (jv >= C::kVStages) mbar_wait(&v_empty[st], ((jv / C::kVStages) - 1) & 1);
         mbar_expect_tx(&v_full[st], C::kTileBytes);
-        bool vs;
-        const int vrow = v_tile_row(p, t_begin + jv, vs);
+        const int tv = t_begin + jv;
+        const bool vs = tv < v_src_tiles;
+        const int vrow = !vs ? kv_row0 + tv * kBN
+                         : v_blk_off ? (int)(v_blk_off[tv] / p.v_row_elems + v_layer_row)
+                                     : (int)(p.v_src_row0 + (int64_t)tv * kBN);
 #pragma unroll
         for (int c = 0; c < C::kChunks; ++c)
           tma_load_3d_hint(sV + st * C::kTileBytes + c * (kBN * 128), vs ? &tm_vs : &tm_v,
@@ -477,7 +521,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
     const uint32_t t_s = tmem + lane_off + C::col_s(w);
     const uint32_t t_o = tmem + lane_off + C::col_o(w);
     const int qt0 = q0 + (paired ? w * kBM : 0);  // first query of this group's tile
-    const int row_limit = p.n_cached + tok(qt0 + r);
+    const int row_limit = n_cached + tok(qt0 + r);
     const float sl2 = p.scale_log2;
     const int my_tiles = paired ? (w ? nt_b : nt_a) : (n_tiles - w + 1) / 2;
     float m_acc = -INFINITY, l_acc = 0.f;
@@ -575,7 +619,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
       tc_fence_after();
       const int kbase = (t_begin + j) * kBN;
       // group-uniform: does any row of this tile see a masked column here?
-      if (kbase + kBN - 1 > p.n_cached + tok(qt0))
+      if (kbase + kBN - 1 > n_cached + tok(qt0))
         tile(std::true_type{}, t, row_limit - kbase);
       else
         tile(std::false_type{}, t, 0);
@@ -628,7 +672,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
       }
       if (r < rows_g) {
         if (!partial) {
-          __nv_bfloat16* dst = p.out + out_row(qi) * HD + col;
+          __nv_bfloat16* dst = out_base + out_row(qi) * HD + col;
 #pragma unroll
           for (int e = 0; e < 32; e += 8) {
             uint4 v;
@@ -639,7 +683,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
             *reinterpret_cast<uint4*>(dst + e) = v;
           }
         } else {
-          const int64_t row = (int64_t)split * p.n_new * p.hq + out_row(qi);
+          const int64_t row = (int64_t)split * n_new * p.hq + out_row(qi);
           float4* po = reinterpret_cast<float4*>(p.part_o + row * HD + col);
 #pragma unroll
           for (int e = 0; e < 32; e += 4)
@@ -1511,8 +1555,10 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
       if (e != cudaSuccess) return cuda_status(e, "attn smem attribute");
       attr = true;
     }
+    VarJobs none;
+    none.n = 0;
     kern<<<grid, Cfg<HD, true>::kThreads, Cfg<HD, true>::kSmemBytes, stream>>>(mq, mk, mv, mvs,
-                                                                                prm);
+                                                                                prm, none);
   } else {
     auto kern = attn_fwd_kernel<HD, false>;
     static bool attr = false;
@@ -1522,8 +1568,10 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
       if (e != cudaSuccess) return cuda_status(e, "attn smem attribute");
       attr = true;
     }
+    VarJobs none;
+    none.n = 0;
     kern<<<grid, Cfg<HD, false>::kThreads, Cfg<HD, false>::kSmemBytes, stream>>>(mq, mk, mv,
-                                                                                 mvs, prm);
+                                                                                 mvs, prm, none);
   }
   rc = launch_status("attn_fwd launch");
   if (rc || splits == 1) return rc;
@@ -1531,6 +1579,72 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
   attn_combine_kernel<HD><<<(rows_qh + 3) / 4, 128, 0, stream>>>(
       prm.part_o, prm.part_lse, splits, rows_qh, static_cast<__nv_bfloat16*>(out), stamp);
   return launch_status("attn_combine launch");
+}
+
+template <int HD>
+int launch_varlen(const VarlenBatch& b, cudaStream_t stream, unsigned long long* stamp) {
+  const int hq = b.hq, hkv = b.hkv;
+  const int pack = gqa_pack(hq, hkv);
+  const int heads = pack > 1 ? hkv : hq;
+  int q_tot = 0, kv_tot = 0;
+  for (int i = 0; i < b.n; ++i) {
+    q_tot = std::max(q_tot, b.q_row0[i] + b.n_new[i]);
+    kv_tot = std::max(kv_tot, b.kv_row0[i] + b.n_cached[i] + b.n_new[i]);
+  }
+  CUtensorMap mq, mk, mv, mvs;
+  int rc = make_map(&mq, b.q, HD, hq, HD, q_tot, (int64_t)hq * HD, pack);
+  if (!rc) rc = make_map(&mk, b.kv, HD, hkv, HD, kv_tot, b.kv_row_stride);
+  if (!rc)
+    rc = make_map(&mv, static_cast<const __nv_bfloat16*>(b.kv) + (int64_t)hkv * HD, HD, hkv, HD,
+                  kv_tot, b.kv_row_stride);
+  const bool use_vs = b.vsrc_base != nullptr;
+  if (!rc && use_vs)
+    rc = make_map(&mvs, static_cast<const __nv_bfloat16*>(b.vsrc_base) + (int64_t)hkv * HD, HD,
+                  hkv, HD, b.vsrc_rows, b.vsrc_row_elems);
+  if (rc) return rc;
+  if (!use_vs) mvs = mv;
+  AttnParams prm{};
+  prm.hq = hq;
+  prm.group = hq / hkv;
+  prm.pack = pack;
+  prm.num_splits = 1;
+  prm.tiles_per_split = 1 << 20;
+  prm.scale_log2 = b.scale * 1.4426950408889634f;
+  prm.stamp = stamp;
+  prm.v_row_elems = use_vs ? b.vsrc_row_elems : 1;
+  auto kern = attn_fwd_kernel<HD, false>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg<HD, false>::kSmemBytes);
+    if (e != cudaSuccess) return cuda_status(e, "attn smem attribute");
+    attr = true;
+  }
+  for (int i0 = 0; i0 < b.n; i0 += kMaxVarJobs) {   // <= kMaxVarJobs jobs per launch
+    VarJobs vj;
+    vj.n = std::min(kMaxVarJobs, b.n - i0);
+    int ctas = 0;
+    for (int k = 0; k < vj.n; ++k) {
+      const int i = i0 + k;
+      VarJob& J = vj.j[k];
+      J.n_new = b.n_new[i];
+      J.n_cached = b.n_cached[i];
+      J.q_row0 = b.q_row0[i];
+      J.kv_row0 = b.kv_row0[i];
+      J.cta0 = ctas;
+      J.q_groups = (b.n_new[i] * pack + kBM - 1) / kBM;
+      J.v_src_tiles = use_vs ? b.v_src_tiles[i] : 0;
+      J.v_blk_off = use_vs ? b.v_blk_off[i] : nullptr;
+      J.v_layer_row = b.v_layer_row;
+      J.out = static_cast<__nv_bfloat16*>(b.out[i]);
+      ctas += J.q_groups * heads;
+    }
+    kern<<<ctas, Cfg<HD, false>::kThreads, Cfg<HD, false>::kSmemBytes, stream>>>(mq, mk, mv, mvs,
+                                                                                 prm, vj);
+    rc = launch_status("attn_fwd varlen launch");
+    if (rc) return rc;
+  }
+  return ASKV_OK;
 }
 
 }  // namespace
@@ -1613,4 +1727,16 @@ int askv::prefill_attn_stamped(const void* q, const void* kv, int64_t kv_row_str
                             vsrc);
   return launch_attn<64>(q, kv, kv_row_stride, n_cached, n_new, n_heads, n_kv_heads, scale, out,
                          workspace, workspace_bytes, splits, (cudaStream_t)stream, stamp, vsrc);
+}
+
+int askv::prefill_attn_varlen(const VarlenBatch& b, void* stream, unsigned long long* stamp) {
+  ASKV_REQUIRE(b.n >= 1 && b.hq > 0 && b.hkv > 0 && b.hq % b.hkv == 0,
+               "prefill_attn_varlen: bad batch");
+  ASKV_REQUIRE(b.head_dim == 64 || b.head_dim == 128, "prefill_attn_varlen: head_dim %d",
+               b.head_dim);
+  for (int i = 0; i < b.n; ++i)
+    ASKV_REQUIRE(b.n_new[i] > 0 && b.n_cached[i] >= 0 && b.out[i],
+                 "prefill_attn_varlen: job %d", i);
+  if (b.head_dim == 128) return launch_varlen<128>(b, (cudaStream_t)stream, stamp);
+  return launch_varlen<64>(b, (cudaStream_t)stream, stamp);
 }

@@ -456,7 +456,7 @@ extern "C" int askv_gemm(const void* x, const void* w, void* y, int n, int m, in
               (cudaStream_t)stream);
 }
 
-static int issue_layers(const askv_prefill_plan* p, cudaStream_t s);
+static int issue_layers_multi(const askv_prefill_plan* ps, int nj, cudaStream_t s);
 
 // Row-parallel output projection + NCCL sum into the residual stream:
 // rank 0: x = x + in W^T (GEMM epilogue), then in-place all-reduce of x;
@@ -469,10 +469,8 @@ static int tp_out_proj(const askv_prefill_plan* p, const void* in, const void* w
   return tp_allreduce_bf16(r0 ? p->x : p->h, p->x, (int64_t)n * d, p->nccl_comm, s);
 }
 
-extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
-  clear_error();
-  ASKV_REQUIRE(p != nullptr, "prefill_layers: null plan");
-  cudaStream_t s = (cudaStream_t)stream;
+static int prefill_multi(const askv_prefill_plan* ps, int nj, cudaStream_t s) {
+  const askv_prefill_plan* p = ps;
   // Graph issue: one launch per job instead of ~11 per layer.  While the
   // pre-loader saturates the host link, every stream launch's command fetch
   // queues behind the H2D DMA and the GPU idles between kernels
@@ -481,15 +479,15 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
   // on the stream instead (same kernels, same order).  A tensor-parallel
   // host callback issues on the stream (a host function cannot be captured);
   // the HBM-tier copies are captured (graph_key counts their segments).
-  if (!p->graph || p->allreduce) return issue_layers(p, s);
+  if (!p->graph || p->allreduce) return issue_layers_multi(ps, nj, s);
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
-    return issue_layers(p, s);  // caller is capturing already: record into its graph
+    return issue_layers_multi(ps, nj, s);  // caller is capturing already: record into its graph
   int rc = cuda_status(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed),
                        "cudaStreamBeginCapture");
   if (rc != ASKV_OK) return rc;
   g_capturing = true;
-  rc = issue_layers(p, s);
+  rc = issue_layers_multi(ps, nj, s);
   g_capturing = false;
   cudaGraph_t g = nullptr;
   const cudaError_t ec = cudaStreamEndCapture(s, &g);
@@ -500,9 +498,14 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
   if (ec != cudaSuccess) {  // capture invalidated: issue on the stream
     cudaGetLastError();
     if (g) cudaGraphDestroy(g);
-    return issue_layers(p, s);
+    return issue_layers_multi(ps, nj, s);
   }
-  const auto key = graph_key(p, s);
+  auto key = graph_key(p, s);
+  key.push_back(nj);
+  for (int i = 1; i < nj; ++i) {
+    const auto ki = graph_key(ps + i, s);
+    key.insert(key.end(), ki.begin(), ki.end());
+  }
   std::lock_guard<std::mutex> lk(g_graph_mu);
   sweep_retired();
   auto it = g_graphs.find(key);
@@ -533,7 +536,7 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
       cudaGraphDestroy(g);
       cudaGetLastError();
       clear_error();
-      return issue_layers(p, s);
+      return issue_layers_multi(ps, nj, s);
     }
     it = g_graphs.emplace(key, e).first;
   }
@@ -542,6 +545,19 @@ extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
   rc = cuda_status(cudaGraphLaunch(it->second.exec, s), "cudaGraphLaunch");
   if (rc == ASKV_OK) rc = cuda_status(cudaEventRecord(it->second.done, s), "cudaEventRecord");
   return rc;
+}
+
+extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {
+  clear_error();
+  ASKV_REQUIRE(p != nullptr, "prefill_layers: null plan");
+  return prefill_multi(p, 1, (cudaStream_t)stream);
+}
+
+extern "C" int askv_prefill_layers_batch(const askv_prefill_plan* plans, int njobs,
+                                         void* stream) {
+  clear_error();
+  ASKV_REQUIRE(plans != nullptr && njobs >= 1, "prefill_layers_batch: no jobs");
+  return prefill_multi(plans, njobs, (cudaStream_t)stream);
 }
 
 namespace askv {
@@ -573,29 +589,70 @@ SideCtx* side_ctx(int layers) {
 }  // namespace
 }  // namespace askv
 
-static int issue_layers(const askv_prefill_plan* p, cudaStream_t s) {
-  ASKV_REQUIRE(p->layers > 0 && p->n_new > 0 && p->kept >= 0 && p->head >= 0,
-               "prefill_layers: bad layers=%d n_new=%d kept=%d", p->layers, p->n_new, p->kept);
-  ASKV_REQUIRE(p->w_in && p->w_qkv && p->w_o && p->w_post && p->w_gu && p->w_down,
-               "prefill_layers: missing weight arrays");
-  ASKV_REQUIRE(p->kept == 0 || ((p->src_kind == 1 || p->src_kind == 2) && p->src_layer) ||
-                   (p->src_kind == 0 && p->kv_layers),
-               "prefill_layers: kept rows need a source (or resident kv_layers)");
-  const int n = p->n_new, d = p->d_model, hq = p->n_heads, hkv = p->n_kv_heads,
-            hd = p->head_dim, f = p->ffn;
+// Per-job facts the loop needs (one job, or each job of a batch).
+struct JobView {
+  const askv_prefill_plan* p;
+  bool reemb, vs_on, waits;
+  int vs_tiles;
+};
+
+// nj jobs share one pass over the layers: the norms, projections and MLP run
+// once over the jobs' concatenated tokens (their x / h / qkv / q_rot /
+// attn_out / gu / act buffers are consecutive slices of job 0's), while
+// rope_new, the pre-load wait, K2 and K3 run per job on its own rows.  nj = 1
+// is the single-job loop.
+static int issue_layers_multi(const askv_prefill_plan* ps, int nj, cudaStream_t s) {
+  const askv_prefill_plan* p = ps;  // job 0: the shared buffers and the timeline
+  ASKV_REQUIRE(nj >= 1, "prefill_layers: no jobs");
+  int n = 0;
+  for (int i = 0; i < nj; ++i) {
+    const askv_prefill_plan* q = ps + i;
+    ASKV_REQUIRE(q->layers > 0 && q->n_new > 0 && q->kept >= 0 && q->head >= 0,
+                 "prefill_layers: bad layers=%d n_new=%d kept=%d", q->layers, q->n_new,
+                 q->kept);
+    ASKV_REQUIRE(q->w_in && q->w_qkv && q->w_o && q->w_post && q->w_gu && q->w_down,
+                 "prefill_layers: missing weight arrays");
+    ASKV_REQUIRE(q->kept == 0 || ((q->src_kind == 1 || q->src_kind == 2) && q->src_layer) ||
+                     (q->src_kind == 0 && q->kv_layers),
+                 "prefill_layers: kept rows need a source (or resident kv_layers)");
+    if (i > 0) {
+      const int64_t d = p->d_model;
+      const int64_t qc = (int64_t)(p->n_heads + 2 * p->n_kv_heads) * p->head_dim;
+      auto at = [&](const void* base, int64_t cols) {
+        return static_cast<const char*>(base) + (int64_t)n * cols * 2;
+      };
+      ASKV_REQUIRE(q->layers == p->layers && q->d_model == p->d_model &&
+                       q->n_heads == p->n_heads && q->n_kv_heads == p->n_kv_heads &&
+                       q->head_dim == p->head_dim && q->ffn == p->ffn &&
+                       q->w_qkv == p->w_qkv && q->w_o == p->w_o && q->w_gu == p->w_gu &&
+                       q->w_down == p->w_down && q->w_in == p->w_in && q->w_post == p->w_post,
+                   "prefill_layers: batched jobs must share the model");
+      ASKV_REQUIRE(q->x == at(p->x, d) && q->h == at(p->h, d) && q->qkv == at(p->qkv, qc) &&
+                       q->q_rot == at(p->q_rot, (int64_t)p->n_heads * p->head_dim) &&
+                       q->attn_out == at(p->attn_out, (int64_t)p->n_heads * p->head_dim) &&
+                       q->gu == at(p->gu, 2LL * p->ffn) && q->act == at(p->act, p->ffn),
+                   "prefill_layers: batched jobs' activations must be consecutive slices");
+      ASKV_REQUIRE(!q->allreduce && !q->nccl_comm && !q->kv_alt,
+                   "prefill_layers: batched jobs cannot be tensor parallel or overlapped");
+    }
+    n += q->n_new;
+  }
+  ASKV_REQUIRE(nj == 1 || (!p->allreduce && !p->nccl_comm && !p->kv_alt),
+               "prefill_layers: batched jobs cannot be tensor parallel or overlapped");
+  const int d = p->d_model, hq = p->n_heads, hkv = p->n_kv_heads, hd = p->head_dim,
+            f = p->ffn;
   const int qkv_cols = (hq + 2 * hkv) * hd;
   const int64_t row = 2LL * hkv * hd;
   // Timeline stamps ride on the kernels that bound each interval (no extra
   // launches): loop begin / previous layer end = start of the layer's input
   // rmsnorm, pre-load wait begin = end of rope_new, wait end = start of K2;
-  // one stamp kernel marks the end of the last layer.
+  // one stamp kernel marks the end of the last layer.  The layer timeline is
+  // job 0's; every job keeps its own K2 / K3 probe stamps.
   const bool tl = p->stamps && (p->stamp_flags & 1);
-  auto ts = [&](int idx) -> unsigned long long* {
-    return reinterpret_cast<unsigned long long*>(p->stamps + idx);
+  auto ts_of = [](const askv_prefill_plan* q, int idx) -> unsigned long long* {
+    return reinterpret_cast<unsigned long long*>(q->stamps + idx);
   };
-  const bool reemb = p->kept > 0 && p->src_kind != 0;
-  const bool ovl = p->kv_alt && !p->kv_layers && reemb && !p->promote_base && !p->allreduce &&
-                   !p->nccl_comm;
+  auto ts = [&](int idx) { return ts_of(p, idx); };
   // K3 reads the V of the kept rows' whole tiles from the pre-load source
   // (ASKV_VSRC=0 turns it off: K2 then copies every V row, the round-1 path)
   static int vsrc_knob = -1;
@@ -603,59 +660,100 @@ static int issue_layers(const askv_prefill_plan* p, cudaStream_t s) {
     const char* e = getenv("ASKV_VSRC");
     vsrc_knob = (e && e[0] == '0') ? 0 : 1;
   }
-  const bool vs_on = vsrc_knob && reemb && !p->kv_layers && !ovl && p->src_rows > 0 &&
-                     (p->src_kind == 1 ||
-                      (p->src_kind == 2 && p->head == 0 && p->block_tokens == 128));
-  const int vs_tiles = vs_on ? p->kept / 128 : 0;
+  const bool ovl = nj == 1 && p->kv_alt && !p->kv_layers && p->kept > 0 && p->src_kind != 0 &&
+                   !p->promote_base && !p->allreduce && !p->nccl_comm;
+  std::vector<JobView> jv(nj);
+  for (int i = 0; i < nj; ++i) {
+    const askv_prefill_plan* q = ps + i;
+    JobView& v = jv[i];
+    v.p = q;
+    v.reemb = q->kept > 0 && q->src_kind != 0;
+    v.vs_on = vsrc_knob && v.reemb && !q->kv_layers && !ovl && q->src_rows > 0 &&
+              (q->src_kind == 1 || (q->src_kind == 2 && q->head == 0 && q->block_tokens == 128));
+    v.vs_tiles = v.vs_on ? q->kept / 128 : 0;
+    v.waits = q->stamps && (q->stamp_flags & 1) && v.reemb && q->ev_src_ready;
+  }
+  // One K3 launch for a batch (ASKV_VARLEN=0: one per job): needs the jobs'
+  // KV rows consecutive in job 0's buffer and no per-job read-buffer slot as
+  // V source (host-sourced jobs keep their V in their own slots)
+  static int varlen_knob = -1;
+  if (varlen_knob < 0) {
+    const char* e = getenv("ASKV_VARLEN");
+    varlen_knob = (e && e[0] == '0') ? 0 : 1;
+  }
+  bool varlen = varlen_knob && nj > 1;
+  {
+    const char* kv0 = static_cast<const char*>(p->kv);
+    int64_t rows_before = 0;
+    const void* vbase = nullptr;
+    for (int i = 0; i < nj && varlen; ++i) {
+      const JobView& v = jv[i];
+      const askv_prefill_plan* q = v.p;
+      if (q->kv_layers || !q->kv || (v.vs_on && q->src_kind == 1) ||
+          static_cast<const char*>(q->kv) != kv0 + rows_before * row * 2)
+        varlen = false;
+      if (v.vs_on) {
+        if (vbase && vbase != q->src_layer[0]) varlen = false;
+        vbase = q->src_layer[0];
+      }
+      rows_before += q->kept + q->n_new;
+    }
+  }
   SideCtx* sc = ovl ? side_ctx(p->layers) : nullptr;
   if (ovl && !sc) {
     set_error("prefill_layers: side stream / events for the K2 overlap");
     return ASKV_ECUDA;
   }
-  auto kv_of = [&](int l) {
-    return static_cast<__nv_bfloat16*>(p->kv_layers ? p->kv_layers[l]
-                                       : (ovl && (l & 1)) ? p->kv_alt : p->kv);
+  auto kv_of = [&](const askv_prefill_plan* q, int l) {
+    return static_cast<__nv_bfloat16*>(q->kv_layers ? q->kv_layers[l]
+                                       : (ovl && (l & 1)) ? q->kv_alt : q->kv);
   };
-  // K2 of layer l on stream `ks`: wait for its pre-load, re-embed, release the slot
-  auto issue_k2 = [&](int l, cudaStream_t ks, unsigned long long* k2_st) -> int {
-    wait(p->ev_src_ready, l, ks);
-    if (p->src_kind == 1) {
-      ASKV_TRY(reembed_stamped(p->src_layer[l], nullptr, 0, p->src_row_stride, p->head,
-                               p->kept, hkv, hd, p->rope_table, p->rope_positions, nullptr, 0,
-                               kv_of(l), row, ks, k2_st, vs_tiles * 128));
+  // K2 of layer l on stream `ks`: wait for its pre-load, re-embed
+  auto issue_k2 = [&](const JobView& v, int l, cudaStream_t ks,
+                      unsigned long long* k2_st) -> int {
+    const askv_prefill_plan* q = v.p;
+    wait(q->ev_src_ready, l, ks);
+    if (q->src_kind == 1) {
+      ASKV_TRY(reembed_stamped(q->src_layer[l], nullptr, 0, q->src_row_stride, q->head,
+                               q->kept, hkv, hd, q->rope_table, q->rope_positions, nullptr, 0,
+                               kv_of(q, l), row, ks, k2_st, v.vs_tiles * 128));
     } else {
-      ASKV_TRY(reembed_stamped(p->src_layer[l], p->src_block_off, p->block_tokens,
-                               p->src_row_stride, p->head, p->kept, hkv, hd, p->rope_table,
-                               p->rope_positions, nullptr, 0, kv_of(l), row, ks, k2_st,
-                               vs_tiles * 128));
+      ASKV_TRY(reembed_stamped(q->src_layer[l], q->src_block_off, q->block_tokens,
+                               q->src_row_stride, q->head, q->kept, hkv, hd, q->rope_table,
+                               q->rope_positions, nullptr, 0, kv_of(q, l), row, ks, k2_st,
+                               v.vs_tiles * 128));
     }
     return ASKV_OK;
   };
   if (ovl) {  // fork the side stream; layer 0's K2 starts right away
     cudaEventRecord(sc->ev[0], s);
     cudaStreamWaitEvent(sc->s2, sc->ev[0], 0);
-    ASKV_TRY(issue_k2(0, sc->s2, (p->stamp_flags & 2) && p->stamps ? ts(1 + 3) : nullptr));
+    ASKV_TRY(issue_k2(jv[0], 0, sc->s2,
+                      (p->stamp_flags & 2) && p->stamps ? ts(1 + 3) : nullptr));
     rec(p->ev_src_free, 0, sc->s2);
     cudaEventRecord(sc->ev[2], sc->s2);  // k2_done[0]
   }
   for (int l = 0; l < p->layers; ++l) {
-    auto* kv = kv_of(l);
     const int st = 1 + 7 * l;
     ASKV_TRY(rmsnorm_stamped(p->x, p->w_in[l], p->h, n, d, p->rms_eps, s,
                              tl ? ts(l == 0 ? 0 : st - 7) : nullptr));
     ASKV_TRY(gemm(p->h, p->w_qkv[l], p->qkv, n, qkv_cols, d, false, p->gemm_ws,
                   p->gemm_ws_bytes, s));
-    void* save_rows = p->save_rows ? p->save_rows[l] : nullptr;
-    if (save_rows) wait(p->ev_save_free, l, s);
-    const bool waits = tl && reemb && p->ev_src_ready;
-    ASKV_TRY(rope_new_stamped(p->qkv, qkv_cols, n, hq, hkv, hd, p->rope_table,
-                              p->rope_positions, p->kept, p->q_rot, kv + (int64_t)p->kept * row,
-                              row, save_rows, s, waits ? ts(st + 1) : nullptr));
-    if (save_rows) rec(p->ev_save_ready, l, s);
-    if (save_rows && p->mirror_base) {  // HBM tier write-through, in stream order
-      ASKV_TRY(askv_save_layer(p->mirror_base, p->mirror_block_ids, p->mirror_nblocks,
-                               p->block_bytes, (int64_t)l * p->chunk_bytes, p->block_tokens,
-                               p->row_bytes, p->head + p->kept, n, save_rows, s, nullptr));
+    for (const JobView& v : jv) {  // new tokens: rotate q / k, pre-RoPE rows for the saver
+      const askv_prefill_plan* q = v.p;
+      const int nq = q->n_new;
+      void* save_rows = q->save_rows ? q->save_rows[l] : nullptr;
+      if (save_rows) wait(q->ev_save_free, l, s);
+      ASKV_TRY(rope_new_stamped(q->qkv, qkv_cols, nq, hq, hkv, hd, q->rope_table,
+                                q->rope_positions, q->kept, q->q_rot,
+                                kv_of(q, l) + (int64_t)q->kept * row, row, save_rows, s,
+                                v.waits ? ts_of(q, st + 1) : nullptr));
+      if (save_rows) rec(q->ev_save_ready, l, s);
+      if (save_rows && q->mirror_base) {  // HBM tier write-through, in stream order
+        ASKV_TRY(askv_save_layer(q->mirror_base, q->mirror_block_ids, q->mirror_nblocks,
+                                 q->block_bytes, (int64_t)l * q->chunk_bytes, q->block_tokens,
+                                 q->row_bytes, q->head + q->kept, nq, save_rows, s, nullptr));
+      }
     }
     if (ovl) {
       // K2(l) ran on the side stream; K2(l+1) starts alongside K3(l) (its KV
@@ -664,43 +762,100 @@ static int issue_layers(const askv_prefill_plan* p, cudaStream_t s) {
       cudaEventRecord(sc->ev[3 + 2 * l], s);
       if (l + 1 < p->layers) {
         cudaStreamWaitEvent(sc->s2, sc->ev[3 + 2 * l], 0);
-        ASKV_TRY(issue_k2(l + 1, sc->s2,
+        ASKV_TRY(issue_k2(jv[0], l + 1, sc->s2,
                           (p->stamp_flags & 2) && p->stamps ? ts(st + 7 + 3) : nullptr));
         rec(p->ev_src_free, l + 1, sc->s2);
         cudaEventRecord(sc->ev[2 + 2 * (l + 1)], sc->s2);
       }
-    } else if (reemb) {
-      // K2's own {first CTA begin, last CTA end} into stamps[st + 3 .. 4]:
-      // the probes' K2 interval, and its begin is the pre-load wait's end
-      unsigned long long* k2_st =
-          (p->stamps && ((p->stamp_flags & 2) || waits)) ? ts(st + 3) : nullptr;
-      ASKV_TRY(issue_k2(l, s, k2_st));
-      if (p->promote_base) {  // HBM tier: keep the pre-loaded rows resident
-        const auto* src = static_cast<const char*>(p->src_layer[l]) +
-                          (int64_t)p->head * p->row_bytes;
-        ASKV_TRY(askv_save_layer(p->promote_base, p->promote_block_ids, p->promote_nblocks,
-                                 p->block_bytes, (int64_t)l * p->chunk_bytes, p->block_tokens,
-                                 p->row_bytes, p->head, p->kept, src, s, nullptr));
+    } else {
+      for (const JobView& v : jv) {
+        if (!v.reemb) continue;
+        const askv_prefill_plan* q = v.p;
+        // K2's own {first CTA begin, last CTA end} into stamps[st + 3 .. 4]:
+        // the probes' K2 interval, and its begin is the pre-load wait's end
+        unsigned long long* k2_st =
+            (q->stamps && ((q->stamp_flags & 2) || v.waits)) ? ts_of(q, st + 3) : nullptr;
+        ASKV_TRY(issue_k2(v, l, s, k2_st));
+        if (q->promote_base) {  // HBM tier: keep the pre-loaded rows resident
+          const auto* src = static_cast<const char*>(q->src_layer[l]) +
+                            (int64_t)q->head * q->row_bytes;
+          ASKV_TRY(askv_save_layer(q->promote_base, q->promote_block_ids, q->promote_nblocks,
+                                   q->block_bytes, (int64_t)l * q->chunk_bytes,
+                                   q->block_tokens, q->row_bytes, q->head, q->kept, src, s,
+                                   nullptr));
+        }
+        if (!(v.vs_on && q->src_kind == 1)) rec(q->ev_src_free, l, s);
       }
-      if (!(vs_on && p->src_kind == 1)) rec(p->ev_src_free, l, s);
     }
-    VSource vs;
-    if (vs_on) {
-      vs.kind = p->src_kind;
-      vs.tiles = vs_tiles;
-      vs.base = p->src_kind == 1 ? p->src_layer[l] : p->src_layer[0];
-      vs.rows = p->src_rows;
-      vs.row0 = p->head;
-      vs.blk_off = p->src_block_off;
-      vs.row_elems = p->src_row_stride;
-      vs.layer_row = (int64_t)l * p->block_tokens;
+    if (varlen) {  // one K3 launch for the whole batch: a (query tile, head) grid per job
+      std::vector<int> nn(nj), nc(nj), q0(nj), k0(nj), vt(nj);
+      std::vector<void*> outs(nj);
+      std::vector<const int64_t*> offs(nj);
+      const void* vbase = nullptr;
+      int64_t vrows = 0;
+      int qrow = 0;
+      for (int i = 0; i < nj; ++i) {
+        const JobView& v = jv[i];
+        const askv_prefill_plan* q = v.p;
+        nn[i] = q->n_new;
+        nc[i] = q->kept;
+        q0[i] = qrow;
+        qrow += q->n_new;
+        k0[i] = (int)((static_cast<const char*>(q->kv) - static_cast<const char*>(p->kv)) /
+                      (row * 2));
+        outs[i] = q->attn_out;
+        vt[i] = v.vs_on ? v.vs_tiles : 0;
+        offs[i] = v.vs_on ? q->src_block_off : nullptr;
+        if (v.vs_on && !vbase) {
+          vbase = q->src_layer[0];
+          vrows = q->src_rows;
+        }
+      }
+      VarlenBatch b;
+      b.n = nj;
+      b.q = p->q_rot;
+      b.kv = p->kv;
+      b.kv_row_stride = row;
+      b.hq = hq;
+      b.hkv = hkv;
+      b.head_dim = hd;
+      b.scale = p->attn_scale;
+      b.n_new = nn.data();
+      b.n_cached = nc.data();
+      b.q_row0 = q0.data();
+      b.kv_row0 = k0.data();
+      b.out = outs.data();
+      b.vsrc_base = vbase;
+      b.vsrc_rows = vrows;
+      b.vsrc_row_elems = p->src_row_stride;
+      b.v_layer_row = (int64_t)l * p->block_tokens;
+      b.v_src_tiles = vt.data();
+      b.v_blk_off = offs.data();
+      ASKV_TRY(prefill_attn_varlen(
+          b, s, (p->stamps && (p->stamp_flags & 2)) ? ts(st + 5) : nullptr));
     }
-    ASKV_TRY(prefill_attn_stamped(
-        p->q_rot, kv, row, p->kept, n, hq, hkv, hd, p->attn_scale, p->attn_out, p->attn_ws,
-        p->attn_ws_bytes, p->attn_splits, s,
-        (p->stamps && ((p->stamp_flags & 2) || (ovl && waits))) ? ts(st + 5) : nullptr,
-        vs_on ? &vs : nullptr));
-    if (vs_on && p->src_kind == 1) rec(p->ev_src_free, l, s);  // K3 read V from the slot
+    for (const JobView& v : jv) {  // K3 per job over [its kept rows | its new rows]
+      if (varlen) break;
+      const askv_prefill_plan* q = v.p;
+      VSource vs;
+      if (v.vs_on) {
+        vs.kind = q->src_kind;
+        vs.tiles = v.vs_tiles;
+        vs.base = q->src_kind == 1 ? q->src_layer[l] : q->src_layer[0];
+        vs.rows = q->src_rows;
+        vs.row0 = q->head;
+        vs.blk_off = q->src_block_off;
+        vs.row_elems = q->src_row_stride;
+        vs.layer_row = (int64_t)l * q->block_tokens;
+      }
+      ASKV_TRY(prefill_attn_stamped(
+          q->q_rot, kv_of(q, l), row, q->kept, q->n_new, hq, hkv, hd, q->attn_scale,
+          q->attn_out, q->attn_ws, q->attn_ws_bytes, q->attn_splits, s,
+          (q->stamps && ((q->stamp_flags & 2) || (ovl && v.waits))) ? ts_of(q, st + 5)
+                                                                      : nullptr,
+          v.vs_on ? &vs : nullptr));
+      if (v.vs_on && q->src_kind == 1) rec(q->ev_src_free, l, s);  // K3 read V in the slot
+    }
     if (p->nccl_comm) {
       // tensor parallel over NCCL: x = x + sum_r partial_r, the residual folded
       // into rank 0's GEMM epilogue, the sum landing in x on every rank

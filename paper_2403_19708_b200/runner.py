@@ -569,9 +569,16 @@ class Runner:
             pass
 
     # ------------------------------------------------------------------ main entry
-    def run(self, jobs: list[Job], *, want_logits: bool = False) -> list[JobResult]:
+    def run(self, jobs: list[Job], *, want_logits: bool = False,
+            batch: bool = False) -> list[JobResult]:
         """Issue all jobs back to back; returns results whose timelines are
-        resolved by ``finalize`` (call after synchronising)."""
+        resolved by ``finalize`` (call after synchronising).
+
+        batch=True: one pass over the layers for all jobs
+        (askv_prefill_layers_batch): projections / norms / MLP over the jobs'
+        concatenated new tokens, pre-load wait / K2 / K3 / saves per job.  A
+        scheduler knob -- throughput for time to first token: every job's
+        result carries the batch's timeline."""
         base = id(jobs)
         sids = [j.session_id for j in jobs]
         if len(set(sids)) != len(sids):
@@ -580,9 +587,69 @@ class Runner:
         for i, job in enumerate(jobs):
             self._enqueue_loads((base, i), job)
         results = []
-        for i, job in enumerate(jobs):
-            results.append(self._run_job((base, i), job, want_logits))
+        if batch and len(jobs) > 1:
+            results = self._run_batch(base, jobs, want_logits)
+        else:
+            for i, job in enumerate(jobs):
+                results.append(self._run_job((base, i), job, want_logits))
         self.drain_io()
+        return results
+
+    def _run_batch(self, base, jobs: list[Job], want_logits: bool) -> list[JobResult]:
+        s = self.shape
+        L = s.layers
+        if any(j.kv_cache is not None or j.source == "resident" for j in jobs):
+            raise ValueError("batched jobs cannot use a resident KV cache")
+        if self.tp_reduce is not None:
+            raise ValueError("batched jobs cannot be tensor parallel")
+        n_save = sum(1 for j in jobs if j.save)
+        if n_save * L > self.n_wslots:
+            raise ValueError(f"a batch of {n_save} saving jobs needs {n_save * L} write-buffer "
+                             f"slots ({self.n_wslots} allocated)")
+        ns = [j.n_new for j in jobs]
+        tot = sum(ns)
+        kv_rows = sum(j.kept + j.n_new for j in jobs)
+        hq, hd = s.n_heads, s.head_dim
+        big = {"x": self._buf("bx", tot, s.d_model), "h": self._buf("h", tot, s.d_model),
+               "qkv": self._buf("qkv", tot, s.qkv_cols), "q": self._buf("q", tot, hq * hd),
+               "ao": self._buf("ao", tot, hq * hd), "gu": self._buf("gu", tot, 2 * s.ffn),
+               "act": self._buf("act", tot, s.ffn), "kv": self._buf("kv", kv_rows, self.row_elems)}
+        plans, finishers, keep = [], [], []
+        row0, kv0 = 0, 0
+        probe0 = len(self.probe) if self.probe is not None else 0
+        # one K3 launch for the batch (csrc/runtime.cu, ASKV_VARLEN): unless a
+        # job reads its V from its own read-buffer slot (host source)
+        varlen = (os.environ.get("ASKV_VARLEN", "1") != "0"
+                  and not any(j.source == "host" and j.kept for j in jobs))
+        for i, job in enumerate(jobs):
+            sl = {k: v[row0:row0 + ns[i]] for k, v in big.items() if k != "kv"}
+            sl["kv"] = big["kv"][kv0:kv0 + job.kept + job.n_new]
+            p, fin, kp = self._run_job((base, i), job, want_logits, batch=sl)
+            plans.append(p)
+            finishers.append(fin)
+            keep.append(kp)
+            row0 += ns[i]
+            kv0 += job.kept + job.n_new
+        if varlen and self.probe is not None:
+            # the batch's K3 launch stamps job 0's slots: one probe entry per
+            # layer carrying every job's FLOPs
+            mine = self.probe[probe0:]
+            att = [e for e in mine if e[0] == "attention"]
+            per_layer = {}
+            for e in att:
+                per_layer[e[4]] = per_layer.get(e[4], 0) + e[6]
+            first = att[0][1] if att else None
+            kept_att = [e[:6] + (per_layer[e[4]], 0) for e in att if e[1] == first]
+            self.probe[probe0:] = [e for e in mine if e[0] != "attention"] + kept_att
+        arr = (_lib.PrefillPlan * len(plans))(*plans)
+        _lib.check(_lib.lib().askv_prefill_layers_batch(C.addressof(arr), len(plans),
+                                                        self.s_compute.cuda_stream),
+                   "prefill_layers_batch")
+        results = [fin() for fin in finishers]
+        lead = results[0]
+        for r in results[1:]:    # the layer timeline is the batch's (job 0's stamps)
+            r._batch_leader = lead
+        del keep
         return results
 
     def drain_io(self) -> None:
@@ -595,7 +662,7 @@ class Runner:
             if t.error is not None:
                 raise RuntimeError(f"{t.name} failed") from t.error
 
-    def _run_job(self, jid, job: Job, want_logits: bool) -> JobResult:
+    def _run_job(self, jid, job: Job, want_logits: bool, batch: dict | None = None):
         s = self.shape
         L = s.layers
         n, kept = job.n_new, job.kept
@@ -685,8 +752,14 @@ class Runner:
                 ids = ops.copy_sm(torch.empty(n, dtype=torch.int64, device=self.device),
                                   src.to(torch.int64), stream=cs)
                 self.launches += 1
-            x = F.embedding(ids, self.w.embed)
-            self._buf("h", n, s.d_model)
+            if batch is None:
+                x = F.embedding(ids, self.w.embed)
+                buf = lambda name, rows, cols: self._buf(name, rows, cols)  # noqa: E731
+            else:   # this job's rows of the batch's shared buffers
+                x = batch["x"]
+                torch.index_select(self.w.embed, 0, ids, out=x)
+                buf = lambda name, rows, cols: batch[name]  # noqa: E731
+            buf("h", n, s.d_model)
             splits = ops.attn_num_splits(kept, n, hq, n_kv_heads=hkv)
             wsb = ops.attn_workspace_bytes(kept, n, hq, hd, splits, n_kv_heads=hkv)
             ws = self._workspace(wsb) if wsb else None
@@ -699,22 +772,22 @@ class Runner:
             p.w_in, p.w_qkv, p.w_o = wa["w_in"], wa["wqkv"], wa["wo"]
             p.w_post, p.w_gu, p.w_down = wa["w_post"], wa["wgu"], wa["wd"]
             p.x = x.data_ptr()
-            p.h = self._bufs["h"].data_ptr()
-            p.qkv = self._buf("qkv", n, s.qkv_cols).data_ptr()
-            p.q_rot = self._buf("q", n, hq * hd).data_ptr()
+            p.h = buf("h", n, s.d_model).data_ptr()
+            p.qkv = buf("qkv", n, s.qkv_cols).data_ptr()
+            p.q_rot = buf("q", n, hq * hd).data_ptr()
             if job.kv_cache is not None:
                 if kept + n > job.kv_cache.capacity:
                     raise ValueError("context exceeds the resident KV capacity")
                 p.kv_layers = arr(job.kv_cache.layer_ptrs())
             else:
-                p.kv = self._buf("kv", kept + n, self.row_elems).data_ptr()
-                if (self.overlap and kept and job.source in ("host", "hbm")
+                p.kv = buf("kv", kept + n, self.row_elems).data_ptr()
+                if (batch is None and self.overlap and kept and job.source in ("host", "hbm")
                         and job.promote_block_ids is None and self.tp_reduce is None):
                     p.kv_alt = self._buf("kv2", kept + n, self.row_elems).data_ptr()
                     rec["overlap"] = True
-            p.attn_out = self._buf("ao", n, hq * hd).data_ptr()
-            p.gu = self._buf("gu", n, 2 * s.ffn).data_ptr()
-            p.act = self._buf("act", n, s.ffn).data_ptr()
+            p.attn_out = buf("ao", n, hq * hd).data_ptr()
+            p.gu = buf("gu", n, 2 * s.ffn).data_ptr()
+            p.act = buf("act", n, s.ffn).data_ptr()
             if ws is not None:
                 p.attn_ws, p.attn_ws_bytes = ws.data_ptr(), ws.numel()
             p.gemm_ws, p.gemm_ws_bytes = self._gemm_ws.data_ptr(), self._gemm_ws.numel()
@@ -791,10 +864,14 @@ class Runner:
                 p.nccl_comm, p.tp_rank = self._nccl.handle, self._nccl.rank
             p.graph = 1 if self.graph else 0
             self._cb_error = None
-            _lib.check(_lib.lib().askv_prefill_layers(C.addressof(p), cs.cuda_stream),
-                       "prefill_layers")
+            if batch is None:
+                _lib.check(_lib.lib().askv_prefill_layers(C.addressof(p), cs.cuda_stream),
+                           "prefill_layers")
             if self._cb_error is not None:
                 raise RuntimeError("tensor-parallel all-reduce failed") from self._cb_error
+
+        def finish() -> JobResult:
+          with torch.cuda.stream(cs):
             n_stamps = 0
             if lease:   # job begin / end + the last layer's end (the rest ride on kernels)
                 n_stamps += 3
@@ -828,14 +905,19 @@ class Runner:
             if lease:
                 _lib.check(_lib.lib().askv_stamp(self._stamp_ptr(st_off, 1), cs.cuda_stream),
                            "stamp")
-        res = JobResult(job.session_id, kept, n, None, first, logits_out,
-                        bytes_loaded=kept * s.kv_bytes_per_token if job.source == "host" else 0,
-                        bytes_saved=n * s.kv_bytes_per_token if job.save else 0,
-                        next_token=nxt)
-        if job.kv_cache is not None:
-            job.kv_cache.rows = kept + n
-        res._events = (self, t0, (st_off, st_end, n_st), rec, lease) if lease else None
-        return res
+          res = JobResult(job.session_id, kept, n, None, first, logits_out,
+                          bytes_loaded=(kept * s.kv_bytes_per_token if job.source == "host"
+                                        else 0),
+                          bytes_saved=n * s.kv_bytes_per_token if job.save else 0,
+                          next_token=nxt)
+          if job.kv_cache is not None:
+              job.kv_cache.rows = kept + n
+          res._events = (self, t0, (st_off, st_end, n_st), rec, lease) if lease else None
+          return res
+
+        if batch is not None:
+            return p, finish, keep
+        return finish()
 
     def join(self) -> None:
         """Make the compute stream wait for all loads and saves queued so far
@@ -847,10 +929,12 @@ class Runner:
     # ------------------------------------------------------------------ timelines
     @staticmethod
     def finalize(results: list[JobResult]) -> None:
-        """Resolve CUDA events into seconds (call after synchronising)."""
+        """Resolve CUDA events into seconds (call after synchronising).  The
+        members of a batch (run(..., batch=True)) get the batch's timeline."""
+        members = [r for r in results if getattr(r, "_batch_leader", None) is not None]
         for r in results:
             evs = getattr(r, "_events", None)
-            if not evs:
+            if not evs or getattr(r, "_batch_leader", None) is not None:
                 continue
             runner, t0, (off, end, n_st), rec, lease = evs
             ms = C.c_float()
@@ -888,4 +972,10 @@ class Runner:
             tl.stall_total = stall if stall > 1e-9 else 0.0
             tl.max_gap = max((b - a for a, b in waits), default=0.0)
             r.timeline = tl
+            r._events = None
+        for r in members:
+            lead = r._batch_leader
+            if lead.timeline is None and getattr(lead, "_events", None):
+                Runner.finalize([lead])
+            r.timeline = lead.timeline
             r._events = None
