@@ -233,6 +233,13 @@ class _Lease:
             pass
 
 
+def _await(ev: threading.Event, what: str, timeout: float = 600.0) -> None:
+    """Host wait on an IO-thread flag that fails loudly instead of hanging
+    (a failed job can leave a flag that nobody will set)."""
+    if not ev.wait(timeout):
+        raise RuntimeError(f"{what} stalled ({timeout:.0f} s)")
+
+
 def _ptr_array(items) -> "C.Array":
     """ctypes void*[] of device pointers / event handles (None -> NULL)."""
     return (C.c_void_p * len(items))(*items)
@@ -340,6 +347,7 @@ class Runner:
         self._last_load: dict = {}                   # session -> (event, host flag)
         self._pool = _EventPool()
         self._leases: dict = {}
+        self._pinned_inflight: list = []   # (pinned ids buffer, event of the copy reading it)
         # device timestamp ring (globaltimer ns) for the compute-stream timeline:
         # a CUDA timing event on the compute stream costs ~24 us while the
         # pre-loader saturates the host link (tools/event_probe.cu), a stamp
@@ -614,6 +622,16 @@ class Runner:
                "qkv": self._buf("qkv", tot, s.qkv_cols), "q": self._buf("q", tot, hq * hd),
                "ao": self._buf("ao", tot, hq * hd), "gu": self._buf("gu", tot, 2 * s.ffn),
                "act": self._buf("act", tot, s.ffn), "kv": self._buf("kv", kv_rows, self.row_elems)}
+        # one attention workspace for the whole batch (its K3s run one after
+        # another on the compute stream): size it for the largest job first, so
+        # no job's plan keeps a pointer to a buffer a later job reallocated
+        need = 0
+        for j in jobs:
+            sp = ops.attn_num_splits(j.kept, j.n_new, hq, n_kv_heads=s.n_kv_heads)
+            need = max(need, ops.attn_workspace_bytes(j.kept, j.n_new, hq, hd, sp,
+                                                      n_kv_heads=s.n_kv_heads))
+        if need:
+            self._workspace(need)
         plans, finishers, keep = [], [], []
         row0, kv0 = 0, 0
         probe0 = len(self.probe) if self.probe is not None else 0
@@ -658,7 +676,7 @@ class Runner:
         for t in (self._io_load, self._io_save):
             done = threading.Event()
             t.submit(done.set)
-            done.wait()
+            _await(done, t.name)
             if t.error is not None:
                 raise RuntimeError(f"{t.name} failed") from t.error
 
@@ -731,7 +749,7 @@ class Runner:
                 for sid in {job.session_id, *job.fence_sessions}:
                     dep = self._last_save.get(sid)
                     if dep is not None:
-                        dep[1].wait()
+                        _await(dep[1], "save IO thread")
                         dep[0].wait(cs)
 
             units = None
@@ -749,9 +767,18 @@ class Runner:
                 ids = job.token_ids
             else:  # pinned host ids: SM copy, not behind the pre-load DMAs
                 src = job.token_ids if job.token_ids.is_pinned() else job.token_ids.pin_memory()
+                src = src.to(torch.int64)
                 ids = ops.copy_sm(torch.empty(n, dtype=torch.int64, device=self.device),
-                                  src.to(torch.int64), stream=cs)
+                                  src, stream=cs)
                 self.launches += 1
+                # torch's pinned-memory cache cannot see our kernel read the
+                # staging buffer: hold it until the copy has run (a freed block
+                # could be handed to the next job's ids before it does)
+                done = torch.cuda.Event()
+                done.record(cs)
+                self._pinned_inflight = [(t, e) for t, e in self._pinned_inflight
+                                         if not e.query()]
+                self._pinned_inflight.append((src, done))
             if batch is None:
                 x = F.embedding(ids, self.w.embed)
                 buf = lambda name, rows, cols: self._buf(name, rows, cols)  # noqa: E731
@@ -832,7 +859,7 @@ class Runner:
                     w = self._wseq % self.n_wslots
                     self._wseq += 1
                     if self._wflag[w] is not None:   # its previous save is submitted
-                        self._wflag[w].wait()
+                        _await(self._wflag[w], "save IO thread")
                     wslots.append(w)
                 p.save_rows = arr([self.wbuf[w].data_ptr() for w in wslots])
                 p.ev_save_free = arr([self._wdone[w].handle for w in wslots])
@@ -871,6 +898,7 @@ class Runner:
                 raise RuntimeError("tensor-parallel all-reduce failed") from self._cb_error
 
         def finish() -> JobResult:
+          nonlocal logits_out
           with torch.cuda.stream(cs):
             n_stamps = 0
             if lease:   # job begin / end + the last layer's end (the rest ride on kernels)
@@ -953,7 +981,7 @@ class Runner:
             L = (n_st - 3) // 7
             tl.load_intervals = [(f(a), f(b)) for a, b in rec["loads"]]
             for *_, flag in rec["saves"]:
-                flag.wait()
+                _await(flag, "save IO thread")
             tl.save_intervals = [(f(a), f(b)) for a, b, _ in rec["saves"]]
             comp, waits = [], []
             begin = g(2)
