@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
   // this CTA's job: the launch's only one, or (varlen) the batch job owning
   // blockIdx.x, with its rows' offsets in the shared Q / KV buffers
   int bx = blockIdx.x, h = blockIdx.y, split = blockIdx.z;
-  int n_new = n_new, n_cached = n_cached, q_row0 = 0, kv_row0 = 0;
+  int n_new = p.n_new, n_cached = p.n_cached, q_row0 = 0, kv_row0 = 0;
   __nv_bfloat16* out_base = p.out;
   int v_src_tiles = p.v_src_tiles;
   const int64_t* v_blk_off = p.v_blk_off;

@@ -25,6 +25,10 @@ def main():
     ap.add_argument("--no-save", action="store_true", help="jobs without the K4 save")
     ap.add_argument("--no-graph", action="store_true", help="stream-issue the layer loop")
     ap.add_argument("--overlap", action="store_true", help="K2(l+1) alongside K3(l)")
+    ap.add_argument("--batch", action="store_true",
+                    help="the turns as one batched layer pass (askv_prefill_layers_batch)")
+    ap.add_argument("--no-profiler", action="store_true",
+                    help="skip torch.profiler (for running under ncu)")
     a = ap.parse_args()
     import bench
     from paper_2403_19708_b200 import model
@@ -38,8 +42,11 @@ def main():
     nbs = [-(-(k + n) // tb) for _, _, k, n in turns]
     arena = HostArena(sum(nbs), bb, pin=True)
     hbm = torch.zeros(sum(nbs) * bb // 2, dtype=torch.bfloat16, device="cuda")
+    max_new = max(n for *_, n in turns)
     runner = Runner(shape, host_arena=arena, hbm_arena=hbm, read_buffer_bytes=4 << 30,
-                    write_buffer_bytes=1 << 30, max_new=max(n for *_, n in turns),
+                    write_buffer_bytes=max(1 << 30, len(turns) * shape.layers * max_new
+                                           * shape.row_bytes if a.batch else 0),
+                    max_new=max_new,
                     max_ctx=4096, timeline=True, graph=not a.no_graph, overlap=a.overlap)
     jobs, pos = [], 0
     rng = np.random.default_rng(0)
@@ -58,9 +65,14 @@ def main():
             jobs.append(Job(f"{sid}#{k}",
                             torch.as_tensor(rng.integers(0, shape.vocab, kept + new)).cuda()))
     for _ in range(2):
-        runner.run(jobs)
+        runner.run(jobs, batch=a.batch)
         runner.join()
     torch.cuda.synchronize()
+    if a.no_profiler:   # one more step (the ncu capture window), then stop
+        runner.run(jobs, batch=a.batch)
+        runner.join()
+        torch.cuda.synchronize()
+        return
     from torch.profiler import ProfilerActivity, profile
     bg = None
     if a.bg_h2d:   # isolate copy-engine interference: 1 GB H2D chunks on their own stream
@@ -82,7 +94,7 @@ def main():
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         e0.record(runner.s_compute)
         h0 = time.perf_counter()
-        runner.run(jobs)
+        runner.run(jobs, batch=a.batch)
         runner.join()
         host_issue_ms = (time.perf_counter() - h0) * 1e3
         e1.record(runner.s_compute)
@@ -90,13 +102,13 @@ def main():
     # host issue rate without the profiler attached
     torch.cuda.synchronize()
     h0 = time.perf_counter()
-    runner.run(jobs)
+    runner.run(jobs, batch=a.batch)
     runner.join()
     host_issue_ms_noprof = (time.perf_counter() - h0) * 1e3
     torch.cuda.synchronize()
     gpu_ms_noprof = (time.perf_counter() - h0) * 1e3
     wall_us = e0.elapsed_time(e1) * 1e3
-    res = runner.run(jobs)
+    res = runner.run(jobs, batch=a.batch)
     runner.join()
     torch.cuda.synchronize()
     Runner.finalize(res)
@@ -135,7 +147,8 @@ def main():
         merged += ce - cs
     cpu_total = sum(ev.cpu_time_total for ev in prof.events()
                     if ev.device_type == torch.autograd.DeviceType.CPU and ev.name == "aten::linear")
-    out = {"mode": a.mode, "turns": len(jobs), "wall_us": wall_us, "timelines": tls,
+    out = {"mode": a.mode, "batch": a.batch, "turns": len(jobs), "wall_us": wall_us,
+           "timelines": tls,
            "host_issue_ms": host_issue_ms, "host_issue_ms_noprof": host_issue_ms_noprof,
            "wall_ms_noprof": gpu_ms_noprof,
            "kernel_busy_us": merged, "gpu_idle_frac": 1 - merged / wall_us,
