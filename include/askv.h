@@ -156,6 +156,16 @@ int askv_save_layer(void* host_base, const int64_t* block_ids, int nblocks,
                     int64_t block_bytes, int64_t layer_off, int block_tokens,
                     int64_t row_bytes, int64_t first_token, int n_tokens, const void* src,
                     void* stream, void* done_event);
+/* K4 for all `layers` layers of a job in one call: layer l waits ev_ready[l]
+ * (may be NULL), records ev_t0[l] / ev_t1[l] around its copy (timing, may be
+ * NULL) and ev_done[l] after it; src[l] holds its n_tokens rows; ev_last is
+ * recorded after the last layer.  Replaces: the per-layer save slots of
+ * overlap.py:126-200 (one call instead of one per layer). */
+int askv_save_layers(void* host_base, const int64_t* block_ids, int nblocks, int64_t block_bytes,
+                     int64_t chunk_bytes, int layers, int block_tokens, int64_t row_bytes,
+                     int64_t first_token, int n_tokens, const void* const* src,
+                     void* const* ev_ready, void* const* ev_done, void* const* ev_t0,
+                     void* const* ev_t1, void* ev_last, void* stream);
 
 /*
  * Small copy executed by SMs through unified addressing (pinned host <-> device):
@@ -306,6 +316,10 @@ int askv_prefill_layers(const askv_prefill_plan* plan, void* stream);
  * A scheduler knob: batching trades each turn's time to first token for
  * throughput (GEMMs over thousands of rows instead of a few hundred). */
 int askv_prefill_layers_batch(const askv_prefill_plan* plans, int njobs, void* stream);
+/* Cumulative host microseconds of the layer loop's issue path since load:
+ * out4 = {calls, capture (issuing the loop into the graph), update /
+ * instantiate, launch}.  Diagnostics. */
+void askv_issue_stats(double* out4);
 
 /*
  * K5 — NCCL for the tensor-parallel all-reduce (C5), bound at run time

@@ -38,6 +38,9 @@ SIGNATURES = {
     "askv_attn_workspace_bytes_gqa": (_sz, [_i32, _i32, _i32, _i32, _i32, _i32]),
     "askv_gemm": (_i32, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _sz, _vp]),
     "askv_prefill_layers_batch": (_i32, [_vp, _i32, _vp]),
+    "askv_issue_stats": (None, [_vp]),
+    "askv_save_layers": (_i32, [_vp, _vp, _i32, _i64, _i64, _i32, _i32, _i64, _i64, _i32, _vp,
+                                _vp, _vp, _vp, _vp, _vp, _vp]),
     "askv_nccl_unique_id": (_i32, [_vp]),
     "askv_nccl_comm_init": (_i32, [_i32, _i32, _vp, C.POINTER(_vp)]),
     "askv_nccl_comm_destroy": (_i32, [_vp]),

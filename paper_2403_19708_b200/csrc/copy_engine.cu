@@ -197,3 +197,37 @@ extern "C" int askv_save_layer(void* host_base, const int64_t* block_ids, int nb
                        "save event record");
   return ASKV_OK;
 }
+
+// K4 for a whole job: every layer's save in one call (the saver IO thread
+// otherwise pays ~5 runtime calls through ctypes per layer, which at 16 jobs x
+// 40 layers per batched pass made the host the bottleneck).  Per layer l:
+// wait ev_ready[l] (the loop's rope_new wrote the rows), optional timing event
+// ev_t0[l], the D2H / D2D segments of askv_save_layer, record ev_done[l] (the
+// write-buffer slot is free again), optional ev_t1[l]; then ev_last.
+extern "C" int askv_save_layers(void* host_base, const int64_t* block_ids, int nblocks,
+                                int64_t block_bytes, int64_t chunk_bytes, int layers,
+                                int block_tokens, int64_t row_bytes, int64_t first_token,
+                                int n_tokens, const void* const* src, void* const* ev_ready,
+                                void* const* ev_done, void* const* ev_t0, void* const* ev_t1,
+                                void* ev_last, void* stream) {
+  clear_error();
+  ASKV_REQUIRE(layers > 0 && src != nullptr, "save_layers: bad layers=%d", layers);
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int l = 0; l < layers; ++l) {
+    if (ev_ready && ev_ready[l]) {
+      const int rc = cuda_status(cudaStreamWaitEvent(s, (cudaEvent_t)ev_ready[l], 0),
+                                 "save_layers wait");
+      if (rc) return rc;
+    }
+    if (ev_t0 && ev_t0[l]) cudaEventRecord((cudaEvent_t)ev_t0[l], s);
+    const int rc = askv_save_layer(host_base, block_ids, nblocks, block_bytes,
+                                   (int64_t)l * chunk_bytes, block_tokens, row_bytes,
+                                   first_token, n_tokens, src[l], stream,
+                                   ev_done ? ev_done[l] : nullptr);
+    if (rc) return rc;
+    if (ev_t1 && ev_t1[l]) cudaEventRecord((cudaEvent_t)ev_t1[l], s);
+  }
+  if (ev_last)
+    return cuda_status(cudaEventRecord((cudaEvent_t)ev_last, s), "save_layers event record");
+  return ASKV_OK;
+}

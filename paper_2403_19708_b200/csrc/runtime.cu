@@ -13,6 +13,7 @@
 #include <cublasLt.h>
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -469,8 +470,21 @@ static int tp_out_proj(const askv_prefill_plan* p, const void* in, const void* w
   return tp_allreduce_bf16(r0 ? p->x : p->h, p->x, (int64_t)n * d, p->nccl_comm, s);
 }
 
+// Cumulative host time of the loop's issue path (askv_issue_stats).
+struct IssueStats {
+  double calls = 0, capture_us = 0, update_us = 0, launch_us = 0;
+};
+IssueStats g_issue;
+inline double now_us() {
+  return std::chrono::duration<double, std::micro>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
 static int prefill_multi(const askv_prefill_plan* ps, int nj, cudaStream_t s) {
   const askv_prefill_plan* p = ps;
+  g_issue.calls += 1;
+  const double t_cap = now_us();
   // Graph issue: one launch per job instead of ~11 per layer.  While the
   // pre-loader saturates the host link, every stream launch's command fetch
   // queues behind the H2D DMA and the GPU idles between kernels
@@ -491,6 +505,8 @@ static int prefill_multi(const askv_prefill_plan* ps, int nj, cudaStream_t s) {
   g_capturing = false;
   cudaGraph_t g = nullptr;
   const cudaError_t ec = cudaStreamEndCapture(s, &g);
+  const double t_upd = now_us();
+  g_issue.capture_us += t_upd - t_cap;
   if (rc != ASKV_OK) {
     if (g) cudaGraphDestroy(g);
     return rc;
@@ -542,9 +558,20 @@ static int prefill_multi(const askv_prefill_plan* ps, int nj, cudaStream_t s) {
   }
   cudaGraphDestroy(g);
   it->second.last_use = ++g_graph_clock;
+  const double t_launch = now_us();
+  g_issue.update_us += t_launch - t_upd;
   rc = cuda_status(cudaGraphLaunch(it->second.exec, s), "cudaGraphLaunch");
   if (rc == ASKV_OK) rc = cuda_status(cudaEventRecord(it->second.done, s), "cudaEventRecord");
+  g_issue.launch_us += now_us() - t_launch;
   return rc;
+}
+
+extern "C" void askv_issue_stats(double* out4) {
+  if (!out4) return;
+  out4[0] = g_issue.calls;
+  out4[1] = g_issue.capture_us;
+  out4[2] = g_issue.update_us;
+  out4[3] = g_issue.launch_us;
 }
 
 extern "C" int askv_prefill_layers(const askv_prefill_plan* p, void* stream) {

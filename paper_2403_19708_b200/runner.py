@@ -35,6 +35,7 @@ import queue
 import threading
 from dataclasses import dataclass, field
 
+import numpy as np
 import torch
 import torch.nn.functional as F
 
@@ -527,23 +528,26 @@ class Runner:
         self._freed.setdefault(u.seq, threading.Event()).set()
         self._freed.pop(u.seq - 2 * self.n_slots, None)
 
-    def _submit_save(self, arena, job, layer, kept, n, wslot, times, flag, last):
-        sess_ev = self._sess_ev.get(job.session_id) if last else None
+    def _submit_saves(self, arena, job, kept, n, wslots, times, flag, sess_ev):
+        """K4 for all of a job's layers from the save IO thread in one native
+        call: layer l waits its write-buffer slot's ``ready`` event, copies
+        the rows into the session's blocks, records the slot's ``done``."""
+        L = len(wslots)
+        ids = np.ascontiguousarray(np.asarray(job.block_ids, dtype=np.int64))
+        src = _ptr_array([self.wbuf[w].data_ptr() for w in wslots])
+        ready = _ptr_array([self._wready[w].handle for w in wslots])
+        done = _ptr_array([self._wdone[w].handle for w in wslots])
+        t0 = _ptr_array([a.handle for a, _ in times]) if times else None
+        t1 = _ptr_array([b.handle for _, b in times]) if times else None
+        base = arena.data_ptr()
 
         def submit():
             try:
-                ss = self.s_save
-                self._wready[wslot].wait(ss)
-                if times:
-                    times[0].record(ss)
-                ops.save_layer(arena, job.block_ids, self.block_bytes,
-                               layer * self.chunk_bytes, self.block_tokens, self.row_bytes,
-                               job.head + kept, n, self.wbuf[wslot], stream=ss)
-                self._wdone[wslot].record(ss)
-                if sess_ev is not None:
-                    sess_ev.record(ss)
-                if times:
-                    times[1].record(ss)
+                _lib.check(_lib.lib().askv_save_layers(
+                    base, ids.ctypes.data_as(C.POINTER(C.c_int64)), len(ids), self.block_bytes,
+                    self.chunk_bytes, L, self.block_tokens, self.row_bytes, job.head + kept, n,
+                    src, ready, done, t0, t1, sess_ev.handle, self.s_save.cuda_stream),
+                    "save_layers")
             finally:
                 flag.set()
 
@@ -913,15 +917,14 @@ class Runner:
                 sess_ev = self._sess_ev.get(job.session_id)
                 if sess_ev is None:
                     sess_ev = self._sess_ev[job.session_id] = ops.NativeEvent()
-                flag = None
-                for layer, w in enumerate(wslots):
-                    times = (lease.get(), lease.get()) if lease else None
-                    flag = threading.Event()
+                # every layer's save in one submission (askv_save_layers)
+                flag = threading.Event()
+                times = [(lease.get(), lease.get()) for _ in wslots] if lease else None
+                for w in wslots:
                     self._wflag[w] = flag
-                    self._submit_save(arena, job, layer, kept, n, w, times, flag,
-                                      layer == L - 1)
-                    if times:
-                        rec["saves"].append((times[0], times[1], flag))
+                self._submit_saves(arena, job, kept, n, wslots, times, flag, sess_ev)
+                if times:
+                    rec["saves"].extend((t0_, t1_, flag) for t0_, t1_ in times)
                 self._last_save[job.session_id] = (sess_ev, flag)
             hl = ops.rmsnorm(x[-1:], self.w.w_final, 1e-5, stream=cs)
             logits = F.linear(hl, self.w.lm_head).float()
