@@ -704,6 +704,7 @@ class Runner:
         if kept and job.source == "hbm" and job.dev_block_off is None:
             raise ValueError("hbm job needs dev_block_off")
         arena = None
+        in_hbm = False
         if job.save:
             # an "hbm" job whose session lives in the HBM arena (bench value
             # mode) saves there; an HBM-tier hit (mirror_block_ids set) keeps
@@ -849,14 +850,19 @@ class Runner:
                 p.src_rows = self.hbm_arena.numel() * 2 // self.row_bytes
                 p.src_layer = arr([base + l * self.chunk_bytes for l in range(L)])
                 p.src_block_off = job.dev_block_off.data_ptr()
-            if job.save and job.mirror_block_ids is not None:
-                # HBM tier write-through inside the layer loop (compute-stream
-                # order with promotions and K2 reads of the tier)
-                mids = (C.c_int64 * len(job.mirror_block_ids))(*job.mirror_block_ids)
+            # a session living in the HBM arena saves there inside the layer
+            # loop (device-to-device, in stream order, captured in the graph):
+            # no saver IO-thread work per layer
+            save_in_loop = job.save and in_hbm
+            if (job.save and job.mirror_block_ids is not None) or save_in_loop:
+                # HBM tier write-through (or the arena save itself) inside the
+                # layer loop (compute-stream order with promotions and K2 reads)
+                tgt = job.block_ids if save_in_loop else job.mirror_block_ids
+                mids = (C.c_int64 * len(tgt))(*tgt)
                 keep.append(mids)
                 p.mirror_base = self.hbm_arena.data_ptr()
                 p.mirror_block_ids = mids
-                p.mirror_nblocks = len(job.mirror_block_ids)
+                p.mirror_nblocks = len(tgt)
             wslots = []
             if job.save:
                 for _ in range(L):
@@ -866,8 +872,9 @@ class Runner:
                         _await(self._wflag[w], "save IO thread")
                     wslots.append(w)
                 p.save_rows = arr([self.wbuf[w].data_ptr() for w in wslots])
-                p.ev_save_free = arr([self._wdone[w].handle for w in wslots])
-                p.ev_save_ready = arr([self._wready[w].handle for w in wslots])
+                if not save_in_loop:
+                    p.ev_save_free = arr([self._wdone[w].handle for w in wslots])
+                    p.ev_save_ready = arr([self._wready[w].handle for w in wslots])
             reemb = bool(kept) and job.source != "resident"
             if lease or self.probe is not None:
                 p.stamps = self._stamp_ptr(st_off, 2)
@@ -913,7 +920,11 @@ class Runner:
             if units is not None:
                 for u in units:
                     self._release(u)
-            if job.save:
+            if save_in_loop:   # saved by the loop itself: later readers follow in stream order
+                for w in wslots:
+                    self._wflag[w] = None
+                self._last_save.pop(job.session_id, None)
+            elif job.save:
                 sess_ev = self._sess_ev.get(job.session_id)
                 if sess_ev is None:
                     sess_ev = self._sess_ev[job.session_id] = ops.NativeEvent()
