@@ -96,10 +96,7 @@ __global__ void rope_table_kernel(float* __restrict__ table, int max_pos, int ha
 // HD/2 float2) are staged in shared memory once, then every thread streams
 // 16-byte vectors of the rows (4 in flight per thread), rotating K vectors
 // and copying V vectors.  Source rows come through the session block table.
-#ifndef ASKV_REEMBED_ROWS
-#define ASKV_REEMBED_ROWS 4
-#endif
-constexpr int kReRows = ASKV_REEMBED_ROWS;
+constexpr int kReRows = 2;
 
 template <int HD>
 __global__ void __launch_bounds__(kThreads)
@@ -142,16 +139,10 @@ __global__ void __launch_bounds__(kThreads)
   // are on the same side of it
   const int row_units = row0 >= v_from ? 2 * k_units : k_units;
   const int total = nrows * row_units;
-  // the row of a vector is a few compares, not an integer division (K2 was
-  // issue-bound: ncu 45-50 % issue slots, profiles/r01d_summary.md).  4 rows
-  // per CTA since V moves only in the last partial tile: a K-only row is half
-  // the work, so 2 rows left the per-CTA setup (cos/sin staging) dominant
-  static_assert(kReRows == 2 || kReRows == 4, "row index below assumes 2 or 4 rows per CTA");
-  auto row_of = [&](int g) {
-    int rr = g >= row_units ? 1 : 0;
-    if (kReRows == 4) rr += (g >= 2 * row_units ? 1 : 0) + (g >= 3 * row_units ? 1 : 0);
-    return rr;
-  };
+  // 13B: 2 rows x 1280 vectors = two rounds of 5 per thread; the row of a
+  // vector is a compare (kReRows == 2), not an integer division (K2 was
+  // issue-bound: ncu 45-50 % issue slots, profiles/r01d_summary.md)
+  static_assert(kReRows == 2, "row index below assumes two rows per CTA");
   constexpr int kIlp = 5;
   const uint64_t pol_src = policy_evict_first();
   for (int base = threadIdx.x; base < total; base += kThreads * kIlp) {
@@ -160,7 +151,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int k = 0; k < kIlp; ++k) {
       const int g = base + k * kThreads;
       if (g < total) {
-        const int rr = row_of(g);
+        const int rr = g >= row_units ? 1 : 0;
         v[k] = ld_nc16_ef(srow_s[rr] + (g - rr * row_units) * 8, pol_src);
       }
     }
@@ -168,7 +159,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int k = 0; k < kIlp; ++k) {
       const int g = base + k * kThreads;
       if (g < total) {
-        const int rr = row_of(g);
+        const int rr = g >= row_units ? 1 : 0;
         const int u = g - rr * row_units;
         int4 x = v[k];
         if (u < k_units) x = rotate8(x, cs_s + (rr * kHalf + (u % kUnitsPerHead) * 4) * 2);
@@ -315,8 +306,7 @@ int askv::reembed_stamped(const void* src_base, const int64_t* src_block_off, in
                table_positions);
   ASKV_REQUIRE(src_row_stride % 8 == 0 && dst_row_stride % 8 == 0,
                "reembed: row strides must be multiples of 8 elements");
-  ASKV_REQUIRE(v_from >= 0 && v_from % kReRows == 0,
-               "reembed: v_from %d must be a multiple of %d", v_from, kReRows);
+  ASKV_REQUIRE(v_from >= 0 && v_from % 2 == 0, "reembed: v_from %d must be even", v_from);
   if (kept == 0) return ASKV_OK;
   ASKV_REQUIRE(src_base && dst && rope_table, "reembed: null pointer");
   const int grid = (kept + kReRows - 1) / kReRows;
