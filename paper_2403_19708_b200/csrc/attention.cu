@@ -667,10 +667,8 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
     // and written by TMA: one bulk store per 64 columns instead of scattered
     // 16-byte row pieces.  CTA-uniform choice (every tile of the CTA is full
     // when o_tma == 2).
-    // (the paired instantiation keeps direct stores: the staging pushes its
-    // 128-column epilogue into spills)
-    const bool o_tma = !kAllowPair && !partial &&
-                       (p.o_tma == 1 || (p.o_tma == 2 && rows_a == kBM));
+    const bool o_tma = !partial && (p.o_tma == 1 ||
+                                    (p.o_tma == 2 && rows_a == kBM && (!paired || rows_b == kBM)));
     uint8_t* stg = sK + (paired ? w : 0) * C::kTileBytes;
     // paired: the other group may still run S MMAs out of the K ring until it
     // too has waited its last PV

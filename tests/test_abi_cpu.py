@@ -142,6 +142,4 @@ def test_attention_kernel_does_not_spill(built):
         if m and name and ("attn_fwd_kernel" in name or "attn_sk_kernel" in name):
             stacks[name] = int(m.group(1))
     assert len(stacks) == 6, stacks  # HD 64 / 128 x unpaired / paired / stream-K
-    # a few prologue / epilogue locals (the varlen job lookup, output staging)
-    # stay on the stack; the round-1 softmax spill was ~100 B in the tile loop
-    assert max(stacks.values()) <= 32, stacks
+    assert max(stacks.values()) <= 16, stacks
