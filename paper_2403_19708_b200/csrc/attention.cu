@@ -99,10 +99,6 @@ struct AttnParams {
   // V source (VSource, askv_internal.h): tiles < v_src_tiles load V through
   // tm_vs at row v_blk_off ? v_blk_off[t] / v_row_elems + v_layer_row
   //                         : v_src_row0 + 128 t
-  // bf16 output through a TMA store of the staged tile (tm_o): 0 = direct
-  // stores, 1 = every tile (rows past the tensor are clipped), 2 = full
-  // tiles only (varlen: the next job's rows follow a tail tile)
-  int o_tma;
   int v_src_tiles;
   int64_t v_src_row0;
   const int64_t* v_blk_off;
@@ -246,8 +242,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v,
-                    const __grid_constant__ CUtensorMap tm_vs,
-                    const __grid_constant__ CUtensorMap tm_o, const AttnParams p,
+                    const __grid_constant__ CUtensorMap tm_vs, const AttnParams p,
                     const __grid_constant__ VarJobs vj) {
   using C = Cfg<HD, kAllowPair>;
   extern __shared__ uint8_t smem_raw[];
@@ -663,16 +658,6 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
     const int rows_g = paired ? (w ? rows_b : rows_a) : rows_a;
     const int qi = qt0 + r;
     const uint32_t t_o_other = tmem + lane_off + C::col_o(w ^ 1);
-    // output staged in the (now idle) K ring in the 128B-swizzled tile layout
-    // and written by TMA: one bulk store per 64 columns instead of scattered
-    // 16-byte row pieces.  CTA-uniform choice (every tile of the CTA is full
-    // when o_tma == 2).
-    const bool o_tma = !partial && (p.o_tma == 1 ||
-                                    (p.o_tma == 2 && rows_a == kBM && (!paired || rows_b == kBM)));
-    uint8_t* stg = sK + (paired ? w : 0) * C::kTileBytes;
-    // paired: the other group may still run S MMAs out of the K ring until it
-    // too has waited its last PV
-    if (o_tma && paired) named_bar_sync(1, 256);
     for (int c = 0; c < ncols / 32; ++c) {
       const int col = col0 + c * 32;
       float a[32], b[32];
@@ -685,19 +670,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
         const float y = (!paired && f_other > 0.f) ? b[e] * f_other : 0.f;
         o[e] = (x + y) * inv_l;
       }
-      if (o_tma) {
-#pragma unroll
-        for (int e = 0; e < 32; e += 8) {
-          const int gcol = col + e;
-          const int hh = gcol >> 6, c16 = (gcol & 63) >> 3;
-          uint4 v;
-          v.x = pack_bf16x2(o[e + 0], o[e + 1]);
-          v.y = pack_bf16x2(o[e + 2], o[e + 3]);
-          v.z = pack_bf16x2(o[e + 4], o[e + 5]);
-          v.w = pack_bf16x2(o[e + 6], o[e + 7]);
-          *reinterpret_cast<uint4*>(stg + hh * (kBM * 128) + r * 128 + ((c16 ^ (r & 7)) << 4)) = v;
-        }
-      } else if (r < rows_g) {
+      if (r < rows_g) {
         if (!partial) {
           __nv_bfloat16* dst = out_base + out_row(qi) * HD + col;
 #pragma unroll
@@ -718,20 +691,6 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
           if (c == 0 && (paired || w == 0))
             p.part_lse[row] = l_fin > 0.f ? m_fin + __log2f(l_fin) : -INFINITY;
         }
-      }
-    }
-    if (o_tma) {
-      fence_proxy_async_smem();
-      named_bar_sync(1, 256);
-      if (threadIdx.x == 0) {
-        const int tiles = paired ? 2 : 1;
-        for (int t = 0; t < tiles; ++t)
-#pragma unroll
-          for (int hh = 0; hh < HD / 64; ++hh)
-            tma_store_3d(&tm_o, sK + t * C::kTileBytes + hh * (kBM * 128), hh * 64,
-                         pack > 1 ? h * pack : h, q_row0 + tok(q0 + t * kBM));
-        tma_store_commit();
-        tma_store_wait_read();
       }
     }
   } else {
@@ -1533,9 +1492,6 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
                   hkv, HD, vsrc->rows, vsrc->row_elems);
   if (rc) return rc;
   if (!use_vs) mvs = mv;
-  CUtensorMap mo;
-  rc = make_map(&mo, out, HD, hq, HD, n_new, (int64_t)hq * HD, pack);
-  if (rc) return rc;
   auto set_vs = [&](AttnParams& a) {
     a.v_src_tiles = use_vs ? vsrc->tiles : 0;
     a.v_src_row0 = use_vs ? vsrc->row0 : 0;
@@ -1559,6 +1515,9 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
     prm.out = static_cast<__nv_bfloat16*>(out);
     prm.stamp = stamp;
     set_vs(prm);
+    CUtensorMap mo;
+    rc = make_map(&mo, out, HD, hq, HD, n_new, (int64_t)hq * HD, pack);
+    if (rc) return rc;
     return launch_sk<HD>(mq, mk, mv, mvs, mo, prm, hkv, ws, ws_bytes, stream);
   }
   const int tps = (kv_tiles + splits - 1) / splits;
@@ -1571,7 +1530,6 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
   prm.pack = pack;
   prm.num_splits = splits;
   prm.tiles_per_split = tps;
-  prm.o_tma = splits > 1 ? 0 : 1;
   prm.scale_log2 = scale * 1.4426950408889634f;
   prm.out = static_cast<__nv_bfloat16*>(out);
   prm.stamp = stamp;
@@ -1600,7 +1558,7 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
     VarJobs none;
     none.n = 0;
     kern<<<grid, Cfg<HD, true>::kThreads, Cfg<HD, true>::kSmemBytes, stream>>>(mq, mk, mv, mvs,
-                                                                                mo, prm, none);
+                                                                                prm, none);
   } else {
     auto kern = attn_fwd_kernel<HD, false>;
     static bool attr = false;
@@ -1613,8 +1571,7 @@ int launch_attn(const void* q, const void* kv, int64_t kv_row_stride, int n_cach
     VarJobs none;
     none.n = 0;
     kern<<<grid, Cfg<HD, false>::kThreads, Cfg<HD, false>::kSmemBytes, stream>>>(mq, mk, mv,
-                                                                                 mvs, mo, prm,
-                                                                                 none);
+                                                                                 mvs, prm, none);
   }
   rc = launch_status("attn_fwd launch");
   if (rc || splits == 1) return rc;
@@ -1644,12 +1601,9 @@ int launch_varlen(const VarlenBatch& b, cudaStream_t stream, unsigned long long*
   if (!rc && use_vs)
     rc = make_map(&mvs, static_cast<const __nv_bfloat16*>(b.vsrc_base) + (int64_t)hkv * HD, HD,
                   hkv, HD, b.vsrc_rows, b.vsrc_row_elems);
-  CUtensorMap mo;   // the jobs' outputs are consecutive rows of one buffer
-  if (!rc) rc = make_map(&mo, b.out[0], HD, hq, HD, q_tot, (int64_t)hq * HD, pack);
   if (rc) return rc;
   if (!use_vs) mvs = mv;
   AttnParams prm{};
-  prm.o_tma = 2;
   prm.hq = hq;
   prm.group = hq / hkv;
   prm.pack = pack;
@@ -1686,7 +1640,7 @@ int launch_varlen(const VarlenBatch& b, cudaStream_t stream, unsigned long long*
       ctas += J.q_groups * heads;
     }
     kern<<<ctas, Cfg<HD, false>::kThreads, Cfg<HD, false>::kSmemBytes, stream>>>(mq, mk, mv, mvs,
-                                                                                 mo, prm, vj);
+                                                                                 prm, vj);
     rc = launch_status("attn_fwd varlen launch");
     if (rc) return rc;
   }
@@ -1780,14 +1734,9 @@ int askv::prefill_attn_varlen(const VarlenBatch& b, void* stream, unsigned long 
                "prefill_attn_varlen: bad batch");
   ASKV_REQUIRE(b.head_dim == 64 || b.head_dim == 128, "prefill_attn_varlen: head_dim %d",
                b.head_dim);
-  for (int i = 0; i < b.n; ++i) {
+  for (int i = 0; i < b.n; ++i)
     ASKV_REQUIRE(b.n_new[i] > 0 && b.n_cached[i] >= 0 && b.out[i],
                  "prefill_attn_varlen: job %d", i);
-    ASKV_REQUIRE(static_cast<const char*>(b.out[i]) ==
-                     static_cast<const char*>(b.out[0]) +
-                         (int64_t)b.q_row0[i] * b.hq * b.head_dim * 2,
-                 "prefill_attn_varlen: job %d's output is not at its query rows", i);
-  }
   if (b.head_dim == 128) return launch_varlen<128>(b, (cudaStream_t)stream, stamp);
   return launch_varlen<64>(b, (cudaStream_t)stream, stamp);
 }
