@@ -399,3 +399,53 @@ def test_full_size_rope_properties():
     # both are within the 5e-3 attention bar of the exact result, so they
     # agree within twice that (measured 4.7e-3)
     assert rel <= 1e-2, rel
+
+
+@pytest.mark.parametrize("ids", [[5, 1, 9, 3], [2, 3, 4, 5, 6]])
+def test_preload_strided_runs_and_numa_arena_bitexact(ids):
+    """K1 over a NUMA-bound, cudaHostRegister'ed arena (numa.py): runs of
+    consecutive block ids go as one strided 2-D DMA, isolated ids as single
+    copies -- both land bit-exact; askv_save_layers (a job's layers in one
+    call) writes every layer's rows back bit-exact."""
+    import ctypes as C
+
+    from paper_2403_19708_b200 import _lib
+    from paper_2403_19708_b200.store import HostArena
+    ops = _ops()
+    L, tb, row_bytes = 3, 16, 2 * 2 * 64 * 2
+    chunk = tb * row_bytes
+    block_bytes = L * chunk
+    arena = HostArena(12, block_bytes, pin=True, numa_node=0)
+    assert arena.numa_node == 0
+    g = torch.Generator().manual_seed(9)
+    arena.buffer.copy_(torch.randint(0, 256, arena.buffer.shape, dtype=torch.uint8, generator=g))
+    host = arena.buffer
+    tokens = (len(ids) - 1) * tb + 7
+    s = torch.cuda.Stream()
+    for layer in range(L):
+        dst = torch.empty(len(ids) * chunk, dtype=torch.uint8, device=DEV)
+        with torch.cuda.stream(s):
+            ops.preload_layer(dst, host, ids, block_bytes, layer * chunk, chunk,
+                              tail_bytes=(tokens - (len(ids) - 1) * tb) * row_bytes)
+        s.synchronize()
+        want = torch.cat([host[b * block_bytes + layer * chunk:
+                               b * block_bytes + (layer + 1) * chunk] for b in ids])
+        assert torch.equal(dst.cpu()[:tokens * row_bytes], want[:tokens * row_bytes])
+    # every layer's 21 new rows at token 9 in one askv_save_layers call
+    n, first = 21, 9
+    srcs = [torch.randint(0, 256, (n * row_bytes,), dtype=torch.uint8, generator=g).to(DEV)
+            for _ in range(L)]
+    arr = np.asarray(ids, dtype=np.int64)
+    ptrs = (C.c_void_p * L)(*[t.data_ptr() for t in srcs])
+    _lib.check(_lib.lib().askv_save_layers(
+        host.data_ptr(), arr.ctypes.data_as(C.POINTER(C.c_int64)), len(arr), block_bytes, chunk,
+        L, tb, row_bytes, first, n, ptrs, None, None, None, None, None, s.cuda_stream),
+        "save_layers")
+    s.synchronize()
+    for layer, src in enumerate(srcs):
+        got = []
+        for t in range(first, first + n):
+            b = ids[t // tb]
+            off = b * block_bytes + layer * chunk + (t % tb) * row_bytes
+            got.append(host[off:off + row_bytes])
+        assert torch.equal(torch.cat(got), src.cpu()), layer

@@ -145,10 +145,38 @@ def engine_turns(graph: bool):
     print(f"engine turns graph={graph} done", flush=True)
 
 
+def batch_cases():
+    """A batched layer pass of the tiny model with HBM-resident sessions: the
+    varlen K3 launch (one launch for every job's (query tile, head) grid)."""
+    import numpy as np
+    from paper_2403_19708_b200 import model, runner
+    from paper_2403_19708_b200.runner import Job, Runner
+    shape = model.shape("tiny")
+    bt, nb = 128, 12
+    bb = bt * shape.kv_bytes_per_token
+    hbm = torch.randn(nb * bb // 2, device="cuda").to(torch.bfloat16)
+    r = runner.Runner(shape, seed=1, block_tokens=bt, hbm_arena=hbm, read_buffer_bytes=8 << 20,
+                      write_buffer_bytes=16 << 20, max_new=64, max_ctx=512, autotune=False)
+    rng = np.random.default_rng(1)
+    jobs = []
+    for sid, kept, n, bids in [("a", 200, 17, [0, 1]), ("b", 0, 23, [2]), ("c", 256, 9, [3, 4, 5]),
+                               ("d", 300, 31, [6, 7, 8])]:
+        off = torch.as_tensor([b * bb // 2 for b in bids], dtype=torch.int64, device="cuda")
+        jobs.append(Job(sid, torch.as_tensor(rng.integers(0, shape.vocab, n)).cuda(), kept=kept,
+                        source="hbm" if kept else "none", block_ids=bids, save=True,
+                        dev_block_off=off if kept else None))
+    res = r.run(jobs, want_logits=True, batch=True)
+    r.join()
+    torch.cuda.synchronize()
+    Runner.finalize(res)
+    assert all(torch.isfinite(x.logits).all() for x in res)
+    print("batched varlen pass ok", flush=True)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="", choices=["", "attn", "rope", "provenance", "engine_graph",
-                                                   "engine_stream"])
+                                                   "engine_stream", "batch"])
     a = ap.parse_args()
     from paper_2403_19708_b200 import build
     build.build()
@@ -158,5 +186,7 @@ if __name__ == "__main__":
         rope_cases()
     if a.only == "provenance":
         provenance_cases()
+    if a.only == "batch":
+        batch_cases()
     if a.only.startswith("engine_"):
         engine_turns(a.only == "engine_graph")
