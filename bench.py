@@ -309,8 +309,12 @@ def run_serving(args, rank: int, device: int) -> dict:
     import torch
 
     from paper_2403_19708_b200 import serve
+    # every rank of the node pins its own arena: stay within 60 % of the
+    # available host memory across the node's ranks
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+    dram_gb = min(args.serve_dram_gb, host_mem_available() * 0.6 / local_world / 1e9)
     sa = serve.parse(["--config", args.config, "--shard", str(rank), "--of", "8",
-                      "--device", str(device), "--dram-gb", str(args.serve_dram_gb),
+                      "--device", str(device), "--dram-gb", f"{dram_gb:.1f}",
                       "--hbm-gb", str(args.serve_hbm_gb)])
     t0 = time.perf_counter()
     out = serve.run(sa)
