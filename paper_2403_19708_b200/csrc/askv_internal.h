@@ -86,6 +86,13 @@ int rope_new_stamped(const void* qkv, int64_t qkv_row_stride, int n_new, int n_h
                      int n_kv_heads, int head_dim, const float* rope_table, int table_positions,
                      int pos0, void* q_out, void* kv_out, int64_t kv_row_stride, void* save_out,
                      void* stream, unsigned long long* end);
+// rope_new for a batch of jobs in one launch (their new tokens consecutive
+// in qkv / q_out; per job its first position and K|V / save destinations).
+int rope_new_batch(const void* qkv, int64_t qkv_row_stride, int n_jobs, const int* n_new,
+                   const int* pos0, int n_heads, int n_kv_heads, int head_dim,
+                   const float* rope_table, int table_positions, void* q_out,
+                   void* const* kv_out, int64_t kv_row_stride, void* const* save_out,
+                   void* stream, unsigned long long* end);
 int reembed_stamped(const void* src_base, const int64_t* src_block_off, int block_tokens,
                     int64_t src_row_stride, int64_t first_token, int kept, int n_kv_heads,
                     int head_dim, const float* rope_table, int table_positions,

@@ -181,20 +181,42 @@ __global__ void __launch_bounds__(kThreads)
 // with kRopeIlp loads in flight per thread.
 constexpr int kRopeIlp = 4;
 
+// Batched rope_new (askv_prefill_layers_batch): the jobs' new tokens are
+// consecutive rows of qkv / q_out; token i of the launch belongs to the job
+// with the last tok0 <= i, which has its own first position (its kept rows)
+// and its own K|V and save destinations.  By value in the kernel parameters.
+constexpr int kMaxRopeJobs = 24;
+struct RopeJobs {
+  int n;   // 0: one job (the scalar arguments)
+  int tok0[kMaxRopeJobs];
+  int pos0[kMaxRopeJobs];
+  __nv_bfloat16* kv_out[kMaxRopeJobs];
+  __nv_bfloat16* save_out[kMaxRopeJobs];
+};
+
 template <int HD>
 __global__ void __launch_bounds__(kThreads)
     rope_new_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t qkv_row_stride, int n_new,
                     int hq, int hkv, const float* __restrict__ table, int pos0,
                     __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ kv_out,
                     int64_t kv_row_stride, __nv_bfloat16* __restrict__ save_out,
-                    unsigned long long* __restrict__ end) {
+                    unsigned long long* __restrict__ end, const __grid_constant__ RopeJobs rj) {
   constexpr int kUnitsPerHead = HD / 8;
   const int q_units = hq * kUnitsPerHead;
   const int k_units = hkv * kUnitsPerHead;
   const int row_units = q_units + 2 * k_units;
   const int i = blockIdx.y;
   const __nv_bfloat16* src = qkv + (int64_t)i * qkv_row_stride;
-  const float* cs_row = table + (int64_t)(pos0 + i) * HD;  // (cos, sin) x HD/2
+  int li = i;   // the token's index within its job
+  if (rj.n > 0) {
+    int j = 0;
+    while (j + 1 < rj.n && rj.tok0[j + 1] <= i) ++j;
+    li = i - rj.tok0[j];
+    pos0 = rj.pos0[j];
+    kv_out = rj.kv_out[j];
+    save_out = rj.save_out[j];
+  }
+  const float* cs_row = table + (int64_t)(pos0 + li) * HD;  // (cos, sin) x HD/2
   for (int u0 = blockIdx.x * kThreads * kRopeIlp + threadIdx.x; u0 < row_units;
        u0 += gridDim.x * kThreads * kRopeIlp) {
     int4 x[kRopeIlp];
@@ -212,8 +234,8 @@ __global__ void __launch_bounds__(kThreads)
         st16(q_out + (int64_t)i * q_units * 8 + u * 8, rotate8(x[k], cs));
       } else {
         const int ku = u - q_units;  // [0, 2*k_units): K then V, same as the row layout
-        if (save_out != nullptr) st16(save_out + (int64_t)i * 2 * k_units * 8 + ku * 8, x[k]);
-        st16_keep(kv_out + (int64_t)i * kv_row_stride + ku * 8,
+        if (save_out != nullptr) st16(save_out + (int64_t)li * 2 * k_units * 8 + ku * 8, x[k]);
+        st16_keep(kv_out + (int64_t)li * kv_row_stride + ku * 8,
                   ku < k_units ? rotate8(x[k], cs) : x[k]);
       }
     }
@@ -356,15 +378,63 @@ int askv::rope_new_stamped(const void* qkv, int64_t qkv_row_stride, int n_new, i
   auto* qo = static_cast<__nv_bfloat16*>(q_out);
   auto* kvo = static_cast<__nv_bfloat16*>(kv_out);
   auto* so = static_cast<__nv_bfloat16*>(save_out);
+  RopeJobs one;
+  one.n = 0;
   if (head_dim == 128)
     rope_new_kernel<128><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
         x, qkv_row_stride, n_new, n_heads, n_kv_heads, rope_table, pos0, qo, kvo,
-        kv_row_stride, so, end);
+        kv_row_stride, so, end, one);
   else
     rope_new_kernel<64><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
         x, qkv_row_stride, n_new, n_heads, n_kv_heads, rope_table, pos0, qo, kvo,
-        kv_row_stride, so, end);
+        kv_row_stride, so, end, one);
   return launch_status("rope_new launch");
+}
+
+int askv::rope_new_batch(const void* qkv, int64_t qkv_row_stride, int n_jobs, const int* n_new,
+                         const int* pos0, int n_heads, int n_kv_heads, int head_dim,
+                         const float* rope_table, int table_positions, void* q_out,
+                         void* const* kv_out, int64_t kv_row_stride, void* const* save_out,
+                         void* stream, unsigned long long* end) {
+  ASKV_REQUIRE(n_jobs >= 1 && n_heads > 0 && n_kv_heads > 0 && n_heads % n_kv_heads == 0,
+               "rope_new_batch: bad jobs=%d hq=%d hkv=%d", n_jobs, n_heads, n_kv_heads);
+  ASKV_REQUIRE(head_dim == 64 || head_dim == 128, "rope_new_batch: head_dim %d", head_dim);
+  const int row_units = (n_heads + 2 * n_kv_heads) * (head_dim / 8);
+  const int64_t q_stride_el = (int64_t)n_heads * head_dim;
+  int tok = 0;
+  for (int i0 = 0; i0 < n_jobs; i0 += kMaxRopeJobs) {   // <= kMaxRopeJobs jobs per launch
+    RopeJobs rj;
+    rj.n = n_jobs - i0 < kMaxRopeJobs ? n_jobs - i0 : kMaxRopeJobs;
+    int tokens = 0;
+    for (int k = 0; k < rj.n; ++k) {
+      const int i = i0 + k;
+      ASKV_REQUIRE(n_new[i] > 0 && pos0[i] >= 0 && pos0[i] + n_new[i] <= table_positions &&
+                       kv_out[i],
+                   "rope_new_batch: job %d (n_new %d, pos0 %d, table %d)", i, n_new[i], pos0[i],
+                   table_positions);
+      rj.tok0[k] = tokens;
+      rj.pos0[k] = pos0[i];
+      rj.kv_out[k] = static_cast<__nv_bfloat16*>(kv_out[i]);
+      rj.save_out[k] = save_out ? static_cast<__nv_bfloat16*>(save_out[i]) : nullptr;
+      tokens += n_new[i];
+    }
+    ASKV_REQUIRE(tokens <= 65535, "rope_new_batch: %d tokens exceed the grid's y limit", tokens);
+    const dim3 grid((row_units + kThreads * kRopeIlp - 1) / (kThreads * kRopeIlp), tokens);
+    auto* x = static_cast<const __nv_bfloat16*>(qkv) + (int64_t)tok * qkv_row_stride;
+    auto* qo = static_cast<__nv_bfloat16*>(q_out) + (int64_t)tok * q_stride_el;
+    if (head_dim == 128)
+      rope_new_kernel<128><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+          x, qkv_row_stride, tokens, n_heads, n_kv_heads, rope_table, 0, qo, nullptr,
+          kv_row_stride, nullptr, end, rj);
+    else
+      rope_new_kernel<64><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
+          x, qkv_row_stride, tokens, n_heads, n_kv_heads, rope_table, 0, qo, nullptr,
+          kv_row_stride, nullptr, end, rj);
+    const int rc = launch_status("rope_new_batch launch");
+    if (rc) return rc;
+    tok += tokens;
+  }
+  return ASKV_OK;
 }
 
 extern "C" int askv_rotate_rows(const void* x, int64_t x_row_stride, int n_rows, int n_heads,

@@ -766,15 +766,35 @@ static int issue_layers_multi(const askv_prefill_plan* ps, int nj, cudaStream_t 
                              tl ? ts(l == 0 ? 0 : st - 7) : nullptr));
     ASKV_TRY(gemm(p->h, p->w_qkv[l], p->qkv, n, qkv_cols, d, false, p->gemm_ws,
                   p->gemm_ws_bytes, s));
+    if (nj > 1) {  // new tokens of every job in one launch (each its own positions)
+      std::vector<int> nn(nj), p0(nj);
+      std::vector<void*> kvo(nj), sro(nj);
+      bool any_save = false;
+      for (int i = 0; i < nj; ++i) {
+        const askv_prefill_plan* q = jv[i].p;
+        nn[i] = q->n_new;
+        p0[i] = q->kept;
+        kvo[i] = kv_of(q, l) + (int64_t)q->kept * row;
+        sro[i] = q->save_rows ? q->save_rows[l] : nullptr;
+        any_save = any_save || sro[i];
+        if (sro[i]) wait(q->ev_save_free, l, s);
+      }
+      ASKV_TRY(rope_new_batch(p->qkv, qkv_cols, nj, nn.data(), p0.data(), hq, hkv, hd,
+                              p->rope_table, p->rope_positions, p->q_rot, kvo.data(), row,
+                              any_save ? sro.data() : nullptr, s,
+                              jv[0].waits ? ts(st + 1) : nullptr));
+    }
     for (const JobView& v : jv) {  // new tokens: rotate q / k, pre-RoPE rows for the saver
       const askv_prefill_plan* q = v.p;
       const int nq = q->n_new;
       void* save_rows = q->save_rows ? q->save_rows[l] : nullptr;
-      if (save_rows) wait(q->ev_save_free, l, s);
-      ASKV_TRY(rope_new_stamped(q->qkv, qkv_cols, nq, hq, hkv, hd, q->rope_table,
-                                q->rope_positions, q->kept, q->q_rot,
-                                kv_of(q, l) + (int64_t)q->kept * row, row, save_rows, s,
-                                v.waits ? ts_of(q, st + 1) : nullptr));
+      if (nj == 1) {
+        if (save_rows) wait(q->ev_save_free, l, s);
+        ASKV_TRY(rope_new_stamped(q->qkv, qkv_cols, nq, hq, hkv, hd, q->rope_table,
+                                  q->rope_positions, q->kept, q->q_rot,
+                                  kv_of(q, l) + (int64_t)q->kept * row, row, save_rows, s,
+                                  v.waits ? ts_of(q, st + 1) : nullptr));
+      }
       if (save_rows) rec(q->ev_save_ready, l, s);
       if (save_rows && q->mirror_base) {  // HBM tier write-through, in stream order
         ASKV_TRY(askv_save_layer(q->mirror_base, q->mirror_block_ids, q->mirror_nblocks,

@@ -59,23 +59,46 @@ def _mbind(addr: int, length: int, node: int) -> None:
         raise OSError(e, f"mbind(node {node}): {os.strerror(e)}")
 
 
+class _Region:
+    """An mbind'ed anonymous mapping, registered with CUDA while alive: the
+    registration is dropped before the mapping goes (a later mapping at the
+    same address could not be registered otherwise)."""
+
+    def __init__(self, nbytes: int, node: int, pin: bool):
+        import torch
+
+        self.mm = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+        self.addr = ctypes.addressof(ctypes.c_char.from_buffer(self.mm))
+        self.registered = False
+        _mbind(self.addr, nbytes, node)
+        if pin:
+            err = torch.cuda.cudart().cudaHostRegister(self.addr, nbytes, 0)
+            if int(err) != 0:
+                raise RuntimeError(f"cudaHostRegister of {nbytes} B failed: {err}")
+            self.registered = True
+
+    def __del__(self):
+        if self.registered:
+            try:
+                import torch
+
+                torch.cuda.synchronize()
+                torch.cuda.cudart().cudaHostUnregister(self.addr)
+            except Exception:  # noqa: BLE001 - interpreter teardown
+                pass
+            self.registered = False
+
+
 def host_buffer(nbytes: int, node: int, *, pin: bool = True):
     """(uint8 tensor of `nbytes` on NUMA node `node`, node).  pin=True
-    page-locks and registers it with CUDA (cudaHostRegister)."""
+    page-locks and registers it with CUDA (cudaHostRegister); the
+    registration lives as long as the returned tensor object (keep it, e.g.
+    as HostArena.buffer, for as long as views of it are in use)."""
     import torch
 
     if node < 0 or node >= max(1, node_count()):
         raise ValueError(f"no NUMA node {node} (host has {node_count()})")
-    mm = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
-    addr = ctypes.addressof(ctypes.c_char.from_buffer(mm))
-    _mbind(addr, nbytes, node)
-    buf = torch.frombuffer(mm, dtype=torch.uint8)
-    if pin:
-        rt = torch.cuda.cudart()
-        err = rt.cudaHostRegister(addr, nbytes, 0)
-        if int(err) != 0:
-            raise RuntimeError(f"cudaHostRegister of {nbytes} B failed: {err}")
-        buf._askv_registered = (addr, mm)   # keep the mapping alive with the tensor
-    else:
-        buf._askv_registered = (None, mm)
+    region = _Region(nbytes, node, pin)
+    buf = torch.frombuffer(region.mm, dtype=torch.uint8)
+    buf._askv_region = region
     return buf, node

@@ -163,7 +163,7 @@ def batch_cases():
                                ("d", 300, 31, [6, 7, 8])]:
         off = torch.as_tensor([b * bb // 2 for b in bids], dtype=torch.int64, device="cuda")
         jobs.append(Job(sid, torch.as_tensor(rng.integers(0, shape.vocab, n)).cuda(), kept=kept,
-                        source="hbm" if kept else "none", block_ids=bids, save=True,
+                        source="hbm" if kept else "none", block_ids=bids, save=bool(kept),
                         dev_block_off=off if kept else None))
     res = r.run(jobs, want_logits=True, batch=True)
     r.join()
