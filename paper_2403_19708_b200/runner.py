@@ -394,10 +394,11 @@ class Runner:
         self.probe = None          # list -> (kind, ev0, ev1, work) per probed launch
 
     # ------------------------------------------------------------------ buffers
-    def _buf(self, name, rows, cols, dtype=BF16):
+    def _buf(self, name, rows, cols, dtype=BF16, zero=False):
         t = self._bufs.get(name)
         if t is None or t.shape[0] < rows or t.shape[1] != cols:
-            t = torch.empty((max(rows, 1), cols), dtype=dtype, device=self.device)
+            alloc = torch.zeros if zero else torch.empty
+            t = alloc((max(rows, 1), cols), dtype=dtype, device=self.device)
             self._bufs[name] = t
         return t[:rows]
 
@@ -625,7 +626,12 @@ class Runner:
         big = {"x": self._buf("bx", tot, s.d_model), "h": self._buf("h", tot, s.d_model),
                "qkv": self._buf("qkv", tot, s.qkv_cols), "q": self._buf("q", tot, hq * hd),
                "ao": self._buf("ao", tot, hq * hd), "gu": self._buf("gu", tot, 2 * s.ffn),
-               "act": self._buf("act", tot, s.ffn), "kv": self._buf("kv", kv_rows, self.row_elems)}
+               "act": self._buf("act", tot, s.ffn),
+               # zero-initialised once: a varlen K3 reads past each job's last row
+               # into the next job's (masked, P = 0) -- rows that must hold finite
+               # values (0 x NaN would poison the output); they are zeros or
+               # rows written by earlier passes, never uninitialised memory
+               "kv": self._buf("kv", kv_rows, self.row_elems, zero=True)}
         # one attention workspace for the whole batch (its K3s run one after
         # another on the compute stream): size it for the largest job first, so
         # no job's plan keeps a pointer to a buffer a later job reallocated
@@ -786,7 +792,8 @@ class Runner:
                 self._pinned_inflight.append((src, done))
             if batch is None:
                 x = F.embedding(ids, self.w.embed)
-                buf = lambda name, rows, cols: self._buf(name, rows, cols)  # noqa: E731
+                buf = lambda name, rows, cols: self._buf(  # noqa: E731
+                    name, rows, cols, zero=name == "kv")   # shared with batched passes
             else:   # this job's rows of the batch's shared buffers
                 x = batch["x"]
                 torch.index_select(self.w.embed, 0, ids, out=x)

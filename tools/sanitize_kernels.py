@@ -169,7 +169,11 @@ def batch_cases():
     r.join()
     torch.cuda.synchronize()
     Runner.finalize(res)
-    assert all(torch.isfinite(x.logits).all() for x in res)
+    for j, x in zip(jobs, res):
+        fin = bool(torch.isfinite(x.logits).all())
+        print(f"job {j.session_id} kept={j.kept} n={j.n_new} finite={fin} "
+              f"max={float(x.logits.abs().max()):.3g}", flush=True)
+        assert fin, j.session_id
     print("batched varlen pass ok", flush=True)
 
 
