@@ -33,14 +33,24 @@ namespace askv {
 namespace {
 
 // Optional in-kernel timeline (tools/attn_trace.cu builds with ASKV_ATTN_TRACE):
-// globaltimer stamps per CTA at fixed slots.
+// globaltimer stamps per CTA at fixed slots (256 per CTA; 192..255: phases of
+// the softmax tile of WG0's thread 0, tiles 2..17).
 #ifdef ASKV_ATTN_TRACE
 __device__ unsigned long long* g_attn_trace = nullptr;
 __device__ __forceinline__ void trace_stamp(int slot) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-  if (g_attn_trace) g_attn_trace[cta * 192 + slot] = t;
+  if (g_attn_trace) {
+    g_attn_trace[cta * 256 + slot] = t;
+    if (slot == 0) {
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      g_attn_trace[cta * 256 + 5] = sm;  // slot 5: SM id
+      g_attn_trace[cta * 256 + 6] = clock64();  // slots 6 / 7: SM clock at entry / exit
+    }
+    if (slot == 4) g_attn_trace[cta * 256 + 7] = clock64();
+  }
 }
 #define ATTN_TRACE(slot) trace_stamp(slot)
 #else
@@ -472,15 +482,18 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
           if (k_next) wait_k(j + 1);
           if (j < nt_a) {
             mbar_wait(&p_full[0], j & 1);
+            if (j < 28) ATTN_TRACE(64 + j);
             tc_fence_after();
             issue_pv(0, j, j == 0);
             if (j + 1 < nt_a) issue_s(0, j + 1);
           }
           if (j < nt_b) {
             mbar_wait(&p_full[1], j & 1);
+            if (j < 28) ATTN_TRACE(96 + j);
             tc_fence_after();
             issue_pv(1, j, j == 0);
             if (j + 1 < nt_b) issue_s(1, j + 1);
+            if (j < 28) ATTN_TRACE(160 + j);
           }
           umma_commit(&v_empty[j % C::kVStages]);
           if (k_next) umma_commit(&k_empty[(j + 1) % C::kKStages]);
@@ -537,6 +550,8 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
       for (int c = 0; c < kBN / 32; ++c)
         tmem_ld32_nowait(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
       tmem_wait_ld();
+      const bool trace_t = threadIdx.x == 0 && t >= 2 && t < 18;
+      if (trace_t) ATTN_TRACE(192 + 4 * (t - 2));
       if (kMask) {
 #pragma unroll
         for (int e = 0; e < kBN; ++e) sr[e] = (e <= lim) ? sr[e] : 0xff800000u;  // -inf
@@ -554,6 +569,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
       }
       const float m_tile = fmax3(fmax3(a0, a1, a2), a3, -INFINITY) * sl2;
       const bool need = m_tile > m_acc + C::kRescaleLog2;
+      if (trace_t) ATTN_TRACE(193 + 4 * (t - 2));
       if (t > 0) {
         // Every PV's completion phase is consumed here (compute-sanitizer
         // synccheck flags a phase nobody waits for).  Free: s_full of S(t) was
@@ -608,6 +624,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
       }
       const float2 la = fadd2(ls0, ls1), lb = fadd2(ls2, ls3);
       l_acc += (la.x + la.y) + (lb.x + lb.y);
+      if (trace_t) ATTN_TRACE(194 + 4 * (t - 2));
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&p_full[w]);
@@ -1612,35 +1629,49 @@ int launch_varlen(const VarlenBatch& b, cudaStream_t stream, unsigned long long*
   prm.scale_log2 = b.scale * 1.4426950408889634f;
   prm.stamp = stamp;
   prm.v_row_elems = use_vs ? b.vsrc_row_elems : 1;
-  auto kern = attn_fwd_kernel<HD, false>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg<HD, false>::kSmemBytes);
+  // Pair two query tiles of a job per CTA when the batch has more than a wave
+  // of query tiles (the usual case): each K/V tile feeds 256 query rows and
+  // the per-CTA prologue / epilogue is paid once per two tiles.  A job's odd
+  // last tile runs alone in the paired kernel (its CTA-uniform unpaired mode).
+  int q_tiles_all = 0;
+  for (int i = 0; i < b.n; ++i) q_tiles_all += (b.n_new[i] * pack + kBM - 1) / kBM;
+  const bool pair = pack == 1 && use_pairs(q_tiles_all, heads, sm_count());
+  const int qt_per_cta = pair ? 2 : 1;
+  auto kern = pair ? attn_fwd_kernel<HD, true> : attn_fwd_kernel<HD, false>;
+  const int smem = pair ? Cfg<HD, true>::kSmemBytes : Cfg<HD, false>::kSmemBytes;
+  static bool attr[2] = {false, false};
+  if (!attr[pair]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "attn smem attribute");
-    attr = true;
+    attr[pair] = true;
   }
+  // jobs in descending KV length: the longest CTAs start first and the last
+  // wave is made of short ones (longest-processing-time-first)
+  int order[kMaxVarJobs];
   for (int i0 = 0; i0 < b.n; i0 += kMaxVarJobs) {   // <= kMaxVarJobs jobs per launch
     VarJobs vj;
     vj.n = std::min(kMaxVarJobs, b.n - i0);
+    for (int k = 0; k < vj.n; ++k) order[k] = i0 + k;
+    std::stable_sort(order, order + vj.n, [&](int x, int y) {
+      return b.n_cached[x] + b.n_new[x] > b.n_cached[y] + b.n_new[y];
+    });
     int ctas = 0;
     for (int k = 0; k < vj.n; ++k) {
-      const int i = i0 + k;
+      const int i = order[k];
       VarJob& J = vj.j[k];
       J.n_new = b.n_new[i];
       J.n_cached = b.n_cached[i];
       J.q_row0 = b.q_row0[i];
       J.kv_row0 = b.kv_row0[i];
       J.cta0 = ctas;
-      J.q_groups = (b.n_new[i] * pack + kBM - 1) / kBM;
+      J.q_groups = (b.n_new[i] * pack + kBM * qt_per_cta - 1) / (kBM * qt_per_cta);
       J.v_src_tiles = use_vs ? b.v_src_tiles[i] : 0;
       J.v_blk_off = use_vs ? b.v_blk_off[i] : nullptr;
       J.v_layer_row = b.v_layer_row;
       J.out = static_cast<__nv_bfloat16*>(b.out[i]);
       ctas += J.q_groups * heads;
     }
-    kern<<<ctas, Cfg<HD, false>::kThreads, Cfg<HD, false>::kSmemBytes, stream>>>(mq, mk, mv, mvs,
-                                                                                 prm, vj);
+    kern<<<ctas, Cfg<HD, false>::kThreads, smem, stream>>>(mq, mk, mv, mvs, prm, vj);
     rc = launch_status("attn_fwd varlen launch");
     if (rc) return rc;
   }

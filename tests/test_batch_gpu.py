@@ -14,11 +14,10 @@ pytestmark = pytest.mark.gpu
 TOL = 2e-2
 
 
-def _setup(bt=16):
+def _setup(bt=16, nb=40, max_new=64):
     from paper_2403_19708_b200 import model, runner
     from paper_2403_19708_b200.store import HostArena
     shape = model.shape("tiny")
-    nb = 40
     arena = HostArena(nb, bt * shape.kv_bytes_per_token, pin=True)
     hbm = torch.empty(nb * bt * shape.kv_bytes_per_token // 2, dtype=torch.bfloat16,
                       device="cuda")
@@ -26,7 +25,7 @@ def _setup(bt=16):
     hbm.normal_(generator=g)
     arena.buffer.view(torch.bfloat16).copy_(hbm.cpu())
     r = runner.Runner(shape, seed=4, block_tokens=bt, host_arena=arena, hbm_arena=hbm,
-                      read_buffer_bytes=8 << 20, write_buffer_bytes=16 << 20, max_new=64,
+                      read_buffer_bytes=8 << 20, write_buffer_bytes=16 << 20, max_new=max_new,
                       max_ctx=512, autotune=False)
     return shape, r, arena, hbm
 
@@ -43,7 +42,15 @@ MIXES = {
     "varlen_vsrc128": [("a", 200, 17, "hbm", [0, 1]), ("b", 0, 23, "none", [2]),
                        ("c", 256, 9, "hbm", [3, 4, 5]), ("d", 300, 31, "hbm", [6, 7, 8])],
 }
-BT = {"mixed": 16, "varlen": 16, "varlen_vsrc128": 128}
+# more than one query tile per job: with ASKV_ATTN_PAIR=1 (test below) the
+# varlen launch pairs a job's tiles per CTA, odd last tiles running alone
+LONG = {"varlen_long": [("a", 40, 300, "hbm", list(range(0, 22))),
+                        ("b", 0, 150, "none", list(range(55, 65))),
+                        ("c", 130, 257, "hbm", list(range(23, 48))),
+                        ("d", 64, 40, "hbm", list(range(48, 55)))]}
+MIXES.update(LONG)
+BT = {"mixed": 16, "varlen": 16, "varlen_vsrc128": 128, "varlen_long": 16}
+SETUP = {"varlen_long": dict(nb=66, max_new=320)}
 
 
 def _jobs(shape, r, bt, rng, mix):
@@ -80,7 +87,7 @@ def _stored(shape, buf_bf16, bids, bt, rows):
 def test_batched_prefill_matches_oracle_and_single_runs(mix):
     from paper_2403_19708_b200.runner import Runner
     bt = BT[mix]
-    shape, r, arena, hbm = _setup(bt)
+    shape, r, arena, hbm = _setup(bt, **SETUP.get(mix, {}))
     wnp = r.w.to_numpy()
     rng = np.random.default_rng(5)
     jobs = _jobs(shape, r, bt, rng, mix)
@@ -119,3 +126,18 @@ def test_batched_prefill_matches_oracle_and_single_runs(mix):
         for layer in range(shape.layers):
             for a, b in zip(got[layer], batched_saved[j.session_id][layer]):
                 assert np.allclose(a, b, rtol=1e-2, atol=1e-2), (j.session_id, layer)
+
+
+def test_batched_prefill_paired_varlen():
+    """The long mix with paired query tiles forced on (csrc/attention.cu
+    use_pairs, read once per process: run in a subprocess)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+            "from test_batch_gpu import *;"
+            "test_batched_prefill_matches_oracle_and_single_runs('varlen_long')")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       env=dict(os.environ, ASKV_ATTN_PAIR="1"))
+    assert r.returncode == 0, r.stderr[-3000:]

@@ -51,14 +51,14 @@ int main(int argc, char** argv) {
   cudaMalloc(&ws, wsb + 16);
   const int ctas = 160;
   unsigned long long* tr;
-  cudaMalloc(&tr, (size_t)ctas * 192 * 8);
+  cudaMalloc(&tr, (size_t)ctas * 256 * 8);
   cudaMemcpyToSymbol(askv::g_attn_trace, &tr, sizeof(tr));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   float ms = 0;
   for (int rep = 0; rep < 5; ++rep) {
-    cudaMemset(tr, 0, (size_t)ctas * 192 * 8);
+    cudaMemset(tr, 0, (size_t)ctas * 256 * 8);
     cudaEventRecord(e0);
     int rc = askv_prefill_attn(q, kv, 2LL * hkv * d, kept, n, hq, hkv, d, 0.088f, out, ws, wsb,
                                0, nullptr);
@@ -67,22 +67,22 @@ int main(int argc, char** argv) {
     cudaDeviceSynchronize();
     cudaEventElapsedTime(&ms, e0, e1);
   }
-  std::vector<unsigned long long> h((size_t)ctas * 192);
+  std::vector<unsigned long long> h((size_t)ctas * 256);
   cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost);
   unsigned long long t0 = ~0ull, tend = 0;
   int ran = 0;
   for (int c = 0; c < ctas; ++c) {
-    if (!h[c * 192]) continue;
+    if (!h[c * 256]) continue;
     ran = c + 1;
-    t0 = std::min(t0, h[c * 192]);
-    tend = std::max(tend, h[c * 192 + 4]);
+    t0 = std::min(t0, h[c * 256]);
+    tend = std::max(tend, h[c * 256 + 4]);
   }
   printf("kept=%d n=%d hq=%d ctas=%d span %.2f us (events %.2f us incl. combine)\n", kept, n,
          hq, ran, (tend - t0) * 1e-3, ms * 1e3);
   auto us = [&](unsigned long long v) { return v ? (v - t0) * 1e-3 : -1.0; };
   std::vector<double> ent, tm, ex;
   for (int c = 0; c < ran; ++c) {
-    const unsigned long long* r = &h[c * 192];
+    const unsigned long long* r = &h[c * 256];
     ent.push_back(us(r[0]));
     tm.push_back(us(r[1]));
     ex.push_back(us(r[4]));
@@ -94,7 +94,7 @@ int main(int argc, char** argv) {
   printf("tmem   min %.2f p50 %.2f max %.2f\n", tm[0], tm[ran / 2], tm[ran - 1]);
   printf("exit   min %.2f p50 %.2f max %.2f\n", ex[0], ex[ran / 2], ex[ran - 1]);
   for (int c : {0, 1, ran / 2, ran - 1}) {
-    const unsigned long long* r = &h[c * 192];
+    const unsigned long long* r = &h[c * 256];
     printf("cta %d: entry %.2f tmem %.2f | pieces (q, o_free):", c, us(r[0]), us(r[1]));
     for (int k = 0; k < 4 && r[40 + 2 * k]; ++k) printf(" [%.2f %.2f]", us(r[40 + 2 * k]), us(r[41 + 2 * k]));
     printf(" | WG0 tiles:");

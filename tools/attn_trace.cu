@@ -51,24 +51,24 @@ int main(int argc, char** argv) {
   cudaMalloc(&ws, wsb + 16);
   const int ctas = ((n + 127) / 128) * hq * splits;
   unsigned long long* tr;
-  cudaMalloc(&tr, (size_t)ctas * 192 * 8);
+  cudaMalloc(&tr, (size_t)ctas * 256 * 8);
   cudaMemcpyToSymbol(askv::g_attn_trace, &tr, sizeof(tr));
   for (int rep = 0; rep < 5; ++rep) {
-    cudaMemset(tr, 0, (size_t)ctas * 192 * 8);
+    cudaMemset(tr, 0, (size_t)ctas * 256 * 8);
     int rc = askv_prefill_attn(q, kv, 2LL * hkv * d, kept, n, hq, hkv, d, 0.088f, out, ws, wsb,
                                splits, nullptr);
     if (rc) { printf("rc %d %s\n", rc, g_err); return 1; }
     cudaDeviceSynchronize();
   }
-  std::vector<unsigned long long> h((size_t)ctas * 192);
+  std::vector<unsigned long long> h((size_t)ctas * 256);
   cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost);
   unsigned long long t0 = ~0ull, tend = 0;
   int used = 0;  // CTAs that ran (the buffer is sized for one query tile per CTA)
   for (int c = 0; c < ctas; ++c) {
-    if (!h[c * 192]) continue;
+    if (!h[c * 256]) continue;
     used = c + 1;
-    t0 = std::min(t0, h[c * 192]);
-    tend = std::max(tend, h[c * 192 + 4]);
+    t0 = std::min(t0, h[c * 256]);
+    tend = std::max(tend, h[c * 256 + 4]);
   }
   const int ran = used;
   printf("kept=%d n=%d hq=%d splits=%d ctas=%d span %.2f us\n", kept, n, hq, splits, ctas,
@@ -76,7 +76,7 @@ int main(int argc, char** argv) {
   double s_entry = 0, s_tmem = 0, s_q = 0, s_first = 0, s_loop = 0, s_epi = 0, s_exit = 0;
   int cnt = 0;
   for (int c = 0; c < ctas; ++c) {
-    const unsigned long long* r = &h[c * 192];
+    const unsigned long long* r = &h[c * 256];
     if (!r[3]) continue;
     ++cnt;
     s_entry += r[0] - t0;
@@ -94,7 +94,7 @@ int main(int argc, char** argv) {
          cnt, s_entry / cnt * 1e-3, s_tmem / cnt * 1e-3, s_q / cnt * 1e-3, s_first / cnt * 1e-3,
          s_loop / cnt * 1e-3, s_epi / cnt * 1e-3, s_exit / cnt * 1e-3);
   for (int c : {0, 1, ran / 2, ran - 1}) {
-    const unsigned long long* r = &h[c * 192];
+    const unsigned long long* r = &h[c * 256];
     printf("cta %d: entry %.2f tmem %.2f q %.2f |", c, (r[0] - t0) * 1e-3, (r[1] - t0) * 1e-3,
            (r[2] - t0) * 1e-3);
     for (int t = 0; t < 28 && r[8 + 2 * t]; ++t)

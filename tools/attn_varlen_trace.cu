@@ -1,0 +1,202 @@
+// In-kernel timeline of the batched (varlen) K3 launch: the 16 C3 turns of
+// bench.py (kept, new) in one launch, built with ASKV_ATTN_TRACE.  Reports the
+// SM fill (sum of CTA lifetimes / (span x SMs)), the gap between one CTA's
+// exit and the next CTA's entry on the same SM, a least-squares split of a
+// CTA's lifetime into a fixed cost + a per-KV-tile cost, and the tail (span
+// after the first SM runs out of work).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DASKV_ATTN_TRACE \
+//        -Ipaper_2403_19708_b200/csrc tools/attn_varlen_trace.cu -o tools/attn_varlen_trace -lcuda
+#include "../paper_2403_19708_b200/csrc/attention.cu"
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <vector>
+
+static char g_err[512];
+namespace askv {
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+void clear_error() { g_err[0] = 0; }
+}  // namespace askv
+
+__global__ void fill_bf16(__nv_bfloat16* p, size_t n, uint32_t seed) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    uint32_t x = (uint32_t)i * 2654435761u ^ seed;
+    x ^= x >> 13;
+    x *= 0x5bd1e995u;
+    x ^= x >> 15;
+    p[i] = __float2bfloat16(((int)(x & 0xffff) - 32768) * (2.0f / 32768.f));
+  }
+}
+
+__global__ void clock_probe(double* mhz) {
+  unsigned long long g0, g1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  const long long c0 = clock64();
+  do { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1)); } while (g1 - g0 < 200000);
+  const long long c1 = clock64();
+  *mhz = (double)(c1 - c0) / (double)(g1 - g0) * 1e3;
+}
+
+int main() {
+  // bench.py select_turns("c3", 0, 1, 16): (kept, new)
+  const int J[16][2] = {{3018, 414}, {422, 94},   {2741, 217}, {1000, 173},
+                        {3047, 163}, {2883, 287}, {3377, 443}, {1963, 196},
+                        {3117, 351}, {276, 90},   {3653, 374}, {1815, 369},
+                        {2855, 422}, {3675, 412}, {3379, 315}, {228, 97}};
+  const int n = 16, hq = 40, hkv = 40, d = 128;
+  std::vector<int> nn(n), nc(n), q0(n), k0(n);
+  int qt = 0, kt = 0;
+  double flops = 0;
+  for (int i = 0; i < n; ++i) {
+    nc[i] = J[i][0];
+    nn[i] = J[i][1];
+    q0[i] = qt;
+    k0[i] = kt;
+    qt += nn[i];
+    kt += nc[i] + nn[i];
+    flops += 4.0 * hq * d * ((double)nn[i] * nc[i] + nn[i] * (nn[i] + 1) / 2.0);
+  }
+  void *q, *kv, *out;
+  cudaMalloc(&q, (size_t)qt * hq * d * 2);
+  cudaMalloc(&kv, (size_t)kt * 2 * hkv * d * 2);
+  cudaMalloc(&out, (size_t)qt * hq * d * 2);
+  fill_bf16<<<1184, 256>>>((__nv_bfloat16*)q, (size_t)qt * hq * d, 7u);
+  fill_bf16<<<1184, 256>>>((__nv_bfloat16*)kv, (size_t)kt * 2 * hkv * d, 11u);
+  std::vector<void*> outs(n);
+  for (int i = 0; i < n; ++i) outs[i] = (char*)out + (size_t)q0[i] * hq * d * 2;
+  askv::VarlenBatch b;
+  b.n = n;
+  b.q = q;
+  b.kv = kv;
+  b.kv_row_stride = 2LL * hkv * d;
+  b.hq = hq;
+  b.hkv = hkv;
+  b.head_dim = d;
+  b.scale = 0.088f;
+  b.n_new = nn.data();
+  b.n_cached = nc.data();
+  b.q_row0 = q0.data();
+  b.kv_row0 = k0.data();
+  b.out = outs.data();
+  const int max_ctas = 4096;
+  unsigned long long* tr;
+  cudaMalloc(&tr, (size_t)max_ctas * 256 * 8);
+  cudaMemcpyToSymbol(askv::g_attn_trace, &tr, sizeof(tr));
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  std::vector<unsigned long long> h((size_t)max_ctas * 256);
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaMemset(tr, 0, (size_t)max_ctas * 256 * 8);
+    int rc = askv::prefill_attn_varlen(b, nullptr, nullptr);
+    if (rc) { printf("rc %d %s\n", rc, g_err); return 1; }
+    cudaDeviceSynchronize();
+    double* dm;
+    cudaMalloc(&dm, 8);
+    clock_probe<<<1, 1>>>(dm);
+    double mhz = 0;
+    cudaMemcpy(&mhz, dm, 8, cudaMemcpyDeviceToHost);
+    cudaFree(dm);
+    printf("SM clock right after: %.0f MHz\n", mhz);
+    cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull, tend = 0;
+    int ctas = 0;
+    for (int c = 0; c < max_ctas; ++c) {
+      if (!h[c * 256]) continue;
+      ctas = c + 1;
+      t0 = std::min(t0, h[c * 256]);
+      tend = std::max(tend, h[c * 256 + 4]);
+    }
+    const double span = (tend - t0) * 1e-3;
+    double busy = 0, sx = 0, sy = 0, sxx = 0, sxy = 0;
+    std::map<int, std::vector<std::pair<unsigned long long, unsigned long long>>> per_sm;
+    unsigned long long first_idle = tend;
+    for (int c = 0; c < ctas; ++c) {
+      const unsigned long long* r = &h[c * 256];
+      if (!r[0]) continue;
+      const double life = (r[4] - r[0]) * 1e-3;
+      busy += life;
+      int tiles = 0;   // WG0 S-ready stamps (<= 28 recorded) x2 groups ~ KV tiles
+      for (int t = 0; t < 28; ++t) if (r[8 + 2 * t]) ++tiles;
+      sx += tiles; sy += life; sxx += (double)tiles * tiles; sxy += tiles * life;
+      per_sm[(int)r[5]].push_back({r[0], r[4]});
+    }
+    // WG0 softmax: S-ready -> P-done (the tile's softmax) and P-done -> next
+    // S-ready (waiting for the tensor core), tiles 2..25 of CTAs with >= 26
+    double sm_t = 0, wait_t = 0;
+    int nsm = 0;
+    for (int c = 0; c < ctas; ++c) {
+      const unsigned long long* r = &h[c * 256];
+      if (!r[0] || !r[8 + 2 * 26]) continue;
+      for (int t = 2; t < 26; ++t) {
+        sm_t += (r[9 + 2 * t] - r[8 + 2 * t]) * 1e-3;
+        wait_t += (r[8 + 2 * (t + 1)] - r[9 + 2 * t]) * 1e-3;
+        ++nsm;
+      }
+    }
+    double ph[4] = {0, 0, 0, 0};
+    int nph = 0;
+    for (int c = 0; c < ctas; ++c) {
+      const unsigned long long* r = &h[c * 256];
+      if (!r[0] || !r[8 + 2 * 18]) continue;
+      for (int t = 2; t < 18; ++t) {
+        const unsigned long long* q = &r[192 + 4 * (t - 2)];
+        if (!q[0] || !q[1] || !q[2]) continue;
+        ph[0] += (q[0] - r[8 + 2 * t]) * 1e-3;
+        ph[1] += (q[1] - q[0]) * 1e-3;
+        ph[2] += (q[2] - q[1]) * 1e-3;
+        ph[3] += (r[9 + 2 * t] - q[2]) * 1e-3;
+        ++nph;
+      }
+    }
+    {  // one steady paired CTA: MMA warp's view (P_a(j) ready, P_b(j) ready, b issued)
+      for (int c = 0; c < ctas; ++c) {
+        const unsigned long long* r = &h[c * 256];
+        if (!r[0] || !r[8 + 2 * 20] || !r[96 + 12]) continue;
+        const unsigned long long b0 = r[8 + 2 * 4];
+        printf("  cta %d (us from WG0 S(4) ready): ", c);
+        for (int t = 4; t < 12; ++t)
+          printf(" [j%d: Sa %.2f Pa %.2f | MMA sees Pa %.2f Pb %.2f b-issued %.2f]", t,
+                 (r[8 + 2 * t] - b0) * 1e-3, (r[9 + 2 * t] - b0) * 1e-3, (r[64 + t] - b0) * 1e-3,
+                 (r[96 + t] - b0) * 1e-3, (r[160 + t] - b0) * 1e-3);
+        printf("\n");
+        break;
+      }
+    }
+    if (nph) printf("  softmax phases (us): S-ready->ld done %.3f | max (+mask) %.3f | exp/pack/st issue %.3f | "
+                    "st wait + arrive %.3f (%d tiles)\n", ph[0] / nph, ph[1] / nph, ph[2] / nph, ph[3] / nph, nph);
+    if (nsm) printf("  steady WG0 tile: softmax %.3f us, then waits %.3f us for the next S (%d tiles)\n",
+                    sm_t / nsm, wait_t / nsm, nsm);
+    double cyc = 0, ns = 0;
+    for (int c = 0; c < ctas; ++c) {
+      const unsigned long long* r = &h[c * 256];
+      if (!r[0] || !r[4] || !r[7]) continue;
+      cyc += (double)(r[7] - r[6]);
+      ns += (double)(r[4] - r[0]);
+    }
+    printf("  SM clock inside the launch (CTA lifetimes): %.0f MHz\n", cyc / ns * 1e3);
+    double gap = 0;
+    int ngap = 0;
+    for (auto& kvp : per_sm) {
+      auto& v = kvp.second;
+      std::sort(v.begin(), v.end());
+      for (size_t i = 1; i < v.size(); ++i) { gap += (v[i].first - v[i - 1].second) * 1e-3; ++ngap; }
+      first_idle = std::min(first_idle, v.back().second);
+    }
+    const double m = ctas;
+    const double slope = (m * sxy - sx * sy) / (m * sxx - sx * sx);
+    const double icpt = (sy - slope * sx) / m;
+    printf("rep %d: ctas %d span %.2f us  %.1f TF/s algorithmic | fill %.3f | gap between CTAs on an SM "
+           "%.2f us | life = %.2f us + %.3f us x (WG0 tiles, <=28) | tail after first idle SM %.2f us\n",
+           rep, ctas, span, flops / (span * 1e-6) / 1e12, busy / (span * sms), ngap ? gap / ngap : 0.0,
+           icpt, slope, (tend - first_idle) * 1e-3);
+  }
+  return 0;
+}
