@@ -98,5 +98,13 @@ int reembed_stamped(const void* src_base, const int64_t* src_block_off, int bloc
                     int head_dim, const float* rope_table, int table_positions,
                     const int32_t* positions, int pos0, void* dst, int64_t dst_row_stride,
                     void* stream, unsigned long long* stamp, int v_from = 0);
+// K2 for a batch of HBM-arena sessions in one launch (shared source arena
+// layer base, strides and RoPE table; per job its block table, first stored
+// token, kept rows, first position, V-copy start and destination rows).
+int reembed_batch(const void* src_base, int block_tokens, int64_t src_row_stride, int n_jobs,
+                  const int64_t* const* blk_off, const int64_t* first_token, const int* kept,
+                  const int* pos0, const int* v_from, void* const* dst, int64_t dst_row_stride,
+                  int n_kv_heads, int head_dim, const float* rope_table, int table_positions,
+                  void* stream, unsigned long long* stamp);
 
 }  // namespace askv

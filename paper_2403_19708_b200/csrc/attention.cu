@@ -212,6 +212,15 @@ __host__ __device__ __forceinline__ Piece sk_piece(const AttnParams& p, int c, i
 // Warps: 0-3 WG0, 4-7 WG1, 8 TMA Q + K (+ TMEM alloc), 9 MMA, 10 TMA V.
 // ============================================================================
 
+// K/V tiles prefetched into L2 beyond the shared-memory rings (tiles ahead of
+// the ring's furthest load; 0 = off).  Build-time knob; off: 2 / 4 / 8 tiles
+// ahead measured 1-4 % slower (profiles/r02_attn_varlen.md) -- the K/V
+// stream is bound by the L2 -> SM path, not by HBM latency.
+#ifndef ASKV_ATTN_L2_PREFETCH
+#define ASKV_ATTN_L2_PREFETCH 0
+#endif
+constexpr int kL2Prefetch = ASKV_ATTN_L2_PREFETCH;
+
 template <int HD, bool kAllowPair>
 struct Cfg {
   // K is consumed early (S) and V late (PV), so K gets the deeper ring when
@@ -404,6 +413,20 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
       // ordered producer the MMA warp waited ~0.55 us per tile for K(j+2)).
       for (int jk = 0; jk < n_tiles; ++jk) {
         const int st = jk % C::kKStages;
+        if constexpr (kL2Prefetch > 0) {
+          // pull K tiles further ahead into L2 than the shared-memory ring
+          // reaches: the ring's own loads then hit L2 instead of HBM
+          const int jp = jk + C::kKStages + kL2Prefetch - 1;
+          if (jk == 0)
+            for (int q = C::kKStages; q < jp && q < n_tiles; ++q)
+#pragma unroll
+              for (int c = 0; c < C::kChunks; ++c)
+                tma_prefetch_l2_3d(&tm_k, c * 64, kh, kv_row0 + (t_begin + q) * kBN);
+          if (jp < n_tiles)
+#pragma unroll
+            for (int c = 0; c < C::kChunks; ++c)
+              tma_prefetch_l2_3d(&tm_k, c * 64, kh, kv_row0 + (t_begin + jp) * kBN);
+        }
         if (jk >= C::kKStages) mbar_wait(&k_empty[st], ((jk / C::kKStages) - 1) & 1);
         mbar_expect_tx(&k_full[st], C::kTileBytes);
 #pragma unroll
@@ -417,15 +440,28 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
     shrink();
     if (lane == 0) {
       const uint64_t pol_kv = l2_policy_evict_last();
+      auto v_row = [&](int tv, bool vs) {
+        return !vs ? kv_row0 + tv * kBN
+               : v_blk_off ? (int)(v_blk_off[tv] / p.v_row_elems + v_layer_row)
+                           : (int)(p.v_src_row0 + (int64_t)tv * kBN);
+      };
       for (int jv = 0; jv < n_tiles; ++jv) {
         const int st = jv % C::kVStages;
+        if constexpr (kL2Prefetch > 0) {
+          const int jp = jv + C::kVStages + kL2Prefetch - 1;
+          for (int q = jv == 0 ? C::kVStages : jp; q <= jp && q < n_tiles; ++q) {
+            const int tq = t_begin + q;
+            const bool vsq = tq < v_src_tiles;
+#pragma unroll
+            for (int c = 0; c < C::kChunks; ++c)
+              tma_prefetch_l2_3d(vsq ? &tm_vs : &tm_v, c * 64, kh, v_row(tq, vsq));
+          }
+        }
         if (jv >= C::kVStages) mbar_wait(&v_empty[st], ((jv / C::kVStages) - 1) & 1);
         mbar_expect_tx(&v_full[st], C::kTileBytes);
         const int tv = t_begin + jv;
         const bool vs = tv < v_src_tiles;
-        const int vrow = !vs ? kv_row0 + tv * kBN
-                         : v_blk_off ? (int)(v_blk_off[tv] / p.v_row_elems + v_layer_row)
-                                     : (int)(p.v_src_row0 + (int64_t)tv * kBN);
+        const int vrow = v_row(tv, vs);
 #pragma unroll
         for (int c = 0; c < C::kChunks; ++c)
           tma_load_3d_hint(sV + st * C::kTileBytes + c * (kBN * 128), vs ? &tm_vs : &tm_v,

@@ -98,13 +98,30 @@ __global__ void rope_table_kernel(float* __restrict__ table, int max_pos, int ha
 // and copying V vectors.  Source rows come through the session block table.
 constexpr int kReRows = 2;
 
+// K2 over a batch of sessions in one launch (askv::reembed_batch): job i owns
+// CTAs [cta0, next cta0) and its own block table / rows / destination; the
+// source arena, row strides and RoPE table are shared.  n == 0: one job (the
+// scalar arguments).
+constexpr int kMaxReJobs = 24;
+struct ReJobs {
+  int n;
+  int cta0[kMaxReJobs];
+  int kept[kMaxReJobs];
+  int v_from[kMaxReJobs];
+  int pos0[kMaxReJobs];
+  int64_t first_token[kMaxReJobs];
+  const int64_t* blk_off[kMaxReJobs];
+  __nv_bfloat16* dst[kMaxReJobs];
+};
+
 template <int HD>
 __global__ void __launch_bounds__(kThreads)
     reembed_kernel(const __nv_bfloat16* __restrict__ src, const int64_t* __restrict__ blk_off,
                    int block_tokens, int64_t src_row_stride, int64_t first_token, int kept,
                    int hkv, const float* __restrict__ table, const int32_t* __restrict__ positions,
                    int pos0, __nv_bfloat16* __restrict__ dst, int64_t dst_row_stride,
-                   unsigned long long* __restrict__ stamp, int v_from) {
+                   unsigned long long* __restrict__ stamp, int v_from,
+                   const __grid_constant__ ReJobs rj) {
   constexpr int kHalf = HD / 2;
   constexpr int kUnitsPerHead = HD / 8;
   // optional launch timestamps {begin of CTA 0, max CTA end} (attention.cu)
@@ -115,7 +132,18 @@ __global__ void __launch_bounds__(kThreads)
   }
   __shared__ __align__(16) float cs_s[kReRows * kHalf * 2];
   __shared__ const __nv_bfloat16* srow_s[kReRows];
-  const int row0 = blockIdx.x * kReRows;
+  int row0 = blockIdx.x * kReRows;
+  if (rj.n > 0) {  // batched: this CTA's job (positions are pos0 + row)
+    int jb = 0;
+    while (jb + 1 < rj.n && rj.cta0[jb + 1] <= (int)blockIdx.x) ++jb;
+    row0 = (blockIdx.x - rj.cta0[jb]) * kReRows;
+    blk_off = rj.blk_off[jb];
+    first_token = rj.first_token[jb];
+    kept = rj.kept[jb];
+    pos0 = rj.pos0[jb];
+    dst = rj.dst[jb];
+    v_from = rj.v_from[jb];
+  }
   const int nrows = min(kReRows, kept - row0);
   for (int i = threadIdx.x; i < nrows * kHalf; i += kThreads) {
     const int rr = i / kHalf, pi = i - rr * kHalf;
@@ -334,15 +362,70 @@ int askv::reembed_stamped(const void* src_base, const int64_t* src_block_off, in
   const int grid = (kept + kReRows - 1) / kReRows;
   auto* s = static_cast<const __nv_bfloat16*>(src_base);
   auto* d = static_cast<__nv_bfloat16*>(dst);
+  ReJobs none;
+  none.n = 0;
   if (head_dim == 128)
     reembed_kernel<128><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
         s, src_block_off, block_tokens, src_row_stride, first_token, kept, n_kv_heads,
-        rope_table, positions, pos0, d, dst_row_stride, stamp, v_from);
+        rope_table, positions, pos0, d, dst_row_stride, stamp, v_from, none);
   else
     reembed_kernel<64><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
         s, src_block_off, block_tokens, src_row_stride, first_token, kept, n_kv_heads,
-        rope_table, positions, pos0, d, dst_row_stride, stamp, v_from);
+        rope_table, positions, pos0, d, dst_row_stride, stamp, v_from, none);
   return launch_status("reembed launch");
+}
+
+int askv::reembed_batch(const void* src_base, int block_tokens, int64_t src_row_stride,
+                        int n_jobs, const int64_t* const* blk_off, const int64_t* first_token,
+                        const int* kept, const int* pos0, const int* v_from, void* const* dst,
+                        int64_t dst_row_stride, int n_kv_heads, int head_dim,
+                        const float* rope_table, int table_positions, void* stream,
+                        unsigned long long* stamp) {
+  ASKV_REQUIRE(n_jobs > 0 && n_kv_heads > 0 && block_tokens > 0,
+               "reembed_batch: bad n_jobs=%d hkv=%d block_tokens=%d", n_jobs, n_kv_heads,
+               block_tokens);
+  ASKV_REQUIRE(head_dim == 64 || head_dim == 128, "reembed_batch: head_dim %d unsupported",
+               head_dim);
+  ASKV_REQUIRE(src_row_stride % 8 == 0 && dst_row_stride % 8 == 0,
+               "reembed_batch: row strides must be multiples of 8 elements");
+  ASKV_REQUIRE(src_base && rope_table, "reembed_batch: null pointer");
+  auto* s = static_cast<const __nv_bfloat16*>(src_base);
+  for (int i0 = 0; i0 < n_jobs; i0 += kMaxReJobs) {
+    ReJobs rj;
+    rj.n = 0;
+    int ctas = 0;
+    for (int i = i0; i < n_jobs && i < i0 + kMaxReJobs; ++i) {
+      if (kept[i] == 0) continue;
+      ASKV_REQUIRE(kept[i] > 0 && first_token[i] >= 0 && pos0[i] >= 0 &&
+                       pos0[i] + kept[i] <= table_positions && v_from[i] >= 0 &&
+                       v_from[i] % 2 == 0 && blk_off[i] && dst[i],
+                   "reembed_batch: job %d (kept %d, pos0 %d, v_from %d)", i, kept[i], pos0[i],
+                   v_from[i]);
+      const int k = rj.n++;
+      rj.cta0[k] = ctas;
+      rj.kept[k] = kept[i];
+      rj.v_from[k] = v_from[i];
+      rj.pos0[k] = pos0[i];
+      rj.first_token[k] = first_token[i];
+      rj.blk_off[k] = blk_off[i];
+      rj.dst[k] = static_cast<__nv_bfloat16*>(dst[i]);
+      ctas += (kept[i] + kReRows - 1) / kReRows;
+    }
+    if (rj.n == 0) continue;
+    // only the first launch of a batch carries the stamps
+    unsigned long long* st = i0 == 0 ? stamp : nullptr;
+    if (head_dim == 128)
+      reembed_kernel<128><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(
+          s, nullptr, block_tokens, src_row_stride, 0, 0, n_kv_heads, rope_table, nullptr, 0,
+          nullptr, dst_row_stride, st, 0, rj);
+    else
+      reembed_kernel<64><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(
+          s, nullptr, block_tokens, src_row_stride, 0, 0, n_kv_heads, rope_table, nullptr, 0,
+          nullptr, dst_row_stride, st, 0, rj);
+    const int rc = launch_status("reembed_batch launch");
+    if (rc) return rc;
+  }
+  return ASKV_OK;
 }
 
 extern "C" int askv_rope_new(const void* qkv, int64_t qkv_row_stride, int n_new, int n_heads,

@@ -669,6 +669,21 @@ class Runner:
             first = att[0][1] if att else None
             kept_att = [e[:6] + (per_layer[e[4]], 0) for e in att if e[1] == first]
             self.probe[probe0:] = [e for e in mine if e[0] != "attention"] + kept_att
+        # one K2 launch per layer when every re-embedded job reads the HBM arena
+        # (csrc/runtime.cu k2_batch): it stamps the first such job's slots
+        k2_batch = (os.environ.get("ASKV_K2_BATCH", "1") != "0" and len(jobs) > 1
+                    and any(j.kept for j in jobs)
+                    and all(j.source == "hbm" for j in jobs if j.kept))
+        if k2_batch and self.probe is not None:
+            mine = self.probe[probe0:]
+            re = [e for e in mine if e[0] == "reembed"]
+            work, moved = {}, {}
+            for e in re:
+                work[e[4]] = work.get(e[4], 0) + e[6]
+                moved[e[4]] = moved.get(e[4], 0) + e[7]
+            first = re[0][1] if re else None
+            kept_re = [e[:6] + (work[e[4]], moved[e[4]]) for e in re if e[1] == first]
+            self.probe[probe0:] = [e for e in mine if e[0] != "reembed"] + kept_re
         arr = (_lib.PrefillPlan * len(plans))(*plans)
         _lib.check(_lib.lib().askv_prefill_layers_batch(C.addressof(arr), len(plans),
                                                         self.s_compute.cuda_stream),
