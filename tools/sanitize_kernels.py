@@ -147,7 +147,8 @@ def engine_turns(graph: bool):
 
 def batch_cases():
     """A batched layer pass of the tiny model with HBM-resident sessions: the
-    varlen K3 launch (one launch for every job's (query tile, head) grid)."""
+    varlen K3 launch (one launch for every job's (query tile, head) grid; with
+    ASKV_ATTN_PAIR=1 jobs a and d pair their query tiles) and the batched K2."""
     import numpy as np
     from paper_2403_19708_b200 import model, runner
     from paper_2403_19708_b200.runner import Job, Runner
@@ -156,11 +157,11 @@ def batch_cases():
     bb = bt * shape.kv_bytes_per_token
     hbm = torch.randn(nb * bb // 2, device="cuda").to(torch.bfloat16)
     r = runner.Runner(shape, seed=1, block_tokens=bt, hbm_arena=hbm, read_buffer_bytes=8 << 20,
-                      write_buffer_bytes=16 << 20, max_new=64, max_ctx=512, autotune=False)
+                      write_buffer_bytes=16 << 20, max_new=256, max_ctx=512, autotune=False)
     rng = np.random.default_rng(1)
     jobs = []
-    for sid, kept, n, bids in [("a", 200, 17, [0, 1]), ("b", 0, 23, [2]), ("c", 256, 9, [3, 4, 5]),
-                               ("d", 300, 31, [6, 7, 8])]:
+    for sid, kept, n, bids in [("a", 200, 150, [0, 1, 2]), ("b", 0, 23, [3]),
+                               ("c", 256, 9, [4, 5, 6]), ("d", 300, 200, [7, 8, 9, 10])]:
         off = torch.as_tensor([b * bb // 2 for b in bids], dtype=torch.int64, device="cuda")
         jobs.append(Job(sid, torch.as_tensor(rng.integers(0, shape.vocab, n)).cuda(), kept=kept,
                         source="hbm" if kept else "none", block_ids=bids, save=bool(kept),
