@@ -92,11 +92,22 @@ __global__ void rope_table_kernel(float* __restrict__ table, int max_pos, int ha
   }
 }
 
-// K2: one CTA per kReRows consecutive rows.  The rows' cos/sin (kReRows x
+// K2: one CTA per `rows` consecutive rows (re_rows: 2 for wide K rows, up to
+// kMaxReRows for GQA's narrow ones, ~1,000+ vectors per CTA).  The rows' cos/sin (rows x
 // HD/2 float2) are staged in shared memory once, then every thread streams
 // 16-byte vectors of the rows (4 in flight per thread), rotating K vectors
 // and copying V vectors.  Source rows come through the session block table.
-constexpr int kReRows = 2;
+constexpr int kMaxReRows = 32;
+// rows per CTA: two when a row's K is >= 512 16-byte vectors (13B: 640; four
+// rows measured slower there), else enough rows for ~1,000 vectors (70B's
+// 8 kv heads: 128 per row -> 8 rows), a power of two dividing the 128-row tile
+inline int re_rows(int hkv, int head_dim) {
+  const int units = hkv * head_dim / 8;
+  if (units >= 512) return 2;
+  int r = 2;
+  while (r < kMaxReRows && (r * 2) * units <= 1280) r *= 2;
+  return r;
+}
 
 // K2 over a batch of sessions in one launch (askv::reembed_batch): job i owns
 // CTAs [cta0, next cta0) and its own block table / rows / destination; the
@@ -120,7 +131,7 @@ __global__ void __launch_bounds__(kThreads)
                    int block_tokens, int64_t src_row_stride, int64_t first_token, int kept,
                    int hkv, const float* __restrict__ table, const int32_t* __restrict__ positions,
                    int pos0, __nv_bfloat16* __restrict__ dst, int64_t dst_row_stride,
-                   unsigned long long* __restrict__ stamp, int v_from,
+                   unsigned long long* __restrict__ stamp, int v_from, int rows,
                    const __grid_constant__ ReJobs rj) {
   constexpr int kHalf = HD / 2;
   constexpr int kUnitsPerHead = HD / 8;
@@ -130,13 +141,13 @@ __global__ void __launch_bounds__(kThreads)
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     stamp[0] = t;
   }
-  __shared__ __align__(16) float cs_s[kReRows * kHalf * 2];
-  __shared__ const __nv_bfloat16* srow_s[kReRows];
-  int row0 = blockIdx.x * kReRows;
+  __shared__ __align__(16) float cs_s[kMaxReRows * kHalf * 2];
+  __shared__ const __nv_bfloat16* srow_s[kMaxReRows];
+  int row0 = blockIdx.x * rows;
   if (rj.n > 0) {  // batched: this CTA's job (positions are pos0 + row)
     int jb = 0;
     while (jb + 1 < rj.n && rj.cta0[jb + 1] <= (int)blockIdx.x) ++jb;
-    row0 = (blockIdx.x - rj.cta0[jb]) * kReRows;
+    row0 = (blockIdx.x - rj.cta0[jb]) * rows;
     blk_off = rj.blk_off[jb];
     first_token = rj.first_token[jb];
     kept = rj.kept[jb];
@@ -144,7 +155,7 @@ __global__ void __launch_bounds__(kThreads)
     dst = rj.dst[jb];
     v_from = rj.v_from[jb];
   }
-  const int nrows = min(kReRows, kept - row0);
+  const int nrows = min(rows, kept - row0);
   for (int i = threadIdx.x; i < nrows * kHalf; i += kThreads) {
     const int rr = i / kHalf, pi = i - rr * kHalf;
     const int pos = positions ? positions[row0 + rr] : pos0 + row0 + rr;
@@ -163,14 +174,14 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   const int k_units = hkv * kUnitsPerHead;
   // rows below v_from: K only (their V is read by K3 straight from the
-  // source); v_from is a multiple of the 128-row KV tile, so a CTA's two rows
-  // are on the same side of it
+  // source); v_from is a multiple of the 128-row KV tile and `rows` a power of
+  // two dividing it, so a CTA's rows are all on the same side of it
   const int row_units = row0 >= v_from ? 2 * k_units : k_units;
   const int total = nrows * row_units;
-  // 13B: 2 rows x 1280 vectors = two rounds of 5 per thread; the row of a
-  // vector is a compare (kReRows == 2), not an integer division (K2 was
+  // 13B: 2 rows x 640 K vectors = one round of 5 per thread; with two rows
+  // the row of a vector is a compare, not an integer division (K2 was
   // issue-bound: ncu 45-50 % issue slots, profiles/r01d_summary.md)
-  static_assert(kReRows == 2, "row index below assumes two rows per CTA");
+  auto row_of = [&](int g) { return rows == 2 ? (g >= row_units ? 1 : 0) : g / row_units; };
   constexpr int kIlp = 5;
   const uint64_t pol_src = policy_evict_first();
   for (int base = threadIdx.x; base < total; base += kThreads * kIlp) {
@@ -179,7 +190,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int k = 0; k < kIlp; ++k) {
       const int g = base + k * kThreads;
       if (g < total) {
-        const int rr = g >= row_units ? 1 : 0;
+        const int rr = row_of(g);
         v[k] = ld_nc16_ef(srow_s[rr] + (g - rr * row_units) * 8, pol_src);
       }
     }
@@ -187,7 +198,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int k = 0; k < kIlp; ++k) {
       const int g = base + k * kThreads;
       if (g < total) {
-        const int rr = g >= row_units ? 1 : 0;
+        const int rr = row_of(g);
         const int u = g - rr * row_units;
         int4 x = v[k];
         if (u < k_units) x = rotate8(x, cs_s + (rr * kHalf + (u % kUnitsPerHead) * 4) * 2);
@@ -356,10 +367,12 @@ int askv::reembed_stamped(const void* src_base, const int64_t* src_block_off, in
                table_positions);
   ASKV_REQUIRE(src_row_stride % 8 == 0 && dst_row_stride % 8 == 0,
                "reembed: row strides must be multiples of 8 elements");
-  ASKV_REQUIRE(v_from >= 0 && v_from % 2 == 0, "reembed: v_from %d must be even", v_from);
+  const int rows = re_rows(n_kv_heads, head_dim);
+  ASKV_REQUIRE(v_from >= 0 && v_from % rows == 0,
+               "reembed: v_from %d must be a multiple of %d rows", v_from, rows);
   if (kept == 0) return ASKV_OK;
   ASKV_REQUIRE(src_base && dst && rope_table, "reembed: null pointer");
-  const int grid = (kept + kReRows - 1) / kReRows;
+  const int grid = (kept + rows - 1) / rows;
   auto* s = static_cast<const __nv_bfloat16*>(src_base);
   auto* d = static_cast<__nv_bfloat16*>(dst);
   ReJobs none;
@@ -367,11 +380,11 @@ int askv::reembed_stamped(const void* src_base, const int64_t* src_block_off, in
   if (head_dim == 128)
     reembed_kernel<128><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
         s, src_block_off, block_tokens, src_row_stride, first_token, kept, n_kv_heads,
-        rope_table, positions, pos0, d, dst_row_stride, stamp, v_from, none);
+        rope_table, positions, pos0, d, dst_row_stride, stamp, v_from, rows, none);
   else
     reembed_kernel<64><<<grid, kThreads, 0, (cudaStream_t)stream>>>(
         s, src_block_off, block_tokens, src_row_stride, first_token, kept, n_kv_heads,
-        rope_table, positions, pos0, d, dst_row_stride, stamp, v_from, none);
+        rope_table, positions, pos0, d, dst_row_stride, stamp, v_from, rows, none);
   return launch_status("reembed launch");
 }
 
@@ -390,6 +403,7 @@ int askv::reembed_batch(const void* src_base, int block_tokens, int64_t src_row_
                "reembed_batch: row strides must be multiples of 8 elements");
   ASKV_REQUIRE(src_base && rope_table, "reembed_batch: null pointer");
   auto* s = static_cast<const __nv_bfloat16*>(src_base);
+  const int rows = re_rows(n_kv_heads, head_dim);
   for (int i0 = 0; i0 < n_jobs; i0 += kMaxReJobs) {
     ReJobs rj;
     rj.n = 0;
@@ -398,7 +412,7 @@ int askv::reembed_batch(const void* src_base, int block_tokens, int64_t src_row_
       if (kept[i] == 0) continue;
       ASKV_REQUIRE(kept[i] > 0 && first_token[i] >= 0 && pos0[i] >= 0 &&
                        pos0[i] + kept[i] <= table_positions && v_from[i] >= 0 &&
-                       v_from[i] % 2 == 0 && blk_off[i] && dst[i],
+                       v_from[i] % rows == 0 && blk_off[i] && dst[i],
                    "reembed_batch: job %d (kept %d, pos0 %d, v_from %d)", i, kept[i], pos0[i],
                    v_from[i]);
       const int k = rj.n++;
@@ -409,7 +423,7 @@ int askv::reembed_batch(const void* src_base, int block_tokens, int64_t src_row_
       rj.first_token[k] = first_token[i];
       rj.blk_off[k] = blk_off[i];
       rj.dst[k] = static_cast<__nv_bfloat16*>(dst[i]);
-      ctas += (kept[i] + kReRows - 1) / kReRows;
+      ctas += (kept[i] + rows - 1) / rows;
     }
     if (rj.n == 0) continue;
     // only the first launch of a batch carries the stamps
@@ -417,11 +431,11 @@ int askv::reembed_batch(const void* src_base, int block_tokens, int64_t src_row_
     if (head_dim == 128)
       reembed_kernel<128><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(
           s, nullptr, block_tokens, src_row_stride, 0, 0, n_kv_heads, rope_table, nullptr, 0,
-          nullptr, dst_row_stride, st, 0, rj);
+          nullptr, dst_row_stride, st, 0, rows, rj);
     else
       reembed_kernel<64><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(
           s, nullptr, block_tokens, src_row_stride, 0, 0, n_kv_heads, rope_table, nullptr, 0,
-          nullptr, dst_row_stride, st, 0, rj);
+          nullptr, dst_row_stride, st, 0, rows, rj);
     const int rc = launch_status("reembed_batch launch");
     if (rc) return rc;
   }

@@ -120,6 +120,30 @@ int main() {
   if (run("2 streams, 2.6 MB chunk per memcpy + D2H", 2, 0, true)) return 1;
   if (run("1 stream, 23-block 2-D runs + D2H", 1, 1, true)) return 1;
   if (run("1 stream, 64 MB memcpy + D2H", 1, 2, true)) return 1;
+  // the saver's shape: D2H of 2 / 6 MB pieces (one layer's new rows of a
+  // 100 / 301-token turn) on one stream while a large H2D streams
+  for (size_t piece : {(size_t)2 << 20, (size_t)6 << 20}) {
+    for (int with_h2d = 0; with_h2d < 2; ++with_h2d) {
+      float best = 0.f;
+      for (int rep = 0; rep < 3; ++rep) {
+        CK(cudaDeviceSynchronize());
+        if (with_h2d) CK(cudaMemcpyAsync(d2, h2, bytes, cudaMemcpyHostToDevice, st[1]));
+        CK(cudaEventRecord(a, sd));
+        size_t moved = 0;
+        for (size_t off = 0; off + piece <= bytes / 4; off += piece, moved += piece)
+          CK(cudaMemcpyAsync(h + off * 3, d + off, piece, cudaMemcpyDeviceToHost, sd));
+        CK(cudaEventRecord(b, sd));
+        CK(cudaEventSynchronize(b));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        const float g = moved / (ms * 1e-3f) / 1e9f;
+        if (g > best) best = g;
+      }
+      CK(cudaDeviceSynchronize());
+      printf("D2H %zu MB pieces, one stream%-22s D2H %6.1f GB/s\n", piece >> 20,
+             with_h2d ? ", 2 GB H2D running" : "", best);
+    }
+  }
   {
     CK(cudaDeviceSynchronize());
     CK(cudaEventRecord(a, sd));
