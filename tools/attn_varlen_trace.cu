@@ -45,13 +45,15 @@ __global__ void clock_probe(double* mhz) {
   *mhz = (double)(c1 - c0) / (double)(g1 - g0) * 1e3;
 }
 
-int main() {
+int main(int argc, char** argv) {
   // bench.py select_turns("c3", 0, 1, 16): (kept, new)
   const int J[16][2] = {{3018, 414}, {422, 94},   {2741, 217}, {1000, 173},
                         {3047, 163}, {2883, 287}, {3377, 443}, {1963, 196},
                         {3117, 351}, {276, 90},   {3653, 374}, {1815, 369},
                         {2855, 422}, {3675, 412}, {3379, 315}, {228, 97}};
-  const int n = 16, hq = 40, hkv = 40, d = 128;
+  // argv[1]: use the first n turns (2: ~80 MB of K/V, L2-resident after the
+  // first repetition -- separates DRAM from the L2 -> SM path)
+  const int n = argc > 1 ? atoi(argv[1]) : 16, hq = 40, hkv = 40, d = 128;
   std::vector<int> nn(n), nc(n), q0(n), k0(n);
   int qt = 0, kt = 0;
   double flops = 0;

@@ -24,11 +24,13 @@ __global__ void probe(long long* out, int iters, int writers) {
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar;
+  __shared__ uint64_t cbar[6];
   __shared__ uint32_t slot;
   __shared__ volatile int done;
   const int warp = threadIdx.x / 32;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
+    for (int i = 0; i < 6; ++i) mbar_init(&cbar[i], 1);
     fence_mbar_init();
     done = 0;
   }
@@ -48,6 +50,41 @@ __global__ void probe(long long* out, int iters, int writers) {
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
       const uint32_t tile = sb + (it % 3) * 32768 + (MODE == 1 ? (it & 1) * 8192 : 0);
+#pragma unroll
+      if (MODE >= 5) {
+        // the K3 group sequence: PV (A = P in TMEM cols [0, 64), D = O at 256)
+        // then S (SS, D = cols [0, 128) -- aliasing P, as in the kernel -- or
+        // cols [128, 256) with MODE 6: no alias); MODE 7: PV_a, S_a, PV_b, S_b
+        // with two groups (a: S 0 / O 256, b: S 128 / O 384), MODE 8 = 7
+        // reordered PV_a, PV_b, S_a, S_b
+        const uint32_t vt = sb + (it % 3) * 32768;
+        auto pv = [&](uint32_t s_col, uint32_t o_col) {
+          const uint32_t idp = idesc_bf16_f32(128, 128, 0, 1);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            umma_bf16_tmem_a(tmem + o_col, tmem + s_col + k * 8,
+                             sdesc_sw128(vt + k * 2048, 16384, 1024), idp, true);
+        };
+        auto ss = [&](uint32_t s_col) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
+            umma_bf16(tmem + s_col, sdesc_sw128(sa + off, 16, 1024),
+                      sdesc_sw128(vt + off, 16, 1024), idesc, k > 0);
+          }
+        };
+        if (MODE == 9) {  // = 7 with the kernel's commits (o_full, s_full, v_empty, k_empty)
+          pv(0, 256); umma_commit(&cbar[0]); ss(0); umma_commit(&cbar[1]);
+          pv(128, 384); umma_commit(&cbar[2]); ss(128); umma_commit(&cbar[3]);
+          umma_commit(&cbar[4]); umma_commit(&cbar[5]);
+          continue;
+        }
+        if (MODE == 5) { pv(0, 256); ss(0); }
+        else if (MODE == 6) { pv(0, 256); ss(128); }
+        else if (MODE == 7) { pv(0, 256); ss(0); pv(128, 384); ss(128); }
+        else { pv(0, 256); pv(128, 384); ss(0); ss(128); }
+        continue;
+      }
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
@@ -104,7 +141,9 @@ int main() {
   cudaMalloc(&d, 148 * sizeof(long long));
   const int smem = 170 * 1024;
   const char* names[] = {"SS N=128 (S, kernel 1)", "SS N=64 (S, kernel 2)", "TS N=128 (PV)",
-                         "SS N=256", "TS N=128 A=Q in TMEM (S)"};
+                         "SS N=256", "TS N=128 A=Q in TMEM (S)", "PV then S over P (alias)",
+                         "PV then S, no alias", "PVa Sa PVb Sb (K3 paired)",
+                         "PVa PVb Sa Sb (reordered)", "K3 paired + 6 commits"};
   auto run = [&](auto kern, int mode) {
     if (mode > 9) mode -= 10;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -122,12 +161,21 @@ int main() {
         double mx = 0;
         for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
         const int n = mode == 1 ? 64 : mode == 3 ? 256 : 128;
+        const double per_it = mode == 5 || mode == 6 ? 16.0 : mode >= 7 ? 32.0 : 8.0;  // 9: 32
         printf("%-26s grid=%3d smem-writers=%d: %6.1f cycles/MMA (%5.0f MAC/clk/SM)\n",
-               names[mode], grid, writers, mx / (iters * 8.0),
-               128.0 * n * 16 * iters * 8 / mx);
+               names[mode], grid, writers, mx / (iters * per_it),
+               128.0 * n * 16 * iters * per_it / mx);
       }
     }
   };
+  if (getenv("MIX_ONLY")) {
+    run(probe<5>, 5);
+    run(probe<6>, 6);
+    run(probe<7>, 7);
+    run(probe<8>, 8);
+    run(probe<9>, 9);
+    return 0;
+  }
   if (!getenv("TMEM_ONLY")) {
     run(probe<0>, 0);
     run(probe<1>, 1);
