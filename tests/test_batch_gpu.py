@@ -48,8 +48,12 @@ LONG = {"varlen_long": [("a", 40, 300, "hbm", list(range(0, 22))),
                         ("b", 0, 150, "none", list(range(55, 65))),
                         ("c", 130, 257, "hbm", list(range(23, 48))),
                         ("d", 64, 40, "hbm", list(range(48, 55)))]}
+# truncated sessions (store.head_row > 0: the session's token 0 sits inside
+# its first block) in the batched K2 launch, next to an aligned one
+LONG["varlen_head"] = [("a", 40, 17, "hbm", [0, 1, 2, 3], 5), ("b", 0, 23, "none", [4, 5]),
+                       ("c", 33, 9, "hbm", [6, 7, 8, 15], 11), ("d", 64, 31, "hbm", [9, 10, 11, 12, 13, 14])]
 MIXES.update(LONG)
-BT = {"mixed": 16, "varlen": 16, "varlen_vsrc128": 128, "varlen_long": 16}
+BT = {"mixed": 16, "varlen": 16, "varlen_vsrc128": 128, "varlen_long": 16, "varlen_head": 16}
 SETUP = {"varlen_long": dict(nb=66, max_new=320)}
 
 
@@ -58,22 +62,24 @@ def _jobs(shape, r, bt, rng, mix):
     specs = MIXES[mix]
     jobs = []
     elems = bt * shape.kv_bytes_per_token // 2
-    for sid, kept, n, src, bids in specs:
+    for sid, kept, n, src, bids, *rest in specs:
         ids = torch.as_tensor(rng.integers(0, shape.vocab, n))
         off = torch.as_tensor([b * elems for b in bids], dtype=torch.int64, device="cuda")
         jobs.append(Job(sid, ids, kept=kept, source=src, block_ids=bids, save=True,
-                        dev_block_off=off if src == "hbm" else None))
+                        dev_block_off=off if src == "hbm" else None,
+                        head=rest[0] if rest else 0))
     return jobs
 
 
-def _stored(shape, buf_bf16, bids, bt, rows):
-    """Pre-RoPE K/V rows [0, rows) of a block list, per layer, float64."""
+def _stored(shape, buf_bf16, bids, bt, rows, head=0):
+    """Pre-RoPE K/V rows [0, rows) of a block list (session token 0 at row
+    `head` of the first block), per layer, float64."""
     L, rb = shape.layers, shape.row_elems
     blk = bt * rb * L
     out = []
     for layer in range(L):
         rws = []
-        for t in range(rows):
+        for t in range(head, head + rows):
             b = bids[t // bt]
             base = b * blk + layer * bt * rb + (t % bt) * rb
             rws.append(buf_bf16[base:base + rb])
@@ -96,14 +102,14 @@ def test_batched_prefill_matches_oracle_and_single_runs(mix):
     for j in jobs:
         if j.kept:
             src = hbm if j.source == "hbm" else arena.buffer.view(torch.bfloat16)
-            caches[j.session_id] = _stored(shape, src, j.block_ids, bt, j.kept)
+            caches[j.session_id] = _stored(shape, src, j.block_ids, bt, j.kept, j.head)
     res = r.run(jobs, want_logits=True, batch=True)
     r.join()
     torch.cuda.synchronize()
     Runner.finalize(res)
     batched_saved = {j.session_id: _stored(shape, hbm if j.source == "hbm" else
                                            arena.buffer.view(torch.bfloat16),
-                                           j.block_ids, bt, j.kept + j.n_new)
+                                           j.block_ids, bt, j.kept + j.n_new, j.head)
                      for j in jobs}
     for j, o in zip(jobs, res):
         empty = [(np.zeros((0, shape.n_kv_heads, shape.head_dim)),) * 2] * shape.layers
@@ -122,7 +128,7 @@ def test_batched_prefill_matches_oracle_and_single_runs(mix):
         torch.cuda.synchronize()
         Runner.finalize(single)
         got = _stored(shape, hbm if j.source == "hbm" else arena.buffer.view(torch.bfloat16),
-                      j.block_ids, bt, j.kept + j.n_new)
+                      j.block_ids, bt, j.kept + j.n_new, j.head)
         for layer in range(shape.layers):
             for a, b in zip(got[layer], batched_saved[j.session_id][layer]):
                 assert np.allclose(a, b, rtol=1e-2, atol=1e-2), (j.session_id, layer)
