@@ -200,10 +200,26 @@ extern "C" int askv_save_layer(void* host_base, const int64_t* block_ids, int nb
 
 // K4 for a whole job: every layer's save in one call (the saver IO thread
 // otherwise pays ~5 runtime calls through ctypes per layer, which at 16 jobs x
-// 40 layers per batched pass made the host the bottleneck).  Per layer l:
-// wait ev_ready[l] (the loop's rope_new wrote the rows), optional timing event
-// ev_t0[l], the D2H / D2D segments of askv_save_layer, record ev_done[l] (the
-// write-buffer slot is free again), optional ev_t1[l]; then ev_last.
+// 40 layers per batched pass made the host the bottleneck).  Layers are saved
+// in groups of up to G (ASKV_SAVE_GROUP, default 8) whose write-buffer slots
+// sit at a constant stride: one 2-D DMA per block piece covers the group's
+// layers (host pitch = the block's layer chunk), so a 301-token turn moves
+// ~16 MB pieces instead of ~2 MB ones -- the link gives small D2H pieces far
+// less while the pre-loader's H2D runs (profiles/r02_link_probe.txt).  Per
+// group: wait ev_ready of its layers (the loop's rope_new wrote the rows),
+// the DMAs bracketed by its first layer's timing events ev_t0 / ev_t1 (the
+// other layers get zero-length intervals at the group's end), ev_done of
+// every layer in it (the slots are free again); then ev_last.
+static int save_group_knob() {
+  static int g = -1;
+  if (g < 0) {
+    const char* e = getenv("ASKV_SAVE_GROUP");
+    g = e ? atoi(e) : 8;
+    if (g < 1) g = 1;
+  }
+  return g;
+}
+
 extern "C" int askv_save_layers(void* host_base, const int64_t* block_ids, int nblocks,
                                 int64_t block_bytes, int64_t chunk_bytes, int layers,
                                 int block_tokens, int64_t row_bytes, int64_t first_token,
@@ -213,19 +229,64 @@ extern "C" int askv_save_layers(void* host_base, const int64_t* block_ids, int n
   clear_error();
   ASKV_REQUIRE(layers > 0 && src != nullptr, "save_layers: bad layers=%d", layers);
   cudaStream_t s = (cudaStream_t)stream;
-  for (int l = 0; l < layers; ++l) {
-    if (ev_ready && ev_ready[l]) {
-      const int rc = cuda_status(cudaStreamWaitEvent(s, (cudaEvent_t)ev_ready[l], 0),
-                                 "save_layers wait");
-      if (rc) return rc;
+  const int gmax = save_group_knob();
+  auto rec = [&](void* const* evs, int l) {
+    if (evs && evs[l]) cudaEventRecord((cudaEvent_t)evs[l], s);
+  };
+  for (int l0 = 0; l0 < layers;) {
+    // the group: consecutive layers whose sources are a constant stride apart
+    int l1 = l0 + 1;
+    const int64_t stride = l0 + 1 < layers ? static_cast<const char*>(src[l0 + 1]) -
+                                                 static_cast<const char*>(src[l0])
+                                           : 0;
+    while (l1 < layers && l1 - l0 < gmax && stride > 0 &&
+           static_cast<const char*>(src[l1]) - static_cast<const char*>(src[l1 - 1]) == stride)
+      ++l1;
+    for (int l = l0; l < l1; ++l) {
+      if (ev_ready && ev_ready[l]) {
+        const int rc = cuda_status(cudaStreamWaitEvent(s, (cudaEvent_t)ev_ready[l], 0),
+                                   "save_layers wait");
+        if (rc) return rc;
+      }
     }
-    if (ev_t0 && ev_t0[l]) cudaEventRecord((cudaEvent_t)ev_t0[l], s);
-    const int rc = askv_save_layer(host_base, block_ids, nblocks, block_bytes,
-                                   (int64_t)l * chunk_bytes, block_tokens, row_bytes,
-                                   first_token, n_tokens, src[l], stream,
-                                   ev_done ? ev_done[l] : nullptr);
-    if (rc) return rc;
-    if (ev_t1 && ev_t1[l]) cudaEventRecord((cudaEvent_t)ev_t1[l], s);
+    rec(ev_t0, l0);
+    if (l1 - l0 == 1) {
+      const int rc = askv_save_layer(host_base, block_ids, nblocks, block_bytes,
+                                     (int64_t)l0 * chunk_bytes, block_tokens, row_bytes,
+                                     first_token, n_tokens, src[l0], stream, nullptr);
+      if (rc) return rc;
+    } else {
+      ASKV_REQUIRE(n_tokens >= 0 && block_tokens > 0 && row_bytes > 0 && first_token >= 0,
+                   "save_layers: bad n_tokens=%d", n_tokens);
+      ASKV_REQUIRE((int64_t)(l1 - 1) * chunk_bytes + block_tokens * row_bytes <= block_bytes,
+                   "save_layers: layer chunk outside block");
+      const int64_t last = first_token + n_tokens;
+      ASKV_REQUIRE(n_tokens == 0 || (last + block_tokens - 1) / block_tokens <= nblocks,
+                   "save_layers: tokens need more than %d blocks", nblocks);
+      ASKV_REQUIRE(n_tokens == 0 || (host_base && block_ids), "save_layers: null pointer");
+      auto* hb = static_cast<char*>(host_base) + (int64_t)l0 * chunk_bytes;
+      auto* sb = static_cast<const char*>(src[l0]);
+      for (int64_t t = first_token; t < last;) {
+        const int64_t b = t / block_tokens;
+        const int64_t r = t - b * block_tokens;
+        int64_t cnt = block_tokens - r;
+        if (cnt > last - t) cnt = last - t;
+        ASKV_REQUIRE(block_ids[b] >= 0, "save_layers: negative block id");
+        const cudaError_t e = cudaMemcpy2DAsync(
+            hb + block_ids[b] * block_bytes + r * row_bytes, (size_t)chunk_bytes,
+            sb + (t - first_token) * row_bytes, (size_t)stride, (size_t)(cnt * row_bytes),
+            (size_t)(l1 - l0), cudaMemcpyDefault, s);
+        if (e != cudaSuccess) return cuda_status(e, "save_layers cudaMemcpy2DAsync");
+        t += cnt;
+      }
+    }
+    for (int l = l0; l < l1; ++l) rec(ev_done, l);
+    rec(ev_t1, l0);
+    for (int l = l0 + 1; l < l1; ++l) {  // zero-length intervals: the group's time is l0's
+      rec(ev_t0, l);
+      rec(ev_t1, l);
+    }
+    l0 = l1;
   }
   if (ev_last)
     return cuda_status(cudaEventRecord((cudaEvent_t)ev_last, s), "save_layers event record");
