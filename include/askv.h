@@ -156,11 +156,15 @@ int askv_save_layer(void* host_base, const int64_t* block_ids, int nblocks,
                     int64_t block_bytes, int64_t layer_off, int block_tokens,
                     int64_t row_bytes, int64_t first_token, int n_tokens, const void* src,
                     void* stream, void* done_event);
-/* K4 for all `layers` layers of a job in one call: layer l waits ev_ready[l]
- * (may be NULL), records ev_t0[l] / ev_t1[l] around its copy (timing, may be
- * NULL) and ev_done[l] after it; src[l] holds its n_tokens rows; ev_last is
- * recorded after the last layer.  Replaces: the per-layer save slots of
- * overlap.py:126-200 (one call instead of one per layer). */
+/* K4 for all `layers` layers of a job in one call: src[l] holds layer l's
+ * n_tokens rows.  Layers whose src are a constant stride apart are saved in
+ * groups (ASKV_SAVE_GROUP, default 8) as one 2-D DMA per block piece: a
+ * group waits every ev_ready[l] of its layers (may be NULL), brackets its
+ * DMAs with its first layer's ev_t0 / ev_t1 (timing, may be NULL; the other
+ * layers' pairs are recorded together after it, zero-length) and records
+ * each layer's ev_done after them; ev_last after the last group.  Replaces:
+ * the per-layer save slots of overlap.py:126-200 (one call instead of one
+ * per layer). */
 int askv_save_layers(void* host_base, const int64_t* block_ids, int nblocks, int64_t block_bytes,
                      int64_t chunk_bytes, int layers, int block_tokens, int64_t row_bytes,
                      int64_t first_token, int n_tokens, const void* const* src,
