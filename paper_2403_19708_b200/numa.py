@@ -2,10 +2,12 @@
 each with its pinned KV arena on its own GPU's NUMA node, so the pre-loader's
 H2D DMAs never cross the socket interconnect).
 
-The arena is an anonymous mapping bound to the node with mbind(MPOL_BIND)
-before any page is touched; page-locking it with cudaHostRegister then
-faults every page in on that node and makes it DMA-able like cudaHostAlloc
-memory.  No libnuma is needed (raw syscall through libc)."""
+The arena is an anonymous mapping given the node as its preferred node with
+mbind(MPOL_PREFERRED) before any page is touched; page-locking it with
+cudaHostRegister then faults every page in on that node (falling back to
+another node only if that one is full -- MPOL_BIND would have the kernel
+kill the process instead) and makes it DMA-able like cudaHostAlloc memory.
+No libnuma is needed (raw syscall through libc)."""
 
 from __future__ import annotations
 
@@ -14,8 +16,7 @@ import mmap
 import os
 import platform
 
-_MPOL_BIND = 2
-_MPOL_MF_STRICT = 1
+_MPOL_PREFERRED = 1
 _SYS_MBIND = {"x86_64": 237, "aarch64": 235}
 
 
@@ -52,8 +53,8 @@ def _mbind(addr: int, length: int, node: int) -> None:
     libc = ctypes.CDLL(None, use_errno=True)
     libc.syscall.restype = ctypes.c_long
     rc = libc.syscall(ctypes.c_long(nr), ctypes.c_void_p(addr), ctypes.c_ulong(length),
-                      ctypes.c_int(_MPOL_BIND), mask, ctypes.c_ulong(maxnode + 1),
-                      ctypes.c_uint(_MPOL_MF_STRICT))
+                      ctypes.c_int(_MPOL_PREFERRED), mask, ctypes.c_ulong(maxnode + 1),
+                      ctypes.c_uint(0))
     if rc != 0:
         e = ctypes.get_errno()
         raise OSError(e, f"mbind(node {node}): {os.strerror(e)}")
