@@ -8,6 +8,7 @@ S_buf is sized by the reference's preload_buffer_size (model.py:273-287) over
 the workload's hit turns.
 
     python -m paper_2403_19708_b200.serve --config c3 --shard 0 --of 8 --json out.json
+    python -m paper_2403_19708_b200.serve --config c3 --of 8 --load 8   # 8x the arrival rate
 
 Reports, for reuse and for the recompute comparator (Mode.RECOMPUTE):
 queue-inclusive p50 / p99 TTFT (sim.py:489), isolated prefill p50
@@ -75,6 +76,12 @@ def run(args) -> dict:
     wl = sim.workload_from_dict(raw, ids)
     if args.max_sessions:
         wl.sessions = wl.sessions[:args.max_sessions]
+    if args.load != 1.0:
+        # k x the reference's offered load: session starts and think times
+        # (the gaps between a session's generator arrivals, sim.py:493) / k
+        wl.sessions = [sim.Session(x.session_id, x.turns,
+                                   tuple(a / args.load for a in x.arrival_times))
+                       for x in wl.sessions]
     shape = model.shape(shape_name)
     tb = args.block_tokens
     bb = tb * shape.kv_bytes_per_token
@@ -107,6 +114,7 @@ def run(args) -> dict:
     cfg = sim.SimConfig(profile=prof0, tiers=tiers, block_bytes=bb,
                         batch_size=args.batch_size)
     out = {"config": args.config, "model": shape_name, "shard": [args.shard, args.of],
+           "load": args.load,
            "sessions": len(wl.sessions), "turns": sum(len(s.turns) for s in wl.sessions),
            "dram_bytes": eng.store.mem_capacity, "read_buffer_bytes": rb,
            "block_tokens": tb, "batch_size": args.batch_size,
@@ -168,6 +176,9 @@ def parse(argv=None):
     ap.add_argument("--shard", type=int, default=0)
     ap.add_argument("--of", type=int, default=1, help="session shards (ranks of a node)")
     ap.add_argument("--max-sessions", type=int, default=0)
+    ap.add_argument("--load", type=float, default=1.0,
+                    help="offered load relative to the reference workload: arrival "
+                         "times and think times divided by this factor")
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--dram-gb", type=float, default=96.0)
     ap.add_argument("--hbm-gb", type=float, default=0.0,
