@@ -1,18 +1,18 @@
-# Final round-2 sweep on the committed code: build, smoke, GPU tests,
+# Final round-2 sweep (rg_: after grouped saves, GQA K2 rows, rank-safe build) on the committed code: build, smoke, GPU tests,
 # sanitizers on the batched pass, benches (C3 default + reference arm, C2, C4,
 # C5 rank probe), launch list and full ncu captures of the batched step.
 set -x
 mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/rf_build.txt 2>&1
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/rf_smoke.txt 2>&1; echo "smoke rc=$?" >> gpurun_out/rf_rc.txt
-timeout 1500 python -m pytest tests -m gpu -x -q --timeout 600 > gpurun_out/rf_pytest.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/rf_rc.txt
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/rg_build.txt 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/rg_smoke.txt 2>&1; echo "smoke rc=$?" >> gpurun_out/rg_rc.txt
+timeout 1500 python -m pytest tests -m gpu -x -q --timeout 600 > gpurun_out/rg_pytest.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/rg_rc.txt
 for tool in racecheck synccheck memcheck; do
-  ASKV_ATTN_PAIR=1 timeout 900 compute-sanitizer --tool $tool python tools/sanitize_kernels.py --only batch > gpurun_out/rf_san_batch_$tool.txt 2>&1; echo "san $tool rc=$?" >> gpurun_out/rf_rc.txt
+  ASKV_ATTN_PAIR=1 timeout 900 compute-sanitizer --tool $tool python tools/sanitize_kernels.py --only batch > gpurun_out/rg_san_batch_$tool.txt 2>&1; echo "san $tool rc=$?" >> gpurun_out/rg_rc.txt
 done
-timeout 900 python bench.py > gpurun_out/rf_bench_c3.log 2>&1; echo "bench rc=$?" >> gpurun_out/rf_rc.txt
-timeout 600 python bench.py --impl reference > gpurun_out/rf_bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/rf_rc.txt
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/rf_launches_batch.csv python tools/step_profile.py --mode hbm --turns 16 --batch --no-profiler > gpurun_out/rf_l1.txt 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 82 -c 1 -o gpurun_out/rf_attn_full python tools/step_profile.py --mode hbm --turns 16 --batch --no-profiler > gpurun_out/rf_l2.txt 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:reembed -s 90 -c 1 -o gpurun_out/rf_reembed_full python tools/step_profile.py --mode hbm --turns 16 --batch --no-profiler > gpurun_out/rf_l3.txt 2>&1
-timeout 600 python tools/step_profile.py --mode hbm --turns 16 --batch > gpurun_out/rf_step_batch.json 2> gpurun_out/rf_step_batch.err
-for c in c2 c4 c5; do timeout 900 python bench.py --config $c --no-cpu-baseline > gpurun_out/rf_bench_$c.log 2>&1; echo "bench $c rc=$?" >> gpurun_out/rf_rc.txt; done
+timeout 900 python bench.py > gpurun_out/rg_bench_c3.log 2>&1; echo "bench rc=$?" >> gpurun_out/rg_rc.txt
+timeout 600 python bench.py --impl reference > gpurun_out/rg_bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/rg_rc.txt
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/rg_launches_batch.csv python tools/step_profile.py --mode hbm --turns 16 --batch --no-profiler > gpurun_out/rg_l1.txt 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 82 -c 1 -o gpurun_out/rg_attn_full python tools/step_profile.py --mode hbm --turns 16 --batch --no-profiler > gpurun_out/rg_l2.txt 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:reembed -s 90 -c 1 -o gpurun_out/rg_reembed_full python tools/step_profile.py --mode hbm --turns 16 --batch --no-profiler > gpurun_out/rg_l3.txt 2>&1
+timeout 600 python tools/step_profile.py --mode hbm --turns 16 --batch > gpurun_out/rg_step_batch.json 2> gpurun_out/rg_step_batch.err
+for c in c2 c4 c5; do timeout 900 python bench.py --config $c --no-cpu-baseline > gpurun_out/rg_bench_$c.log 2>&1; echo "bench $c rc=$?" >> gpurun_out/rg_rc.txt; done
