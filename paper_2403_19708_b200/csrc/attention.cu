@@ -75,9 +75,21 @@ __device__ __forceinline__ void launch_stamp_end(unsigned long long* st) {
 }
 
 // Quarters of the softmax exponentials evaluated on the FMA pipe (packed
-// cubic) instead of MUFU ex2 (build-time A/B knob; 1 = one quarter).
+// cubic) instead of MUFU ex2 (build-time A/B knob; 1 = one quarter), or an
+// explicit mask over the 8 pair slots of each 16 columns (ASKV_ATTN_POLY_MASK).
 #ifndef ASKV_ATTN_POLY_Q
 #define ASKV_ATTN_POLY_Q 1
+#endif
+#ifndef ASKV_ATTN_POLY_MASK
+#define ASKV_ATTN_POLY_MASK (0x11 * ((0xF0 >> ASKV_ATTN_POLY_Q) & 0xF))
+#endif
+// 1: off-diagonal tiles after a group's first skip the max pass (exps
+// against the running max, overflow past the lazy threshold detected from
+// the row sum / the polynomial lanes' max).  Same values as the max-first
+// order; +5.7 % on the batched pass's varlen launch (attn_varlen_trace, two
+// A/B pairs), neutral at single-launch shapes (attn_ab).  Build-time knob.
+#ifndef ASKV_ATTN_SUMCHECK
+#define ASKV_ATTN_SUMCHECK 1
 #endif
 
 constexpr int kBM = 128;  // query rows per tile (UMMA M)
@@ -253,6 +265,8 @@ struct Cfg {
   static constexpr int kSoftmaxRegs = ASKV_ATTN_SOFTMAX_REGS;
   static constexpr int kThreads = kSoftmaxRegs > 0 ? 384 : 352;
   static constexpr float kRescaleLog2 = 8.0f;
+  static constexpr float kRescaleLin = 256.0f;  // 2^kRescaleLog2
+  static constexpr int kPolyMask = ASKV_ATTN_POLY_MASK;
   static_assert(kSmemBytes <= 232448, "smem budget");
 };
 
@@ -588,35 +602,44 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
       tmem_wait_ld();
       const bool trace_t = threadIdx.x == 0 && t >= 2 && t < 18;
       if (trace_t) ATTN_TRACE(192 + 4 * (t - 2));
-      if (kMask) {
+      const float2 sl2v = make_float2(sl2, sl2);
+      float2 ls0 = make_float2(0.f, 0.f), ls1 = ls0, ls2 = ls0, ls3 = ls0;
+      // exps of the row against -neg_m, P (bf16 pairs) over the S columns
+      // already read, row sums into ls*; kTrack: max of the raw scores of the
+      // polynomial lanes into *pmax.  Pair slot (e / 2) % 8 of each 16 goes to
+      // the FMA pipe (packed cubic) when bit slot of kPolyMask is set, so MUFU
+      // and FMA share the load; masked tiles keep MUFU (exact zeros).
+      auto exps = [&](auto track_tag, float neg_m, float* pmax) {
+        constexpr bool kTrack = decltype(track_tag)::value;
+        const float2 negm2 = make_float2(neg_m, neg_m);
+        ls0 = ls1 = ls2 = ls3 = make_float2(0.f, 0.f);
+        float pm = -INFINITY;
 #pragma unroll
-        for (int e = 0; e < kBN; ++e) sr[e] = (e <= lim) ? sr[e] : 0xff800000u;  // -inf
-      }
-      float a0 = fmaxf(__uint_as_float(sr[0]), __uint_as_float(sr[1]));
-      float a1 = fmaxf(__uint_as_float(sr[2]), __uint_as_float(sr[3]));
-      float a2 = fmaxf(__uint_as_float(sr[4]), __uint_as_float(sr[5]));
-      float a3 = fmaxf(__uint_as_float(sr[6]), __uint_as_float(sr[7]));
+        for (int c = 0; c < kBN / 32; ++c) {
+          uint32_t pk[16];
 #pragma unroll
-      for (int e = 8; e < kBN; e += 8) {
-        a0 = fmax3(a0, __uint_as_float(sr[e + 0]), __uint_as_float(sr[e + 1]));
-        a1 = fmax3(a1, __uint_as_float(sr[e + 2]), __uint_as_float(sr[e + 3]));
-        a2 = fmax3(a2, __uint_as_float(sr[e + 4]), __uint_as_float(sr[e + 5]));
-        a3 = fmax3(a3, __uint_as_float(sr[e + 6]), __uint_as_float(sr[e + 7]));
-      }
-      const float m_tile = fmax3(fmax3(a0, a1, a2), a3, -INFINITY) * sl2;
-      const bool need = m_tile > m_acc + C::kRescaleLog2;
-      if (trace_t) ATTN_TRACE(193 + 4 * (t - 2));
-      if (t > 0) {
-        // Every PV's completion phase is consumed here (compute-sanitizer
-        // synccheck flags a phase nobody waits for).  Free: s_full of S(t) was
-        // committed after PV(t-1) was issued, and a commit tracks every earlier
-        // tcgen05 op of the issuing thread, so PV(t-1) is already complete.
-        mbar_wait(&o_full[w], (t - 1) & 1);
-      }
-      if (t == 0) {
-        if (need) m_acc = m_tile;
-      } else if (__any_sync(0xffffffffu, need)) {
-        // O_w holds this group's tiles < t (their last PV waited above): rescale in place
+          for (int e = 0; e < 32; e += 2) {
+            const int k = c * 32 + e;
+            const float2 x = ffma2(
+                make_float2(__uint_as_float(sr[k]), __uint_as_float(sr[k + 1])), sl2v, negm2);
+            const bool poly = !kMask && ((C::kPolyMask >> ((e >> 1) & 7)) & 1);
+            if (kTrack && poly) pm = fmax3(pm, __uint_as_float(sr[k]), __uint_as_float(sr[k + 1]));
+            const float2 pp = poly ? ex2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+            switch ((e >> 1) & 3) {
+              case 0: ls0 = fadd2(ls0, pp); break;
+              case 1: ls1 = fadd2(ls1, pp); break;
+              case 2: ls2 = fadd2(ls2, pp); break;
+              default: ls3 = fadd2(ls3, pp); break;
+            }
+            pk[e >> 1] = pack_bf16x2(pp.x, pp.y);
+          }
+          tmem_st16(t_s + c * 16, pk);
+        }
+        if (kTrack) *pmax = pm;
+      };
+      // O_w holds this group's tiles < t (their last PV complete): rescale it
+      // in place by 2^(m_acc - m_tile) where a row's max grew past the threshold
+      auto rescale = [&](float m_tile, bool need) {
         tc_fence_after();
         const float f = need ? ex2(m_acc - m_tile) : 1.f;
 #pragma unroll 1
@@ -632,31 +655,72 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
           l_acc *= f;
           m_acc = m_tile;
         }
-      }
-      const float neg_m = (m_acc == -INFINITY) ? 0.f : -m_acc;
-      const float2 sl2v = make_float2(sl2, sl2), negm2 = make_float2(neg_m, neg_m);
-      float2 ls0 = make_float2(0.f, 0.f), ls1 = ls0, ls2 = ls0, ls3 = ls0;
+      };
+      auto row_max = [&]() {
+        float a0 = fmaxf(__uint_as_float(sr[0]), __uint_as_float(sr[1]));
+        float a1 = fmaxf(__uint_as_float(sr[2]), __uint_as_float(sr[3]));
+        float a2 = fmaxf(__uint_as_float(sr[4]), __uint_as_float(sr[5]));
+        float a3 = fmaxf(__uint_as_float(sr[6]), __uint_as_float(sr[7]));
 #pragma unroll
-      for (int c = 0; c < kBN / 32; ++c) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const int k = c * 32 + e;
-          const float2 x = ffma2(make_float2(__uint_as_float(sr[k]), __uint_as_float(sr[k + 1])),
-                                 sl2v, negm2);
-          // a quarter of the exponentials go to the FMA pipe (packed cubic) so
-          // MUFU and FMA share the load; masked tiles keep MUFU (exact zeros)
-          const float2 pp = (!kMask && ((e >> 1) & 3) >= 4 - ASKV_ATTN_POLY_Q) ? ex2_poly2(x)
-                                                             : make_float2(ex2(x.x), ex2(x.y));
-          switch ((e >> 1) & 3) {
-            case 0: ls0 = fadd2(ls0, pp); break;
-            case 1: ls1 = fadd2(ls1, pp); break;
-            case 2: ls2 = fadd2(ls2, pp); break;
-            default: ls3 = fadd2(ls3, pp); break;
-          }
-          pk[e >> 1] = pack_bf16x2(pp.x, pp.y);
+        for (int e = 8; e < kBN; e += 8) {
+          a0 = fmax3(a0, __uint_as_float(sr[e + 0]), __uint_as_float(sr[e + 1]));
+          a1 = fmax3(a1, __uint_as_float(sr[e + 2]), __uint_as_float(sr[e + 3]));
+          a2 = fmax3(a2, __uint_as_float(sr[e + 4]), __uint_as_float(sr[e + 5]));
+          a3 = fmax3(a3, __uint_as_float(sr[e + 6]), __uint_as_float(sr[e + 7]));
         }
-        tmem_st16(t_s + c * 16, pk);  // P (bf16 pairs) over the S columns already read
+        return fmax3(fmax3(a0, a1, a2), a3, -INFINITY) * sl2;
+      };
+      // Every PV's completion phase is consumed (compute-sanitizer synccheck
+      // flags a phase nobody waits for).  Free: s_full of S(t) was committed
+      // after PV(t-1) was issued, and a commit tracks every earlier tcgen05 op
+      // of the issuing thread, so PV(t-1) is already complete.
+      auto consume_pv = [&] {
+        if (t > 0) mbar_wait(&o_full[w], (t - 1) & 1);
+      };
+      bool done = false;
+#if ASKV_ATTN_SUMCHECK
+      if (!kMask && t > 0 && __all_sync(0xffffffffu, m_acc > -INFINITY)) {
+        // No max pass: exps straight against m_acc.  A row needs the lazy
+        // rescale only if some exponent exceeds 2^kRescaleLog2; its MUFU lanes
+        // then push the row sum past 2^kRescaleLog2 (inf included) and its
+        // polynomial lanes are checked through their raw max.  Only then is
+        // the exact max taken and, if it crossed the threshold, the row
+        // rescaled and the tile redone -- the values the max-first order gives.
+        float pmax;
+        exps(std::true_type{}, -m_acc, &pmax);
+        const float2 la = fadd2(ls0, ls1), lb = fadd2(ls2, ls3);
+        const float lsum = (la.x + la.y) + (lb.x + lb.y);
+        const bool over = !(lsum <= C::kRescaleLin) ||
+                          pmax * sl2 > m_acc + C::kRescaleLog2;
+        if (trace_t) ATTN_TRACE(193 + 4 * (t - 2));
+        consume_pv();
+        if (__any_sync(0xffffffffu, over)) {
+          const float m_tile = row_max();
+          const bool need = m_tile > m_acc + C::kRescaleLog2;
+          if (__any_sync(0xffffffffu, need)) {
+            tmem_wait_st();  // the first pass's P stores land before the redo's
+            rescale(m_tile, need);
+            exps(std::false_type{}, -m_acc, nullptr);
+          }
+        }
+        done = true;
+      }
+#endif
+      if (!done) {
+        if (kMask) {
+#pragma unroll
+          for (int e = 0; e < kBN; ++e) sr[e] = (e <= lim) ? sr[e] : 0xff800000u;  // -inf
+        }
+        const float m_tile = row_max();
+        const bool need = m_tile > m_acc + C::kRescaleLog2;
+        if (trace_t) ATTN_TRACE(193 + 4 * (t - 2));
+        consume_pv();
+        if (t == 0) {
+          if (need) m_acc = m_tile;
+        } else if (__any_sync(0xffffffffu, need)) {
+          rescale(m_tile, need);
+        }
+        exps(std::false_type{}, (m_acc == -INFINITY) ? 0.f : -m_acc, nullptr);
       }
       const float2 la = fadd2(ls0, ls1), lb = fadd2(ls2, ls3);
       l_acc += (la.x + la.y) + (lb.x + lb.y);
