@@ -237,8 +237,14 @@ template <int HD, bool kAllowPair>
 struct Cfg {
   // K is consumed early (S) and V late (PV), so K gets the deeper ring when
   // two Q tiles take 64 KB of shared memory.
-  static constexpr int kKStages = 3;
-  static constexpr int kVStages = kAllowPair ? 2 : 3;
+#ifndef ASKV_ATTN_PAIR_KSTAGES  // build-time A/B knobs of the paired instance's rings
+#define ASKV_ATTN_PAIR_KSTAGES 3
+#endif
+#ifndef ASKV_ATTN_PAIR_VSTAGES
+#define ASKV_ATTN_PAIR_VSTAGES 2
+#endif
+  static constexpr int kKStages = kAllowPair ? ASKV_ATTN_PAIR_KSTAGES : 3;
+  static constexpr int kVStages = kAllowPair ? ASKV_ATTN_PAIR_VSTAGES : 3;
   static constexpr int kQTiles = kAllowPair ? 2 : 1;
   static constexpr int kChunks = HD / 64;
   static constexpr int kTileBytes = kBM * HD * 2;
