@@ -268,8 +268,26 @@ struct Cfg {
   // warpgroups (setmaxnreg).  The launch-bound cap for 11-12 warps is 168
   // registers, which spilled in the softmax (96 B/thread); with 224: no
   // spills, paired shapes -12 %, C3 -1 % (tools/kbench.py --batch 50)
-  static constexpr int kSoftmaxRegs = ASKV_ATTN_SOFTMAX_REGS;
-  static constexpr int kThreads = kSoftmaxRegs > 0 ? 384 : 352;
+#ifndef ASKV_ATTN_COLSPLIT
+#define ASKV_ATTN_COLSPLIT 0
+#endif
+  // Column-split softmax (paired instance, d = 128): each group's 128 x 128
+  // S tile is handled by two warpgroups, one per 64-column half (a thread =
+  // one TMEM lane x 64 columns).  The halves share the running row max, so
+  // they agree once per tile on whether a row needs the exact max (an OR
+  // barrier over the two warps of the same lanes) and keep partial row sums
+  // merged in the epilogue.  Halves the per-tile softmax latency that the
+  // two groups' S -> softmax -> PV chains are paced by.
+  static constexpr bool kCol = kAllowPair && HD == 128 && ASKV_ATTN_COLSPLIT;
+  static constexpr int kSmWarps = kCol ? 16 : 8;  // softmax warps; control warps follow
+  static constexpr int kCtl = kSmWarps;           // TMA Q + K, then MMA, TMA V, idle
+  static constexpr int kNC = kCol ? kBN / 2 : kBN;  // S columns per softmax thread
+#ifndef ASKV_ATTN_COL_REGS  // column split: softmax / control registers (sum <= 4 x 96)
+#define ASKV_ATTN_COL_REGS 112
+#endif
+  static constexpr int kSoftmaxRegs = kCol ? ASKV_ATTN_COL_REGS : ASKV_ATTN_SOFTMAX_REGS;
+  static constexpr int kCtlRegs = kCol ? 96 - 4 * (ASKV_ATTN_COL_REGS - 96) : 56;
+  static constexpr int kThreads = kCol ? 640 : (kSoftmaxRegs > 0 ? 384 : 352);
   static constexpr float kRescaleLog2 = 8.0f;
   static constexpr float kRescaleLin = 256.0f;  // 2^kRescaleLog2
   static constexpr int kPolyMask = ASKV_ATTN_POLY_MASK;
@@ -277,7 +295,7 @@ struct Cfg {
 };
 
 template <int HD, bool kAllowPair>
-__global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
+__global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v,
@@ -364,11 +382,12 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
   }
 
   if (n_tiles == 0) {  // empty split: neutral partials (CTA-uniform branch)
-    if (warp < 8) {
+    if (warp < C::kSmWarps) {
       const int r = threadIdx.x & 127;
-      const int g = paired ? (warp >> 2) : 0;
+      const int g = warp / (C::kSmWarps / 2);
+      const bool writer = !C::kCol || ((warp >> 2) & 1) == 0;  // one half of a row writes
       const int rows = g ? rows_b : rows_a;
-      if ((paired || warp < 4) && r < rows) {
+      if (writer && (paired || g == 0) && r < rows) {
         const int64_t row = (int64_t)split * n_new * p.hq + out_row(q0 + g * kBM + r);
         p.part_lse[row] = -INFINITY;
         float4* po = reinterpret_cast<float4*>(p.part_o + row * HD);
@@ -391,24 +410,24 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
     }
     for (int w = 0; w < 2; ++w) {
       mbar_init(&s_full[w], 1);
-      mbar_init(&p_full[w], 128);
+      mbar_init(&p_full[w], C::kCol ? 256 : 128);
       mbar_init(&o_full[w], 1);
     }
     fence_mbar_init();
   }
-  if (warp == 8) tmem_alloc(tmem_slot, C::kTmemCols);
+  if (warp == C::kCtl) tmem_alloc(tmem_slot, C::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) ATTN_TRACE(1);
   // kSoftmaxRegs > 0: each role branch resizes its registers first
-  // (4 x 32 x 56 + 8 x 32 x kSoftmaxRegs <= 64 K)
+  // (4 x 32 x kCtlRegs + kSmWarps x 32 x kSoftmaxRegs <= 64 K)
   auto shrink = [] {
-    if constexpr (C::kSoftmaxRegs > 0) setmaxnreg_dec<56>();
+    if constexpr (C::kSoftmaxRegs > 0) setmaxnreg_dec<C::kCtlRegs>();
   };
 
-  if (warp == 8) {
+  if (warp == C::kCtl) {
     // ------------------------------------------------------------ TMA producer
     shrink();
     if (lane == 0) {
@@ -455,7 +474,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
                            c * 64, kh, kv_row0 + (t_begin + jk) * kBN, pol_kv);
       }
     }
-  } else if (warp == 10) {
+  } else if (warp == C::kCtl + 2) {
     // ------------------------------------------------------------ TMA producer (V)
     shrink();
     if (lane == 0) {
@@ -488,7 +507,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
                            &v_full[st], c * 64, kh, vrow, pol_kv);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == C::kCtl + 1) {
     // ------------------------------------------------------------ MMA issuer
     shrink();
     if (lane == 0) {
@@ -497,25 +516,39 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
       const uint32_t sk = smem_u32(sK), sv = smem_u32(sV);
       mbar_wait(q_full, 0);
       ATTN_TRACE(2);
+      // Descriptors = base descriptor + (byte offset >> 4) in the start
+      // address field (every operand lies below 256 KB of shared memory), so
+      // the issuer keeps three bases live instead of a hoisted descriptor per
+      // (tile, k) -- the column-split instance gives this warp 32 registers.
+      const uint64_t dq = sdesc_sw128(smem_u32(sQ), 16, 1024);
+      const uint64_t dk = sdesc_sw128(sk, 16, 1024);
+      const uint64_t dv = sdesc_sw128(sv, kBN * 128, 1024);
       // S_w(j) = Q_w K_j^T into group w's S columns
       auto issue_s = [&](int w, int j) {
-        const uint32_t sq = smem_u32(sQ) + (paired ? w * C::kTileBytes : 0);
-        const uint32_t kb = sk + (j % C::kKStages) * C::kTileBytes;
+        const uint32_t qo = (paired ? w * C::kTileBytes : 0) >> 4;
+        const uint32_t ko = ((j % C::kKStages) * C::kTileBytes) >> 4;
+        uint64_t bq = dq + qo, bk = dk + ko;
+        asm volatile("" : "+l"(bq), "+l"(bk));  // per-k sums stay immediates, not hoisted
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
-          const uint32_t off = (k >> 2) * (kBM * 128) + (k & 3) * 32;
-          umma_bf16(tmem + C::col_s(w), sdesc_sw128(sq + off, 16, 1024),
-                    sdesc_sw128(kb + off, 16, 1024), idesc_s, k > 0);
+          const uint32_t off = ((k >> 2) * (kBM * 128) + (k & 3) * 32) >> 4;
+          umma_bf16(tmem + C::col_s(w), bq + off, bk + off, idesc_s, k > 0);
         }
         umma_commit(&s_full[w]);
       };
-      // O_w += P_w V_j, P read from group w's S columns in TMEM
+      // O_w += P_w V_j, P read from group w's S columns in TMEM (column
+      // split: keys 0-63 at columns 0-31, keys 64-127 at 64-95 -- each half
+      // writes its P over its own S columns)
       auto issue_pv = [&](int w, int j, bool first) {
-        const uint32_t vb = sv + (j % C::kVStages) * C::kTileBytes;
+        const uint32_t vo = ((j % C::kVStages) * C::kTileBytes) >> 4;
+        uint64_t bv = dv + vo;
+        uint32_t ta = tmem + C::col_s(w);
+        asm volatile("" : "+l"(bv), "+r"(ta));
 #pragma unroll
         for (int k = 0; k < kBN / 16; ++k)
-          umma_bf16_tmem_a(tmem + C::col_o(w), tmem + C::col_s(w) + k * 8,
-                           sdesc_sw128(vb + k * (16 * 128), kBN * 128, 1024), idesc_o,
+          umma_bf16_tmem_a(tmem + C::col_o(w),
+                           ta + (C::kCol ? 64 * (k >> 2) + (k & 3) * 8 : k * 8),
+                           bv + k * (16 * 128 / 16), idesc_o,
                            (!first) || (k > 0));
         umma_commit(&o_full[w]);
       };
@@ -581,14 +614,40 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
         }
       }
     }
-  } else if (warp < 8) {
+  } else if (warp < C::kSmWarps) {
     // ------------------------------------------------------------ softmax groups
     if constexpr (C::kSoftmaxRegs > 0) setmaxnreg_inc<C::kSoftmaxRegs>();
-    const int w = warp >> 2;
+    const int w = warp / (C::kSmWarps / 2);
+    const int hh = C::kCol ? (warp >> 2) & 1 : 0;  // column half (column split)
     const int r = (warp & 3) * 32 + lane;  // row in tile == TMEM lane
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t t_s = tmem + lane_off + C::col_s(w);
+    // this thread's kNC S columns (P over the first kNC / 2 of them) and O half
+    const uint32_t t_s = tmem + lane_off + C::col_s(w) + hh * C::kNC;
     const uint32_t t_o = tmem + lane_off + C::col_o(w);
+    const uint32_t t_oh = t_o + (C::kCol ? hh * (HD / 2) : 0);
+    // column split: the two warps holding the same TMEM lanes of a group
+    const uint32_t pair_bar = 1 + w * 4 + (warp & 3);
+    // does any row of this warp (or, column split, of its lane pair) see `v`
+    auto pair_any = [&](bool v) -> bool {
+      if constexpr (C::kCol) return named_bar_or(pair_bar, 64, v);
+      else return __any_sync(0xffffffffu, v);
+    };
+    // the row max over both halves (through a free S column of each half:
+    // columns kNC / 2.. are not P and S is not rewritten before p_full)
+    auto pair_max = [&](float m) -> float {
+      if constexpr (C::kCol) {
+        tmem_st2(t_s + C::kNC / 2, m, m);
+        tmem_wait_st();
+        tc_fence_before();
+        named_bar_sync(pair_bar, 64);
+        tc_fence_after();
+        float a, b;
+        tmem_ld2(tmem + lane_off + C::col_s(w) + (hh ^ 1) * C::kNC + C::kNC / 2, a, b);
+        return fmaxf(m, a);
+      } else {
+        return m;
+      }
+    };
     const int qt0 = q0 + (paired ? w * kBM : 0);  // first query of this group's tile
     const int row_limit = n_cached + tok(qt0 + r);
     const float sl2 = p.scale_log2;
@@ -601,9 +660,9 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
     // off-diagonal tile free of per-element selects.
     auto tile = [&](auto mask_tag, int t, int lim) {
       constexpr bool kMask = decltype(mask_tag)::value;
-      uint32_t sr[kBN];
+      uint32_t sr[C::kNC];
 #pragma unroll
-      for (int c = 0; c < kBN / 32; ++c)
+      for (int c = 0; c < C::kNC / 32; ++c)
         tmem_ld32_nowait(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
       tmem_wait_ld();
       const bool trace_t = threadIdx.x == 0 && t >= 2 && t < 18;
@@ -621,7 +680,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
         ls0 = ls1 = ls2 = ls3 = make_float2(0.f, 0.f);
         float pm = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < kBN / 32; ++c) {
+        for (int c = 0; c < C::kNC / 32; ++c) {
           uint32_t pk[16];
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
@@ -649,12 +708,12 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
         tc_fence_after();
         const float f = need ? ex2(m_acc - m_tile) : 1.f;
 #pragma unroll 1
-        for (int c = 0; c < HD / 32; ++c) {
+        for (int c = 0; c < (C::kCol ? HD / 2 : HD) / 32; ++c) {
           float ov[32];
-          tmem_ld32(t_o + c * 32, ov);
+          tmem_ld32(t_oh + c * 32, ov);
 #pragma unroll
           for (int e = 0; e < 32; ++e) ov[e] *= f;
-          tmem_st32(t_o + c * 32, ov);
+          tmem_st32(t_oh + c * 32, ov);
         }
         tmem_wait_st();
         if (need) {
@@ -668,7 +727,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
         float a2 = fmaxf(__uint_as_float(sr[4]), __uint_as_float(sr[5]));
         float a3 = fmaxf(__uint_as_float(sr[6]), __uint_as_float(sr[7]));
 #pragma unroll
-        for (int e = 8; e < kBN; e += 8) {
+        for (int e = 8; e < C::kNC; e += 8) {
           a0 = fmax3(a0, __uint_as_float(sr[e + 0]), __uint_as_float(sr[e + 1]));
           a1 = fmax3(a1, __uint_as_float(sr[e + 2]), __uint_as_float(sr[e + 3]));
           a2 = fmax3(a2, __uint_as_float(sr[e + 4]), __uint_as_float(sr[e + 5]));
@@ -700,8 +759,8 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
                           pmax * sl2 > m_acc + C::kRescaleLog2;
         if (trace_t) ATTN_TRACE(193 + 4 * (t - 2));
         consume_pv();
-        if (__any_sync(0xffffffffu, over)) {
-          const float m_tile = row_max();
+        if (pair_any(over)) {
+          const float m_tile = pair_max(row_max());
           const bool need = m_tile > m_acc + C::kRescaleLog2;
           if (__any_sync(0xffffffffu, need)) {
             tmem_wait_st();  // the first pass's P stores land before the redo's
@@ -715,9 +774,9 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
       if (!done) {
         if (kMask) {
 #pragma unroll
-          for (int e = 0; e < kBN; ++e) sr[e] = (e <= lim) ? sr[e] : 0xff800000u;  // -inf
+          for (int e = 0; e < C::kNC; ++e) sr[e] = (e <= lim) ? sr[e] : 0xff800000u;  // -inf
         }
-        const float m_tile = row_max();
+        const float m_tile = pair_max(row_max());
         const bool need = m_tile > m_acc + C::kRescaleLog2;
         if (trace_t) ATTN_TRACE(193 + 4 * (t - 2));
         consume_pv();
@@ -743,7 +802,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
       const int kbase = (t_begin + j) * kBN;
       // group-uniform: does any row of this tile see a masked column here?
       if (kbase + kBN - 1 > n_cached + tok(qt0))
-        tile(std::true_type{}, t, row_limit - kbase);
+        tile(std::true_type{}, t, row_limit - kbase - hh * C::kNC);
       else
         tile(std::false_type{}, t, 0);
       if (threadIdx.x == 0 && t < 28) ATTN_TRACE(9 + 2 * t);
@@ -758,7 +817,40 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
     // ---- epilogue
     float m_fin = m_acc, l_fin = l_acc, f_self = l_acc > 0.f ? 1.f : 0.f, f_other = 0.f;
     int col0 = 0, ncols = HD;
-    if (!paired) {
+    if constexpr (C::kCol) {
+      // (m, partial l) of each half through a free S column (S / P are dead
+      // after the last PV); unpaired, the groups' (m, l) merge as below and a
+      // thread writes a quarter of the columns
+      tmem_st2(t_s + C::kNC / 2, m_acc, l_acc);
+      tmem_wait_st();
+      tc_fence_before();
+      named_bar_sync(9, 32 * C::kSmWarps);
+      tc_fence_after();
+      float mg[2], lg[2];
+      for (int g = 0; g < (paired ? 1 : 2); ++g) {
+        const int gg = paired ? w : g;
+        float m0, l0, m1, l1;
+        tmem_ld2(tmem + lane_off + C::col_s(gg) + C::kNC / 2, m0, l0);
+        tmem_ld2(tmem + lane_off + C::col_s(gg) + C::kNC + C::kNC / 2, m1, l1);
+        mg[g] = m0;
+        lg[g] = l0 + l1;
+      }
+      if (paired) {
+        l_fin = lg[0];
+        f_self = l_fin > 0.f ? 1.f : 0.f;
+        col0 = hh * (HD / 2);
+        ncols = HD / 2;
+      } else {
+        m_fin = fmaxf(mg[0], mg[1]);
+        const float f0 = lg[0] > 0.f ? ex2(mg[0] - m_fin) : 0.f;
+        const float f1 = lg[1] > 0.f ? ex2(mg[1] - m_fin) : 0.f;
+        l_fin = lg[0] * f0 + lg[1] * f1;
+        f_self = w ? f1 : f0;
+        f_other = w ? f0 : f1;
+        col0 = (w * 2 + hh) * (HD / 4);
+        ncols = HD / 4;
+      }
+    } else if (!paired) {
       // merge the two groups' (m, l, O) through TMEM; each writes half the columns
       tmem_st2(t_s + 64, m_acc, l_acc);  // S columns are free after the last PV
       tmem_wait_st();
@@ -811,7 +903,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
 #pragma unroll
           for (int e = 0; e < 32; e += 4)
             po[e / 4] = make_float4(o[e], o[e + 1], o[e + 2], o[e + 3]);
-          if (c == 0 && (paired || w == 0))
+          if (c == 0 && col0 == 0)
             p.part_lse[row] = l_fin > 0.f ? m_fin + __log2f(l_fin) : -INFINITY;
         }
       }
@@ -822,7 +914,7 @@ __global__ void __launch_bounds__(ASKV_ATTN_SOFTMAX_REGS > 0 ? 384 : 352, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == C::kCtl) {
     tc_fence_after();
     tmem_dealloc(tmem, C::kTmemCols);
   }
@@ -1777,7 +1869,8 @@ int launch_varlen(const VarlenBatch& b, cudaStream_t stream, unsigned long long*
       J.out = static_cast<__nv_bfloat16*>(b.out[i]);
       ctas += J.q_groups * heads;
     }
-    kern<<<ctas, Cfg<HD, false>::kThreads, smem, stream>>>(mq, mk, mv, mvs, prm, vj);
+    kern<<<ctas, pair ? Cfg<HD, true>::kThreads : Cfg<HD, false>::kThreads, smem, stream>>>(
+        mq, mk, mv, mvs, prm, vj);
     rc = launch_status("attn_fwd varlen launch");
     if (rc) return rc;
   }
