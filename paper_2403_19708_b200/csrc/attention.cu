@@ -288,6 +288,10 @@ struct Cfg {
   static constexpr int kSoftmaxRegs = kCol ? ASKV_ATTN_COL_REGS : ASKV_ATTN_SOFTMAX_REGS;
   static constexpr int kCtlRegs = kCol ? 96 - 4 * (ASKV_ATTN_COL_REGS - 96) : 56;
   static constexpr int kThreads = kCol ? 640 : (kSoftmaxRegs > 0 ? 384 : 352);
+#ifndef ASKV_ATTN_WARP_ARRIVE  // P-ready barrier: one arrival per softmax warp (1) or per thread (0)
+#define ASKV_ATTN_WARP_ARRIVE 1
+#endif
+  static constexpr bool kWarpArrive = ASKV_ATTN_WARP_ARRIVE;
   static constexpr float kRescaleLog2 = 8.0f;
   static constexpr float kRescaleLin = 256.0f;  // 2^kRescaleLog2
   static constexpr int kPolyMask = ASKV_ATTN_POLY_MASK;
@@ -410,7 +414,7 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
     }
     for (int w = 0; w < 2; ++w) {
       mbar_init(&s_full[w], 1);
-      mbar_init(&p_full[w], C::kCol ? 256 : 128);
+      mbar_init(&p_full[w], (C::kCol ? 2 : 1) * (C::kWarpArrive ? 4 : 128));
       mbar_init(&o_full[w], 1);
     }
     fence_mbar_init();
@@ -792,7 +796,15 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
       if (trace_t) ATTN_TRACE(194 + 4 * (t - 2));
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&p_full[w]);
+      if constexpr (C::kWarpArrive) {
+        // one arrival per warp: the warp-collective wait::st above completed
+        // every lane's P stores; 4 instead of 128 arrivals on the barrier the
+        // MMA warp waits on
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[w]);
+      } else {
+        mbar_arrive(&p_full[w]);
+      }
     };
     for (int t = 0; t < my_tiles; ++t) {
       const int j = paired ? t : 2 * t + w;
