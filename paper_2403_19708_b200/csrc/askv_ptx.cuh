@@ -228,6 +228,14 @@ __device__ __forceinline__ void setmaxnreg_dec() {
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
+// One elected lane of the (converged) warp: true in exactly one lane.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t r;
+  asm volatile(
+      "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(r));
+  return r != 0;
+}
 // Named barrier that also ORs a predicate over its `count` threads.
 __device__ __forceinline__ bool named_bar_or(uint32_t id, uint32_t count, bool v) {
   uint32_t r;

@@ -91,6 +91,9 @@ __device__ __forceinline__ void launch_stamp_end(unsigned long long* st) {
 #ifndef ASKV_ATTN_SUMCHECK
 #define ASKV_ATTN_SUMCHECK 1
 #endif
+#ifndef ASKV_ATTN_PROBE  // pipeline probes, experiment builds only (see tile())
+#define ASKV_ATTN_PROBE 0
+#endif
 
 constexpr int kBM = 128;  // query rows per tile (UMMA M)
 constexpr int kBN = 128;  // key rows per tile (UMMA N of S, K of PV)
@@ -289,7 +292,7 @@ struct Cfg {
   static constexpr int kCtlRegs = kCol ? 96 - 4 * (ASKV_ATTN_COL_REGS - 96) : 56;
   static constexpr int kThreads = kCol ? 640 : (kSoftmaxRegs > 0 ? 384 : 352);
 #ifndef ASKV_ATTN_WARP_ARRIVE  // P-ready barrier: one arrival per softmax warp (1) or per thread (0)
-#define ASKV_ATTN_WARP_ARRIVE 1
+#define ASKV_ATTN_WARP_ARRIVE 0
 #endif
   static constexpr bool kWarpArrive = ASKV_ATTN_WARP_ARRIVE;
   static constexpr float kRescaleLog2 = 8.0f;
@@ -665,6 +668,25 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
     auto tile = [&](auto mask_tag, int t, int lim) {
       constexpr bool kMask = decltype(mask_tag)::value;
       uint32_t sr[C::kNC];
+#if ASKV_ATTN_PROBE > 0
+      // Pipeline probes (tools/attn_varlen_trace.cu only; the output is not
+      // attention): 1 = no softmax work at all, 2 = the S loads only.  They
+      // time the MMA / TMA pipeline of the real kernel without the softmax.
+      if (ASKV_ATTN_PROBE == 2) {
+#pragma unroll
+        for (int c = 0; c < C::kNC / 32; ++c)
+          tmem_ld32_nowait(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+        tmem_wait_ld();
+        uint32_t x = 0;
+#pragma unroll
+        for (int e = 0; e < C::kNC; ++e) x ^= sr[e];
+        if (x == 0x7fc00001u) l_acc += 1.f;  // keep the loads
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (!C::kWarpArrive || elect_one()) mbar_arrive(&p_full[w]);
+      return;
+#endif
 #pragma unroll
       for (int c = 0; c < C::kNC / 32; ++c)
         tmem_ld32_nowait(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
@@ -801,7 +823,7 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
         // every lane's P stores; 4 instead of 128 arrivals on the barrier the
         // MMA warp waits on
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[w]);
+        if (elect_one()) mbar_arrive(&p_full[w]);
       } else {
         mbar_arrive(&p_full[w]);
       }

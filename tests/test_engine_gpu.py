@@ -575,14 +575,30 @@ def test_hbm_tier_with_evictions_is_bit_identical_to_host_path():
         e.arena.buffer.zero_()
         engs.append(e)
     rng = np.random.default_rng(16)
+    wnp = w.to_numpy()
     for k in range(5):
         for sid in ("a", "b", "c"):
             new_ids = torch.as_tensor(rng.integers(0, shape.vocab, 9 + k))
             out_ids = torch.as_tensor(rng.integers(0, shape.vocab, 6))
+            # the tier engine's stored rows before the turn (host DRAM backs the tier)
+            engs[1].runner.join()
+            torch.cuda.synchronize()
+            hist = engs[1].context.get(sid, 0)
+            before = session_cache(engs[1], sid, hist) if hist else None
             a, b = (e.turn(sid, k, new_ids, out_ids, want_logits=True) for e in engs)
             torch.cuda.synchronize()
             assert (a.kept, a.drop, a.hit) == (b.kept, b.drop, b.hit)
             assert torch.equal(a.result.logits, b.result.logits), (sid, k)
+            # and the oracle: kept stored rows re-embedded at 0..kept-1 (rope.py:118-144)
+            if b.kept:
+                cache = [(K[b.drop:], V[b.drop:]) for K, V in before]
+            else:
+                cache = [(np.zeros((0, shape.n_kv_heads, shape.head_dim)),) * 2] * shape.layers
+            want, _ = llama_ref.forward(wnp, new_ids.numpy(), cache, np.arange(b.kept),
+                                        n_heads=shape.n_heads, n_kv_heads=shape.n_kv_heads,
+                                        head_dim=shape.head_dim)
+            got = b.result.logits.cpu().numpy().astype(np.float64)
+            assert rope_ref.rel_err(got, want[-1]) <= LOGIT_TOL, (sid, k)
     for e in engs:
         e.runner.join()
     torch.cuda.synchronize()
