@@ -91,6 +91,9 @@ __device__ __forceinline__ void launch_stamp_end(unsigned long long* st) {
 #ifndef ASKV_ATTN_SUMCHECK
 #define ASKV_ATTN_SUMCHECK 1
 #endif
+#ifndef ASKV_ATTN_EARLY_VFREE  // paired: release a V slot right after its last PV
+#define ASKV_ATTN_EARLY_VFREE 1
+#endif
 #ifndef ASKV_ATTN_PROBE  // pipeline probes, experiment builds only (see tile())
 #define ASKV_ATTN_PROBE 0
 #endif
@@ -588,10 +591,18 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
             if (j < 28) ATTN_TRACE(96 + j);
             tc_fence_after();
             issue_pv(1, j, j == 0);
+#if ASKV_ATTN_EARLY_VFREE
+            // V(j)'s slot is free once PV_B(j) -- the last MMA reading it --
+            // completes: commit before S_B(j+1) so the V producer does not
+            // also wait for that S (B covers every tile of a paired CTA)
+            umma_commit(&v_empty[j % C::kVStages]);
+#endif
             if (j + 1 < nt_b) issue_s(1, j + 1);
             if (j < 28) ATTN_TRACE(160 + j);
           }
+#if !ASKV_ATTN_EARLY_VFREE
           umma_commit(&v_empty[j % C::kVStages]);
+#endif
           if (k_next) umma_commit(&k_empty[(j + 1) % C::kKStages]);
         }
       } else {
