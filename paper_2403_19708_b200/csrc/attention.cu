@@ -239,6 +239,15 @@ __host__ __device__ __forceinline__ Piece sk_piece(const AttnParams& p, int c, i
 #endif
 constexpr int kL2Prefetch = ASKV_ATTN_L2_PREFETCH;
 
+// L2 policy of the K/V tile loads: 1 = evict_last (keep for the head's other
+// query tiles), 2 = evict_first (streamed).  Build-time A/B knob.
+#ifndef ASKV_ATTN_KV_POLICY
+#define ASKV_ATTN_KV_POLICY 1
+#endif
+__device__ __forceinline__ uint64_t kv_policy() {
+  return ASKV_ATTN_KV_POLICY == 2 ? l2_policy_evict_first() : l2_policy_evict_last();
+}
+
 template <int HD, bool kAllowPair>
 struct Cfg {
   // K is consumed early (S) and V late (PV), so K gets the deeper ring when
@@ -447,7 +456,7 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
       tma_prefetch_desc(&tm_vs);
       // K/V tiles are re-read by every query tile of the head: keep them in L2
       // against streaming traffic (the pre-loader's DMA writes); Q is read once.
-      const uint64_t pol_kv = l2_policy_evict_last();
+      const uint64_t pol_kv = kv_policy();
       const uint64_t pol_q = l2_policy_evict_first();
       const int qt = paired ? 2 : 1;
       mbar_expect_tx(q_full, qt * C::kTileBytes);
@@ -488,7 +497,7 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
     // ------------------------------------------------------------ TMA producer (V)
     shrink();
     if (lane == 0) {
-      const uint64_t pol_kv = l2_policy_evict_last();
+      const uint64_t pol_kv = kv_policy();
       auto v_row = [&](int tv, bool vs) {
         return !vs ? kv_row0 + tv * kBN
                : v_blk_off ? (int)(v_blk_off[tv] / p.v_row_elems + v_layer_row)
