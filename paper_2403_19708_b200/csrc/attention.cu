@@ -307,6 +307,10 @@ struct Cfg {
 #define ASKV_ATTN_WARP_ARRIVE 0
 #endif
   static constexpr bool kWarpArrive = ASKV_ATTN_WARP_ARRIVE;
+#ifndef ASKV_ATTN_LAST_OFULL  // o_full committed by a group's last PV only (1) or by every PV (0)
+#define ASKV_ATTN_LAST_OFULL 1
+#endif
+  static constexpr bool kLastOFull = kAllowPair && ASKV_ATTN_LAST_OFULL;  // (the unpaired instance spills with it)
   static constexpr float kRescaleLog2 = 8.0f;
   static constexpr float kRescaleLin = 256.0f;  // 2^kRescaleLog2
   static constexpr int kPolyMask = ASKV_ATTN_POLY_MASK;
@@ -558,7 +562,10 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
       // O_w += P_w V_j, P read from group w's S columns in TMEM (column
       // split: keys 0-63 at columns 0-31, keys 64-127 at 64-95 -- each half
       // writes its P over its own S columns)
-      auto issue_pv = [&](int w, int j, bool first) {
+      // kLastOFull: only a group's last PV signals o_full (the epilogue's
+      // wait); an earlier PV's completion is implied by the s_full commit of
+      // the S issued after it, which is what the softmax waits for anyway
+      auto issue_pv = [&](int w, int j, bool first, bool last) {
         const uint32_t vo = ((j % C::kVStages) * C::kTileBytes) >> 4;
         uint64_t bv = dv + vo;
         uint32_t ta = tmem + C::col_s(w);
@@ -569,7 +576,7 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
                            ta + (C::kCol ? 64 * (k >> 2) + (k & 3) * 8 : k * 8),
                            bv + k * (16 * 128 / 16), idesc_o,
                            (!first) || (k > 0));
-        umma_commit(&o_full[w]);
+        if (!C::kLastOFull || last) umma_commit(&o_full[w]);
       };
       auto wait_k = [&](int j) {
         mbar_wait(&k_full[j % C::kKStages], (j / C::kKStages) & 1);
@@ -592,14 +599,14 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
             mbar_wait(&p_full[0], j & 1);
             if (j < 28) ATTN_TRACE(64 + j);
             tc_fence_after();
-            issue_pv(0, j, j == 0);
+            issue_pv(0, j, j == 0, j + 1 == nt_a);
             if (j + 1 < nt_a) issue_s(0, j + 1);
           }
           if (j < nt_b) {
             mbar_wait(&p_full[1], j & 1);
             if (j < 28) ATTN_TRACE(96 + j);
             tc_fence_after();
-            issue_pv(1, j, j == 0);
+            issue_pv(1, j, j == 0, j + 1 == nt_b);
 #if ASKV_ATTN_EARLY_VFREE
             // V(j)'s slot is free once PV_B(j) -- the last MMA reading it --
             // completes: commit before S_B(j+1) so the V producer does not
@@ -629,7 +636,7 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
           if (j < 28) ATTN_TRACE(64 + j);
           wait_v(j);
           if (j < 28) ATTN_TRACE(96 + j);
-          issue_pv(w, j, j < 2);
+          issue_pv(w, j, j < 2, j + 2 >= n_tiles);
           umma_commit(&v_empty[j % C::kVStages]);
           if (j < 28) ATTN_TRACE(160 + j);
           if (j + 2 < n_tiles) {
@@ -786,7 +793,7 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
       // after PV(t-1) was issued, and a commit tracks every earlier tcgen05 op
       // of the issuing thread, so PV(t-1) is already complete.
       auto consume_pv = [&] {
-        if (t > 0) mbar_wait(&o_full[w], (t - 1) & 1);
+        if (!C::kLastOFull && t > 0) mbar_wait(&o_full[w], (t - 1) & 1);
       };
       bool done = false;
 #if ASKV_ATTN_SUMCHECK
@@ -864,7 +871,7 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
       if (lane == 0 && w == 0 && (warp & 3) != 0 && t < 4) ATTN_TRACE(180 + 3 * t + (warp & 3) - 1);
     }
     if (my_tiles > 0) {  // this group's last PV
-      mbar_wait(&o_full[w], (my_tiles - 1) & 1);
+      mbar_wait(&o_full[w], C::kLastOFull ? 0 : (my_tiles - 1) & 1);
       tc_fence_after();
     }
     if (threadIdx.x == 0) ATTN_TRACE(3);
