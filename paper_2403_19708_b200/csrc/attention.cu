@@ -310,7 +310,10 @@ struct Cfg {
 #ifndef ASKV_ATTN_LAST_OFULL  // o_full committed by a group's last PV only (1) or by every PV (0)
 #define ASKV_ATTN_LAST_OFULL 1
 #endif
-  static constexpr bool kLastOFull = kAllowPair && ASKV_ATTN_LAST_OFULL;  // (the unpaired instance spills with it)
+#ifndef ASKV_ATTN_LAST_OFULL_ALL  // also in the unpaired instance (A/B knob)
+#define ASKV_ATTN_LAST_OFULL_ALL 0
+#endif
+  static constexpr bool kLastOFull = (kAllowPair || ASKV_ATTN_LAST_OFULL_ALL) && ASKV_ATTN_LAST_OFULL;  // (the unpaired instance spills with it)
   static constexpr float kRescaleLog2 = 8.0f;
   static constexpr float kRescaleLin = 256.0f;  // 2^kRescaleLog2
   static constexpr int kPolyMask = ASKV_ATTN_POLY_MASK;
