@@ -493,6 +493,12 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
               tma_prefetch_l2_3d(&tm_k, c * 64, kh, kv_row0 + (t_begin + jp) * kBN);
         }
         if (jk >= C::kKStages) mbar_wait(&k_empty[st], ((jk / C::kKStages) - 1) & 1);
+#if ASKV_ATTN_PROBE == 3
+        if (jk >= C::kKStages) {  // probe: no K loads after the ring's first fill
+          mbar_expect_tx(&k_full[st], 0);
+          continue;
+        }
+#endif
         mbar_expect_tx(&k_full[st], C::kTileBytes);
 #pragma unroll
         for (int c = 0; c < C::kChunks; ++c)
@@ -523,6 +529,12 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
           }
         }
         if (jv >= C::kVStages) mbar_wait(&v_empty[st], ((jv / C::kVStages) - 1) & 1);
+#if ASKV_ATTN_PROBE == 3
+        if (jv >= C::kVStages) {  // probe: no V loads after the ring's first fill
+          mbar_expect_tx(&v_full[st], 0);
+          continue;
+        }
+#endif
         mbar_expect_tx(&v_full[st], C::kTileBytes);
         const int tv = t_begin + jv;
         const bool vs = tv < v_src_tiles;
@@ -700,8 +712,10 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
       uint32_t sr[C::kNC];
 #if ASKV_ATTN_PROBE > 0
       // Pipeline probes (tools/attn_varlen_trace.cu only; the output is not
-      // attention): 1 = no softmax work at all, 2 = the S loads only.  They
-      // time the MMA / TMA pipeline of the real kernel without the softmax.
+      // attention): 1 = no softmax work at all, 2 = the S loads only, 3 = as
+      // 1 and no K/V loads after the rings' first fill (the producers arrive
+      // on the full barriers without a copy).  They time the MMA / TMA
+      // pipeline of the real kernel without the softmax.
       if (ASKV_ATTN_PROBE == 2) {
 #pragma unroll
         for (int c = 0; c < C::kNC / 32; ++c)
