@@ -143,3 +143,17 @@ def test_attention_kernel_does_not_spill(built):
             stacks[name] = int(m.group(1))
     assert len(stacks) == 6, stacks  # HD 64 / 128 x unpaired / paired / stream-K
     assert max(stacks.values()) <= 16, stacks
+
+
+def test_attention_build_knobs_default_to_the_measured_kernel():
+    """K3's build-time A/B knobs must default to the measured
+    product configuration: the experiment variants (pipeline probes, column
+    split, per-warp arrival, evict_first) are opt-in only."""
+    src = (ROOT / "paper_2403_19708_b200" / "csrc" / "attention.cu").read_text()
+    want = {"ASKV_ATTN_PROBE": "0", "ASKV_ATTN_COLSPLIT": "0", "ASKV_ATTN_WARP_ARRIVE": "0",
+            "ASKV_ATTN_LAST_OFULL": "1", "ASKV_ATTN_LAST_OFULL_ALL": "0",
+            "ASKV_ATTN_EARLY_VFREE": "1", "ASKV_ATTN_KV_POLICY": "1",
+            "ASKV_ATTN_SUMCHECK": "1", "ASKV_ATTN_POLY_Q": "1", "ASKV_ATTN_L2_PREFETCH": "0"}
+    for knob, val in want.items():
+        m = re.search(r"#define %s (\S+)" % knob, src)
+        assert m and m.group(1) == val, (knob, m and m.group(1))
