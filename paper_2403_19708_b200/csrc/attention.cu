@@ -91,6 +91,9 @@ __device__ __forceinline__ void launch_stamp_end(unsigned long long* st) {
 #ifndef ASKV_ATTN_SUMCHECK
 #define ASKV_ATTN_SUMCHECK 1
 #endif
+#ifndef ASKV_ATTN_INTERLEAVE  // paired: S_A(j+1) interleaved with PV_B(j) (A/B knob)
+#define ASKV_ATTN_INTERLEAVE 0
+#endif
 #ifndef ASKV_ATTN_EARLY_VFREE  // paired: release a V slot right after its last PV
 #define ASKV_ATTN_EARLY_VFREE 1
 #endif
@@ -610,6 +613,35 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
           wait_v(j);
           const bool k_next = j + 1 < n_tiles;
           if (k_next) wait_k(j + 1);
+#if ASKV_ATTN_INTERLEAVE
+          if (HD == kBN && j + 1 < nt_a) {  // (nt_a <= nt_b: B has PV(j) and S(j+1) too)
+            // PV_A(j), then S_A(j+1) k-steps interleaved with PV_B(j)'s: an
+            // S MMA reads 8 KB of shared memory, a PV 4 KB, so alternating
+            // them spreads the tensor core's shared-memory operand reads
+            mbar_wait(&p_full[0], j & 1);
+            tc_fence_after();
+            issue_pv(0, j, j == 0, false);
+            mbar_wait(&p_full[1], j & 1);
+            tc_fence_after();
+            uint64_t bq = dq, bk = dk + (((j + 1) % C::kKStages) * C::kTileBytes >> 4);
+            uint64_t bv = dv + ((j % C::kVStages) * C::kTileBytes >> 4);
+            uint32_t ta = tmem + C::col_s(1);
+            asm volatile("" : "+l"(bq), "+l"(bk), "+l"(bv), "+r"(ta));
+#pragma unroll
+            for (int k = 0; k < HD / 16; ++k) {
+              const uint32_t off = ((k >> 2) * (kBM * 128) + (k & 3) * 32) >> 4;
+              umma_bf16(tmem + C::col_s(0), bq + off, bk + off, idesc_s, k > 0);
+              if (k == HD / 16 - 1) umma_commit(&s_full[0]);
+              umma_bf16_tmem_a(tmem + C::col_o(1), ta + k * 8, bv + k * (16 * 128 / 16), idesc_o,
+                               j > 0 || k > 0);
+            }
+            if (!C::kLastOFull) umma_commit(&o_full[1]);
+            umma_commit(&v_empty[j % C::kVStages]);
+            if (j + 1 < nt_b) issue_s(1, j + 1);
+            if (k_next) umma_commit(&k_empty[(j + 1) % C::kKStages]);
+            continue;
+          }
+#endif
           if (j < nt_a) {
             mbar_wait(&p_full[0], j & 1);
             if (j < 28) ATTN_TRACE(64 + j);
