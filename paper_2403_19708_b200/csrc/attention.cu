@@ -837,10 +837,12 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
         }
         return fmax3(fmax3(a0, a1, a2), a3, -INFINITY) * sl2;
       };
-      // Every PV's completion phase is consumed (compute-sanitizer synccheck
-      // flags a phase nobody waits for).  Free: s_full of S(t) was committed
-      // after PV(t-1) was issued, and a commit tracks every earlier tcgen05 op
-      // of the issuing thread, so PV(t-1) is already complete.
+      // Every o_full phase is consumed (compute-sanitizer synccheck flags a
+      // phase nobody waits for): with kLastOFull there is one per group, the
+      // epilogue's; otherwise every PV commits one and it is waited here.
+      // Free either way: s_full of S(t) was committed after PV(t-1) was
+      // issued, and a commit tracks every earlier tcgen05 op of the issuing
+      // thread, so PV(t-1) is already complete.
       auto consume_pv = [&] {
         if (!C::kLastOFull && t > 0) mbar_wait(&o_full[w], (t - 1) & 1);
       };
