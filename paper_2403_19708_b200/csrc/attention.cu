@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
               tma_prefetch_l2_3d(&tm_k, c * 64, kh, kv_row0 + (t_begin + jp) * kBN);
         }
         if (jk >= C::kKStages) mbar_wait(&k_empty[st], ((jk / C::kKStages) - 1) & 1);
-#if ASKV_ATTN_PROBE == 3
+#if ASKV_ATTN_PROBE >= 3
         if (jk >= C::kKStages) {  // probe: no K loads after the ring's first fill
           mbar_expect_tx(&k_full[st], 0);
           continue;
@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
           }
         }
         if (jv >= C::kVStages) mbar_wait(&v_empty[st], ((jv / C::kVStages) - 1) & 1);
-#if ASKV_ATTN_PROBE == 3
+#if ASKV_ATTN_PROBE >= 3
         if (jv >= C::kVStages) {  // probe: no V loads after the ring's first fill
           mbar_expect_tx(&v_full[st], 0);
           continue;
@@ -597,10 +597,16 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
         if (!C::kLastOFull || last) umma_commit(&o_full[w]);
       };
       auto wait_k = [&](int j) {
+#if ASKV_ATTN_PROBE == 4  // probe: no ring waits after the first fill
+        if (j >= C::kKStages) return;
+#endif
         mbar_wait(&k_full[j % C::kKStages], (j / C::kKStages) & 1);
         tc_fence_after();
       };
       auto wait_v = [&](int j) {
+#if ASKV_ATTN_PROBE == 4
+        if (j >= C::kVStages) return;
+#endif
         mbar_wait(&v_full[j % C::kVStages], (j / C::kVStages) & 1);
         tc_fence_after();
       };
@@ -746,7 +752,8 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
       // Pipeline probes (tools/attn_varlen_trace.cu only; the output is not
       // attention): 1 = no softmax work at all, 2 = the S loads only, 3 = as
       // 1 and no K/V loads after the rings' first fill (the producers arrive
-      // on the full barriers without a copy).  They time the MMA / TMA
+      // on the full barriers without a copy), 4 = as 3 and the MMA warp does
+      // not wait on the ring barriers after the first fill.  They time the MMA / TMA
       // pipeline of the real kernel without the softmax.
       if (ASKV_ATTN_PROBE == 2) {
 #pragma unroll

@@ -149,7 +149,7 @@ int main() {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     for (int writers : {0, 4}) {
       for (int grid : {1, 148}) {
-        const int iters = 400;
+        const int iters = getenv("ITERS") ? atoi(getenv("ITERS")) : 400;
         kern<<<grid, 160, smem>>>(d, iters, writers);
         cudaError_t e = cudaDeviceSynchronize();
         if (e) {
