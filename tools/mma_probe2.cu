@@ -18,7 +18,7 @@
 using namespace askv;
 
 template <int MODE_>
-__global__ void probe(long long* out, int iters, int writers) {
+__global__ void probe(long long* out, int iters, int writers, int kmap) {
   constexpr int MODE = MODE_ >= 10 ? MODE_ - 10 : MODE_;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -39,7 +39,7 @@ __global__ void probe(long long* out, int iters, int writers) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = slot;
-  for (int i = threadIdx.x; i < 160 * 1024 / 4; i += blockDim.x)
+  for (int i = threadIdx.x; i < 224 * 1024 / 4; i += blockDim.x)
     ((uint32_t*)smem)[i] = 0x3c003c00u ^ (i * 2654435761u & 0x00ff00ffu);
   fence_proxy_async_smem();
   __syncthreads();
@@ -57,7 +57,10 @@ __global__ void probe(long long* out, int iters, int writers) {
         // cols [128, 256) with MODE 6: no alias); MODE 7: PV_a, S_a, PV_b, S_b
         // with two groups (a: S 0 / O 256, b: S 128 / O 384), MODE 8 = 7
         // reordered PV_a, PV_b, S_a, S_b
-        const uint32_t vt = sb + (it % 3) * 32768;
+        // KMAP=1: K3's paired shared-memory map -- Q_a at 0, Q_b at 32 KB,
+        // K ring at 64 KB (3 x 32 KB), V ring at 160 KB (2 x 32 KB)
+        const uint32_t vt = kmap ? sa + 163840 + (it % 2) * 32768 : sb + (it % 3) * 32768;
+        const uint32_t kt = kmap ? sa + 65536 + (it % 3) * 32768 : vt;
         auto pv = [&](uint32_t s_col, uint32_t o_col) {
           const uint32_t idp = idesc_bf16_f32(128, 128, 0, 1);
 #pragma unroll
@@ -69,12 +72,17 @@ __global__ void probe(long long* out, int iters, int writers) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
-            umma_bf16(tmem + s_col, sdesc_sw128(sa + off, 16, 1024),
-                      sdesc_sw128(vt + off, 16, 1024), idesc, k > 0);
+            const uint32_t qa = kmap && s_col ? sa + 32768 : sa;
+            umma_bf16(tmem + s_col, sdesc_sw128(qa + off, 16, 1024),
+                      sdesc_sw128(kt + off, 16, 1024), idesc, k > 0);
           }
         };
         if (MODE == 9) {  // = 7 with the kernel's commits (o_full, s_full, v_empty, k_empty)
+          // KMAP=2: also the kernel's handshake before each group -- a wait
+          // on an already completed mbarrier phase + tcgen05.fence::after_thread_sync
+          if (kmap == 2) { mbar_wait(&bar, 1); tc_fence_after(); }
           pv(0, 256); umma_commit(&cbar[0]); ss(0); umma_commit(&cbar[1]);
+          if (kmap == 2) { mbar_wait(&bar, 1); tc_fence_after(); }
           pv(128, 384); umma_commit(&cbar[2]); ss(128); umma_commit(&cbar[3]);
           umma_commit(&cbar[4]); umma_commit(&cbar[5]);
           continue;
@@ -139,7 +147,7 @@ __global__ void probe(long long* out, int iters, int writers) {
 int main() {
   long long* d;
   cudaMalloc(&d, 148 * sizeof(long long));
-  const int smem = 170 * 1024;
+  const int smem = 226 * 1024;
   const char* names[] = {"SS N=128 (S, kernel 1)", "SS N=64 (S, kernel 2)", "TS N=128 (PV)",
                          "SS N=256", "TS N=128 A=Q in TMEM (S)", "PV then S over P (alias)",
                          "PV then S, no alias", "PVa Sa PVb Sb (K3 paired)",
@@ -150,7 +158,7 @@ int main() {
     for (int writers : {0, 4}) {
       for (int grid : {1, 148}) {
         const int iters = getenv("ITERS") ? atoi(getenv("ITERS")) : 400;
-        kern<<<grid, 160, smem>>>(d, iters, writers);
+        kern<<<grid, 160, smem>>>(d, iters, writers, getenv("KMAP") ? atoi(getenv("KMAP")) : 0);
         cudaError_t e = cudaDeviceSynchronize();
         if (e) {
           printf("err %s\n", cudaGetErrorString(e));
