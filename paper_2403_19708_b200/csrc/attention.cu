@@ -91,6 +91,9 @@ __device__ __forceinline__ void launch_stamp_end(unsigned long long* st) {
 #ifndef ASKV_ATTN_SUMCHECK
 #define ASKV_ATTN_SUMCHECK 1
 #endif
+#ifndef ASKV_ATTN_ELECT_ISSUE  // MMA warp: warp-converged issue, lane elected in the asm
+#define ASKV_ATTN_ELECT_ISSUE 1
+#endif
 #ifndef ASKV_ATTN_INTERLEAVE  // paired: S_A(j+1) interleaved with PV_B(j) (A/B knob)
 #define ASKV_ATTN_INTERLEAVE 0
 #endif
@@ -316,6 +319,7 @@ struct Cfg {
 #ifndef ASKV_ATTN_LAST_OFULL_ALL  // also in the unpaired instance (A/B knob)
 #define ASKV_ATTN_LAST_OFULL_ALL 0
 #endif
+  static constexpr bool kElectIssue = ASKV_ATTN_ELECT_ISSUE;
   static constexpr bool kLastOFull = (kAllowPair || ASKV_ATTN_LAST_OFULL_ALL) && ASKV_ATTN_LAST_OFULL;  // (the unpaired instance spills with it)
   static constexpr float kRescaleLog2 = 8.0f;
   static constexpr float kRescaleLin = 256.0f;  // 2^kRescaleLog2
@@ -551,7 +555,21 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
   } else if (warp == C::kCtl + 1) {
     // ------------------------------------------------------------ MMA issuer
     shrink();
-    if (lane == 0) {
+    // kElectIssue: the whole warp runs the issue loop and each MMA / commit
+    // elects its issuing lane inside the asm (no per-instruction ELECT loop)
+    auto mma_ss = [](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+      if constexpr (C::kElectIssue) umma_bf16_el(d, a, b, id, acc);
+      else umma_bf16(d, a, b, id, acc);
+    };
+    auto mma_ts = [](uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
+      if constexpr (C::kElectIssue) umma_bf16_tmem_a_el(d, a, b, id, acc);
+      else umma_bf16_tmem_a(d, a, b, id, acc);
+    };
+    auto mma_commit = [](uint64_t* bar) {
+      if constexpr (C::kElectIssue) umma_commit_el(bar);
+      else umma_commit(bar);
+    };
+    if (C::kElectIssue || lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(kBM, kBN, 0, 0);
       constexpr uint32_t idesc_o = idesc_bf16_f32(kBM, HD, 0, 1);
       const uint32_t sk = smem_u32(sK), sv = smem_u32(sV);
@@ -573,9 +591,9 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
           const uint32_t off = ((k >> 2) * (kBM * 128) + (k & 3) * 32) >> 4;
-          umma_bf16(tmem + C::col_s(w), bq + off, bk + off, idesc_s, k > 0);
+          mma_ss(tmem + C::col_s(w), bq + off, bk + off, idesc_s, k > 0);
         }
-        umma_commit(&s_full[w]);
+        mma_commit(&s_full[w]);
       };
       // O_w += P_w V_j, P read from group w's S columns in TMEM (column
       // split: keys 0-63 at columns 0-31, keys 64-127 at 64-95 -- each half
@@ -590,11 +608,11 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
         asm volatile("" : "+l"(bv), "+r"(ta));
 #pragma unroll
         for (int k = 0; k < kBN / 16; ++k)
-          umma_bf16_tmem_a(tmem + C::col_o(w),
+          mma_ts(tmem + C::col_o(w),
                            ta + (C::kCol ? 64 * (k >> 2) + (k & 3) * 8 : k * 8),
                            bv + k * (16 * 128 / 16), idesc_o,
                            (!first) || (k > 0));
-        if (!C::kLastOFull || last) umma_commit(&o_full[w]);
+        if (!C::kLastOFull || last) mma_commit(&o_full[w]);
       };
       auto wait_k = [&](int j) {
 #if ASKV_ATTN_PROBE == 4  // probe: no ring waits after the first fill
@@ -614,7 +632,7 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
         wait_k(0);
         if (nt_a > 0) issue_s(0, 0);
         if (nt_b > 0) issue_s(1, 0);
-        umma_commit(&k_empty[0]);
+        mma_commit(&k_empty[0]);
         for (int j = 0; j < n_tiles; ++j) {
           wait_v(j);
           const bool k_next = j + 1 < n_tiles;
@@ -636,15 +654,15 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
 #pragma unroll
             for (int k = 0; k < HD / 16; ++k) {
               const uint32_t off = ((k >> 2) * (kBM * 128) + (k & 3) * 32) >> 4;
-              umma_bf16(tmem + C::col_s(0), bq + off, bk + off, idesc_s, k > 0);
-              if (k == HD / 16 - 1) umma_commit(&s_full[0]);
-              umma_bf16_tmem_a(tmem + C::col_o(1), ta + k * 8, bv + k * (16 * 128 / 16), idesc_o,
+              mma_ss(tmem + C::col_s(0), bq + off, bk + off, idesc_s, k > 0);
+              if (k == HD / 16 - 1) mma_commit(&s_full[0]);
+              mma_ts(tmem + C::col_o(1), ta + k * 8, bv + k * (16 * 128 / 16), idesc_o,
                                j > 0 || k > 0);
             }
-            if (!C::kLastOFull) umma_commit(&o_full[1]);
-            umma_commit(&v_empty[j % C::kVStages]);
+            if (!C::kLastOFull) mma_commit(&o_full[1]);
+            mma_commit(&v_empty[j % C::kVStages]);
             if (j + 1 < nt_b) issue_s(1, j + 1);
-            if (k_next) umma_commit(&k_empty[(j + 1) % C::kKStages]);
+            if (k_next) mma_commit(&k_empty[(j + 1) % C::kKStages]);
             continue;
           }
 #endif
@@ -664,24 +682,24 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
             // V(j)'s slot is free once PV_B(j) -- the last MMA reading it --
             // completes: commit before S_B(j+1) so the V producer does not
             // also wait for that S (B covers every tile of a paired CTA)
-            umma_commit(&v_empty[j % C::kVStages]);
+            mma_commit(&v_empty[j % C::kVStages]);
 #endif
             if (j + 1 < nt_b) issue_s(1, j + 1);
             if (j < 28) ATTN_TRACE(160 + j);
           }
 #if !ASKV_ATTN_EARLY_VFREE
-          umma_commit(&v_empty[j % C::kVStages]);
+          mma_commit(&v_empty[j % C::kVStages]);
 #endif
-          if (k_next) umma_commit(&k_empty[(j + 1) % C::kKStages]);
+          if (k_next) mma_commit(&k_empty[(j + 1) % C::kKStages]);
         }
       } else {
         wait_k(0);
         issue_s(0, 0);
-        umma_commit(&k_empty[0]);
+        mma_commit(&k_empty[0]);
         if (n_tiles > 1) {
           wait_k(1);
           issue_s(1, 1);
-          umma_commit(&k_empty[1]);
+          mma_commit(&k_empty[1]);
         }
         for (int j = 0; j < n_tiles; ++j) {
           const int w = j & 1;
@@ -690,13 +708,13 @@ __global__ void __launch_bounds__(Cfg<HD, kAllowPair>::kThreads, 1)
           wait_v(j);
           if (j < 28) ATTN_TRACE(96 + j);
           issue_pv(w, j, j < 2, j + 2 >= n_tiles);
-          umma_commit(&v_empty[j % C::kVStages]);
+          mma_commit(&v_empty[j % C::kVStages]);
           if (j < 28) ATTN_TRACE(160 + j);
           if (j + 2 < n_tiles) {
             wait_k(j + 2);
             if (j < 28) ATTN_TRACE(128 + j);
             issue_s(w, j + 2);
-            umma_commit(&k_empty[(j + 2) % C::kKStages]);
+            mma_commit(&k_empty[(j + 2) % C::kKStages]);
           }
         }
       }

@@ -152,7 +152,7 @@ def test_attention_build_knobs_default_to_the_measured_kernel():
     src = (ROOT / "paper_2403_19708_b200" / "csrc" / "attention.cu").read_text()
     want = {"ASKV_ATTN_PROBE": "0", "ASKV_ATTN_COLSPLIT": "0", "ASKV_ATTN_WARP_ARRIVE": "0",
             "ASKV_ATTN_LAST_OFULL": "1", "ASKV_ATTN_LAST_OFULL_ALL": "0",
-            "ASKV_ATTN_EARLY_VFREE": "1", "ASKV_ATTN_KV_POLICY": "1", "ASKV_ATTN_INTERLEAVE": "0",
+            "ASKV_ATTN_EARLY_VFREE": "1", "ASKV_ATTN_KV_POLICY": "1", "ASKV_ATTN_INTERLEAVE": "0", "ASKV_ATTN_ELECT_ISSUE": "1",
             "ASKV_ATTN_SUMCHECK": "1", "ASKV_ATTN_POLY_Q": "1", "ASKV_ATTN_L2_PREFETCH": "0"}
     for knob, val in want.items():
         m = re.search(r"#define %s (\S+)" % knob, src)
